@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Reshard throughput bench: GB/s of param+Adam state resharded.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+    python bench.py --impl reference ...      # CPU reference-algorithm arm
+
+One step = convert + load of every parameter of the workload (N=1 default:
+BASELINE configs[1], LLaMA-2-7B ZeRO-1 TP2/DP4 -> TP4/DP2, fp32 params + Adam
+m, v), with the source fragments of every source rank resident in HBM when
+the timed region starts. value = S / t_step, S = 12 B x numel. Under torchrun
+each rank owns an LPT share of the parameters (no data-path collective; the
+fragments a rank converts are already on it), value = total S / max-over-ranks
+step time.
+
+Extra keys: roofline (dominant kernel, algorithmic bytes / CUDA-event time vs
+MEASURED_PEAKS.json), e2e (host-streamed sample through pinned memory, H2D
+and D2H inside the timed region), cpu_baseline (oracle port of the reference
+algorithm on the host's cores, bounded sample), clocks, gpu_launches, parity
+(full-size on-device round-trip identities).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GB/s of param+Adam state resharded (1/2/4/8 B200, % HBM roofline) vs host CPU"
+GB = 1e9
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--layers", type=int, default=None, help="truncate the model (debug only)")
+    ap.add_argument("--window-gb", type=float, default=2.5)
+    ap.add_argument("--tile-kb", type=int, default=128)
+    ap.add_argument("--e2e-gb", type=float, default=24.0, help="pinned host budget of the e2e sample")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=os.cpu_count())
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=10)
+        rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        os.unlink(self.path)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[2:]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- helpers
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic_ratio(config: str):
+    """dram bytes / algorithmic bytes of the dominant kernel from the
+    committed ncu --set full summary (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(config) or d.get("default")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_reshard(spec, src, tgt, frags: dict, threads: int) -> float:
+    """The reference algorithm (oracle port) over a sample: union of every
+    (param, kind) unit, then extract_fragment of every target record of it,
+    materialised. Returns seconds."""
+    from oracle import ucp_oracle as O
+    from paper_2406_18820_b200.layout import all_rank_records
+
+    tgt_recs = all_rank_records(spec, tgt)
+    by_unit = {}
+    for g in range(tgt.world_size):
+        for m in tgt_recs[g]:
+            if (m.param, m.kind) in frags:
+                by_unit.setdefault((m.param, m.kind), []).append(m)
+
+    def unit(key):
+        p = spec.param(key[0])
+        full = O.union(p, src, frags[key], True)
+        for m in by_unit.get(key, ()):
+            O.extract(p, tgt, m, full).copy()
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        list(pool.map(unit, list(frags)))
+    return time.perf_counter() - t0
+
+
+def sample_params(spec, budget_state_bytes: float) -> list:
+    """First transformer layer(s) of the spec as the bounded CPU sample."""
+    names, acc = [], 0
+    for p in spec.params:
+        if p.name.startswith("layers."):
+            layer = int(p.name.split(".")[1])
+            if acc and (layer > 0 and acc + 12 * p.numel > budget_state_bytes):
+                break
+            names.append(p.name)
+            acc += 12 * p.numel
+    return names
+
+
+def oracle_frags(spec, src, names, threads):
+    """Source fragments of `names` generated on the CPU by the oracle
+    (reference arm input synthesis; outside the timed region)."""
+    from oracle import ucp_oracle as O
+    from paper_2406_18820_b200.layout import all_rank_records
+
+    recs = all_rank_records(spec, src)
+
+    def state(name):
+        p = spec.param(name)
+        w = O.gen_values(7, spec.tied_leader(name), "weight", p.shape)
+        m = O.gen_values(7, spec.tied_leader(name), "m", p.shape)
+        v = abs(O.gen_values(7, spec.tied_leader(name), "v", p.shape))
+        return name, {"weight": w, "m": m, "v": v}
+
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        st = dict(pool.map(state, names))
+    frags = {}
+    for g in range(src.world_size):
+        for m in recs[g]:
+            if m.param in st:
+                p = spec.param(m.param)
+                frags.setdefault((m.param, m.kind), []).append(
+                    (m, O.extract(p, src, m, st[m.param][m.kind]).copy()))
+    return frags
+
+
+def emit(obj, rank):
+    if rank == 0:
+        print(json.dumps(obj), flush=True)
+
+
+# --------------------------------------------------------------------------- arms
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    from paper_2406_18820_b200 import bench_config, format_config_string
+
+    spec, src, tgt, desc = bench_config(args.config, args.layers)
+    names = sample_params(spec, 3e9)
+    S = sum(12 * spec.param(n).numel for n in names)
+    frags = oracle_frags(spec, src, names, args.cpu_threads)
+    for _ in range(args.warmup):
+        cpu_reshard(spec, src, tgt, frags, args.cpu_threads)
+    times = [cpu_reshard(spec, src, tgt, frags, args.cpu_threads) for _ in range(args.steps)]
+    t = statistics.mean(times)
+    v = S / t / GB
+    sample = f"{len(names)} params ({names[0]} .. {names[-1]}), {S / GB:.2f} GB state"
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+          "data": "synthetic: reference generator init_state(seed=7), partitioned under src",
+          "config": {"workload": desc, "src": format_config_string(src),
+                     "tgt": format_config_string(tgt), "sample": sample},
+          "cpu_baseline": {"value": v, "unit": "GB/s", "cores": args.cpu_threads, "kind": "port",
+                           "sample": sample},
+          "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}},
+         0)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2406_18820_b200 import bench_config, format_config_string
+    from paper_2406_18820_b200.dist import init_process_group, owned_params
+    from paper_2406_18820_b200.reshard import ReshardPlan
+
+    rank, world, local = init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import torch.distributed as dist
+
+    spec, src, tgt, desc = bench_config(args.config, args.layers)
+    mine = owned_params(spec, rank, world) if world > 1 else None
+    plan = ReshardPlan(spec, src, tgt, params=mine, device=dev,
+                       window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024)
+    S_local = plan.state_bytes
+    plan.synthesize(7)
+    torch.cuda.synchronize()
+
+    parity = None
+    if not args.no_verify:
+        parity = plan.verify(7)
+        for k in ("atom_ref", "atom_back"):
+            plan._bufs.pop(k, None)
+        torch.cuda.empty_cache()
+        if not (parity["atomic_ok"] and parity["target_ok"] in (True, None)):
+            raise SystemExit(f"parity failure: {parity}")
+
+    stream = torch.cuda.current_stream()
+    plan.status.reset()
+    for _ in range(args.warmup):
+        plan.step_device(stream)
+    torch.cuda.synchronize()
+    plan.check()
+
+    nW = len(plan.windows)
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nW)]
+           for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for k in range(args.steps):
+        plan.step_device(stream, evs[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    plan.check()
+    ms_local = t0.elapsed_time(t1) / args.steps
+    conv_ms = sum(e[0].elapsed_time(e[1]) for st in evs for e in st) / args.steps
+    load_ms = sum(e[1].elapsed_time(e[2]) for st in evs for e in st) / args.steps
+
+    conv_bytes = plan.bytes["R_c"] + plan.bytes["W_c"]
+    load_bytes = plan.bytes["R_l"] + plan.bytes["W_l"]
+    if world > 1:
+        t = torch.tensor([ms_local, float(S_local)], device=dev, dtype=torch.float64)
+        mx = t.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        ms, S = float(mx[0]), float(t[1])
+    else:
+        ms, S = ms_local, float(S_local)
+    value = S / (ms / 1e3) / GB
+
+    peak, peak_src = measured_peak()
+    dom = "convert_gather" if conv_ms >= load_ms else "load_scatter"
+    dom_bytes, dom_ms = (conv_bytes, conv_ms) if dom == "convert_gather" else (load_bytes, load_ms)
+    launches = sum(1 for W in plan.windows if (W.conv if dom == "convert_gather" else W.load).n_tiles)
+    achieved = (dom_bytes / launches) / (dom_ms / launches / 1e3) / GB
+    ratio = ncu_traffic_ratio(args.config)
+    traffic = None
+    if ratio and ratio.get(dom):
+        traffic = ratio[dom] * dom_bytes / launches
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": dom,
+                "bytes_per_launch": dom_bytes / launches, "ms_per_launch": dom_ms / launches,
+                "launches_per_step": launches, "peak_source": peak_src,
+                "per_stage": {"convert_gather": {"ms": conv_ms, "hbm_bytes": conv_bytes,
+                                                 "GBps": conv_bytes / (conv_ms / 1e3) / GB,
+                                                 "frac": conv_bytes / (conv_ms / 1e3) / GB / peak},
+                              "load_scatter": {"ms": load_ms, "hbm_bytes": load_bytes,
+                                               "GBps": load_bytes / (load_ms / 1e3) / GB,
+                                               "frac": load_bytes / (load_ms / 1e3) / GB / peak},
+                              "step_hbm_frac": plan.hbm_bytes / (ms_local / 1e3) / GB / peak}}
+    gpu_launches = args.steps * plan.n_launches
+
+    # ---- e2e: host-streamed sample, H2D + kernels + D2H in the timed region
+    e2e = None
+    host_cpu_frags = None
+    cpu_names = None
+    if not args.no_e2e:
+        budget = args.e2e_gb * GB
+        wins, acc = [], 0
+        for W in plan.windows:
+            if wins and acc + W.src_bytes + W.tgt_bytes > budget:
+                break
+            wins.append(W)
+            acc += W.src_bytes + W.tgt_bytes
+        arena = plan._bufs["src_arena"]
+        s_lo, s_hi = wins[0].src_base, wins[-1].src_base + wins[-1].src_bytes
+        t_lo, t_hi = wins[0].tgt_base, wins[-1].tgt_base + wins[-1].tgt_bytes
+        host_src = torch.empty(s_hi - s_lo, dtype=torch.uint8, pin_memory=True)
+        host_tgt = torch.empty(t_hi - t_lo, dtype=torch.uint8, pin_memory=True)
+        host_src.copy_(arena[s_lo:s_hi])
+        if rank == 0 and world == 1 and not args.no_cpu:
+            cpu_names = [p.name for p in wins[-1].params]
+            hv = host_src.numpy()
+            host_cpu_frags = {}
+            for g, i, m, off, n in wins[-1].src_frags:
+                at = wins[-1].src_base - s_lo + off
+                a = hv[at:at + 4 * n].view("<f4").copy().reshape(m.shape)
+                host_cpu_frags.setdefault((m.param, m.kind), []).append((m, a))
+        for key in ("src_arena", "tgt0", "tgt1"):
+            plan._bufs.pop(key, None)
+        torch.cuda.empty_cache()
+        # stream_host indexes the host arenas by window base; shift views
+        import types
+
+        shifted = [types.SimpleNamespace(**{**W.__dict__, "src_base": W.src_base - s_lo,
+                                            "tgt_base": W.tgt_base - t_lo}) for W in wins]
+        streams = tuple(torch.cuda.Stream(dev) for _ in range(3))
+        plan.status.reset()
+        plan.stream_host(host_src, host_tgt, shifted, streams)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for s in streams:
+            s.wait_stream(stream)
+        for _ in range(args.e2e_steps):
+            plan.stream_host(host_src, host_tgt, shifted, streams)
+        for s in streams:
+            stream.wait_stream(s)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        S_e2e = sum(12 * p.numel for W in wins for p in W.params)
+        if world > 1:
+            t = torch.tensor([e2e_ms, float(S_e2e)], device=dev, dtype=torch.float64)
+            mx = t.clone()
+            dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+            e2e_ms, S_e2e = float(mx[0]), float(t[1])
+        e2e = {"value": S_e2e / (e2e_ms / 1e3) / GB, "unit": "GB/s",
+               "h2d_bytes_per_step": int(s_hi - s_lo), "d2h_bytes_per_step": int(t_hi - t_lo),
+               "ms_per_step": e2e_ms, "state_bytes_per_step": int(S_e2e),
+               "sample": f"windows 0..{len(wins) - 1} of {nW} ({S_e2e / GB:.2f} GB state/rank) "
+                         "from pinned host memory, H2D + convert + load + D2H, double-buffered"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        if host_cpu_frags is None:
+            cpu_names = sample_params(spec, 3e9)
+            host_cpu_frags = oracle_frags(spec, src, cpu_names, args.cpu_threads)
+        S_cpu = sum(12 * spec.param(n).numel for n in cpu_names)
+        t_cpu = cpu_reshard(spec, src, tgt, host_cpu_frags, args.cpu_threads)
+        cpu = {"value": S_cpu / t_cpu / GB, "unit": "GB/s", "cores": args.cpu_threads,
+               "kind": "port",
+               "sample": f"{len(cpu_names)} params ({cpu_names[0]} .. {cpu_names[-1]}), "
+                         f"{S_cpu / GB:.2f} GB state: oracle union + extract_fragment "
+                         f"(materialised), {args.cpu_threads} threads, one pass"}
+
+    emit({"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+          "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+          "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+          "data": "synthetic: reference generator init_state(seed=7) on GPU, partitioned "
+                  "under src by the same kernels (outside the timed region)",
+          "config": {"workload": desc, "config": args.config, "src": format_config_string(src),
+                     "tgt": format_config_string(tgt), "state_bytes": int(S),
+                     "hbm_bytes_per_step_rank0": int(plan.hbm_bytes),
+                     "bytes": {k: int(v) for k, v in plan.bytes.items()}, "windows": nW,
+                     "parallelism": f"param-sharded x{world}", "l2": "inputs larger than L2 "
+                     f"({plan.src_total / GB:.1f} GB source arena per rank)",
+                     "strict_replicate": True},
+          "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+          "gpu_launches": gpu_launches, "parity": parity}, rank)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/*
+ * ucp_b200.h -- C ABI of libucp_b200.so, the sm_100a data-movement engine
+ * behind the Universal Checkpointing reshard hot path.
+ *
+ * The reference (/root/reference/pkg/src/ucp) is pure Python + numpy and has no
+ * FFI; the entry points below are what its per-element work would bind to.
+ * Each one cites the reference function whose inner loop it replaces:
+ *
+ *   ucp_convert_gather  <- union()            ucp/convert.py:221-308
+ *                          _collapse_dp()      ucp/convert.py:137-193
+ *                          strip_pad()         ucp/convert.py:115-129
+ *                          _union_hy()         ucp/convert.py:196-218
+ *   ucp_load_scatter    <- extract_fragment()  ucp/parallel.py:373-411
+ *                          partial_noise()     ucp/parallel.py:340-370
+ *                          cast()              ucp/tensor.py:208-223 (load epilogue, ucp/load.py:204-205)
+ *   ucp_gen_state       <- hash_unit()/gen_tensor()  ucp/tensor.py:162-184, init_state() ucp/models.py:230-244
+ *
+ * Work is described by a host-compiled table of 2-D strided "runs" (see
+ * DESIGN.md §3). A run moves rows x cols f32 elements from n_src sources to
+ * n_dst destinations with one element-wise op. Sources are laid out
+ * group-major: source (g, k) is the k-th replica of group g; replicas must be
+ * bit-identical to replica 0 of their group (strict replica check), groups
+ * are averaged in f64 in ascending order (MEAN). The table is executed by a
+ * grid of one CTA per tile; tiles never straddle runs.
+ *
+ * Conventions: all pointers are device pointers, all calls are
+ * stream-ordered and reentrant (no global state besides the caller's status
+ * word). Return value is 0 or a negative UCP_E* code for argument / launch
+ * errors. Data-dependent failures (replica mismatch, nonzero pad) are
+ * reported asynchronously through ucp_status, read by the caller after the
+ * stream synchronises.
+ */
+#ifndef UCP_B200_H
+#define UCP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UCP_ABI_VERSION 1
+
+/* status / return codes (mirrored in paper_2406_18820_b200/_errors.py) */
+#define UCP_OK 0
+#define UCP_EREPLICA (-1)  /* ReplicateMismatchError */
+#define UCP_EPAD (-2)      /* PaddingError */
+#define UCP_EINVAL (-10)   /* bad argument / descriptor */
+#define UCP_ECUDA (-11)    /* CUDA launch or runtime error */
+
+/* run ops */
+#define UCP_OP_COPY 0      /* dst = src(g=0,k=0); replicas verified */
+#define UCP_OP_MEAN 1      /* dst = f32(sum_g f64(src(g,0)) / groups); replicas verified */
+#define UCP_OP_NOISE 2     /* dst = partial_noise(src, tp_rank, tp) */
+#define UCP_OP_ZERO 3      /* dst = +0.0 (ZeRO re-pad); n_src == 0 */
+#define UCP_OP_CHECKZERO 4 /* verify src bits == 0 (pad strip); n_dst == 0 */
+
+/* destination dtypes (UCPT dtype codes, ucp/tensor.py:43-59) */
+#define UCP_DT_F32 0
+#define UCP_DT_F16 1
+#define UCP_DT_BF16 2
+
+/* run flags */
+#define UCP_RUN_VEC 1u       /* every src/dst row start shares one 16-B phase */
+#define UCP_RUN_ROWSPLIT 2u  /* tiles cut columns of single rows */
+
+typedef struct ucp_run {
+  uint64_t src;        /* byte offset of source (0,0) from src_base, replica (0,0) */
+  uint64_t dst;        /* byte offset of destination 0's (0,0) from dst_base */
+  uint32_t src_pitch;  /* elements between source rows */
+  uint32_t dst_pitch;  /* elements between destination rows */
+  uint32_t rows;
+  uint32_t cols;       /* elements per row; rows*cols < 2^32 */
+  uint32_t aux;        /* index in aux[] of extra offsets: sources 1..n_src-1, then dsts 1..n_dst-1 */
+  uint16_t n_src;      /* groups * replicas-per-group (0 for ZERO) */
+  uint16_t n_dst;      /* fan-out (0 for CHECKZERO) */
+  uint16_t groups;     /* averaged groups (MEAN), else 1 */
+  uint8_t op;          /* UCP_OP_* */
+  uint8_t dtype;       /* UCP_DT_* of destinations; sources are always f32 */
+  uint16_t tp_rank;    /* NOISE */
+  uint16_t tp;         /* NOISE */
+  uint32_t tag;        /* caller's unit id, echoed in errors */
+  uint32_t flags;      /* UCP_RUN_* */
+  uint32_t pad_;
+} ucp_run;             /* 64 bytes */
+
+typedef struct ucp_tile {
+  uint32_t run;
+  uint32_t row0;
+  uint32_t col0;
+  uint32_t count;      /* rows (default) or cols (UCP_RUN_ROWSPLIT) */
+} ucp_tile;            /* 16 bytes */
+
+typedef struct ucp_status {
+  /* min over failures of (run index << 32 | element index in run); ~0 = ok */
+  unsigned long long first;
+  unsigned long long n_bad;  /* failing (warp, segment) reports, for stats */
+} ucp_status;
+
+/* Version of this ABI (UCP_ABI_VERSION). */
+int ucp_version(void);
+
+/* Reset a device status word to "no failure" (stream-ordered). */
+int ucp_status_reset(ucp_status* status, void* stream);
+
+/*
+ * Consolidate fragments into atomic tensors (union). One launch covers any
+ * number of (param, kind) units. src_base: base of the source-fragment arena;
+ * dst_base: base of the atomic arena. aux: n_aux uint64 byte offsets.
+ */
+int ucp_convert_gather(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
+                       const ucp_tile* tiles, int64_t n_tiles, const void* src_base,
+                       void* dst_base, ucp_status* status, void* stream);
+
+/*
+ * Slice atomic tensors into target fragments (extract_fragment + re-pad +
+ * partial noise + weight cast), fanning each read out to n_dst replicas.
+ */
+int ucp_load_scatter(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
+                     const ucp_tile* tiles, int64_t n_tiles, const void* src_base,
+                     void* dst_base, ucp_status* status, void* stream);
+
+/*
+ * Deterministic generator: out[i] = stream value start+i of stream `base`
+ * (stream_base(seed, name, tag) computed on the host), |.| if abs_flag.
+ * Bit-exact with ucp/tensor.py:162-171.
+ */
+int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, float* out,
+                  void* stream);
+
+/* Byte-compare two device buffers; *mismatch (device) receives the first
+ * differing byte index or ~0. Used by the checker paths of the bench. */
+int ucp_compare(const void* a, const void* b, uint64_t nbytes, unsigned long long* mismatch,
+                void* stream);
+
+/* Synchronous device->host copy of n bytes (error-path diagnostics: reading
+ * the replicas behind a failing run to name them in the exception). */
+int ucp_peek(const void* device_src, void* host_dst, uint64_t nbytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UCP_B200_H */

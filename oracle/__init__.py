@@ -1,0 +1,2 @@
+"""Test-infrastructure oracle (CPU restatement of the reference). Never
+imported by the product package; see ucp_oracle.py's header."""

@@ -1,0 +1,60 @@
+"""ctypes binding of libucp_b200.so (the C ABI in include/ucp_b200.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or
+``python -m paper_2406_18820_b200._build``). There is no fallback: if the
+library or a CUDA device is missing, every compute entry point raises
+:class:`NativeUnavailableError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from ._errors import NativeUnavailableError
+
+LIB_NAME = "libucp_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+# exported symbols declared in include/ucp_b200.h
+EXPORTS = ("ucp_version", "ucp_status_reset", "ucp_convert_gather", "ucp_load_scatter",
+           "ucp_gen_state", "ucp_compare", "ucp_peek")
+ABI_VERSION = 1
+
+_lib = None
+
+_c = ctypes
+_P = _c.c_void_p
+_SIGS = {
+    "ucp_version": (_c.c_int, []),
+    "ucp_status_reset": (_c.c_int, [_P, _P]),
+    "ucp_convert_gather": (_c.c_int, [_P, _c.c_int64, _P, _P, _c.c_int64, _P, _P, _P, _P]),
+    "ucp_load_scatter": (_c.c_int, [_P, _c.c_int64, _P, _P, _c.c_int64, _P, _P, _P, _P]),
+    "ucp_gen_state": (_c.c_int, [_c.c_uint64, _c.c_uint64, _c.c_uint64, _c.c_int, _P, _P]),
+    "ucp_compare": (_c.c_int, [_P, _P, _c.c_uint64, _P, _P]),
+    "ucp_peek": (_c.c_int, [_P, _P, _c.c_uint64]),
+}
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load and type the library (no CUDA device needed)."""
+    global _lib
+    if _lib is not None and path == LIB_PATH:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeUnavailableError(
+            f"{path} is missing; build it with __graft_entry__.build() (no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.ucp_version() != ABI_VERSION:
+        raise NativeUnavailableError(f"{path}: ABI {lib.ucp_version()} != {ABI_VERSION}")
+    if path == LIB_PATH:
+        _lib = lib
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    return load_library()

@@ -1,0 +1,707 @@
+"""The drop-in API: convert / load / resume / union / extract_fragment / ...
+
+Signatures, defaults, return types, raised classes and the statistics
+counters follow the reference package (ucp/convert.py:221-563,
+ucp/load.py:37-281, ucp/parallel.py:373-411, ucp/tensor.py:208-223,
+ucp/partition.py:151-174, ucp/models.py:230-244). Every element of every
+tensor on these paths is produced by libucp_b200.so on the GPU; the host does
+metadata validation, descriptor compilation and file I/O only.
+
+Keyword-only extensions: ``device=`` (CUDA device) and ``window_bytes=``
+(device staging budget per window).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+from collections import defaultdict
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import codec
+from ._errors import (
+    CheckpointLayoutError,
+    ManifestError,
+    MissingFragmentError,
+    ShapeError,
+    UnsupportedCastError,
+)
+from .engine import Arena, Program, Status, align_up, gen_state, require_device
+from .layout import (
+    all_rank_records,
+    enumerate_rank_records,
+    layer_of,
+    pp_layer_map,
+    validate_model_config,
+)
+from .plan import RunTable, compile_extract, compile_union, fragment_elems, fragment_shape
+from .spec import (
+    FORMAT_VERSION,
+    STATE_KINDS,
+    DType,
+    ModelSpec,
+    ParallelConfig,
+    ParamSpec,
+    RecordMeta,
+    Tensor,
+    make_tensor,
+    spec_to_json,
+)
+
+UCP_META_JSON = "ucp_meta.json"
+ATOMIC_FILES = {"weight": "weight.ucpt", "m": "adam_m.ucpt", "v": "adam_v.ucpt"}
+DEFAULT_WINDOW_BYTES = 2 << 30
+
+INVOCATIONS = 0
+
+
+def conversions_invoked() -> int:
+    """Process-wide count of convert() calls (ucp/convert.py:66-74)."""
+    return INVOCATIONS
+
+
+# --------------------------------------------------------------------------- types
+
+
+@dataclass(frozen=True)
+class FragmentMsg:
+    """One fragment in flight; data is a numpy array or a CUDA tensor."""
+
+    meta: RecordMeta
+    data: object
+
+
+@dataclass(frozen=True)
+class ParamState:
+    weight: Tensor
+    m: Tensor
+    v: Tensor
+
+
+@dataclass
+class ModelState:
+    spec: ModelSpec
+    params: dict
+    step: int
+    metadata: dict = field(default_factory=dict)
+
+
+@dataclass(frozen=True)
+class AtomicCheckpoint:
+    root: str
+    spec: ModelSpec
+    step: int
+    metadata: dict
+    source_fingerprint: str
+
+    def param_file(self, param: str, kind: str) -> str:
+        return os.path.join(self.root, param, ATOMIC_FILES[kind])
+
+    def read_param(self, param: str) -> dict:
+        p = self.spec.param(param)
+        out = {}
+        for kind in STATE_KINDS:
+            t = codec.read_tensor(self.param_file(param, kind))
+            if t.dtype is not DType.F32 or tuple(t.shape) != tuple(p.shape):
+                raise CheckpointLayoutError(
+                    f"{param}.{kind}: expected f32 {p.shape}, got {t.dtype.name} {t.shape}")
+            out[kind] = t
+        return out
+
+
+@dataclass(frozen=True)
+class WorldShard:
+    meta: RecordMeta
+    tensor: Tensor
+
+
+@dataclass
+class LoadStats:
+    bypass: bool = True
+    files_read: int = 0
+    bytes_read: int = 0
+    peak_resident_elements: int = 0
+    resident_bound: int = 0
+    conversions_invoked: int = 0
+    group_files_needed: dict = field(default_factory=dict)
+    group_files_read: dict = field(default_factory=dict)
+    per_rank: dict = field(default_factory=dict)
+
+    def to_dict(self) -> dict:
+        return {"bypass": self.bypass, "files_read": self.files_read,
+                "bytes_read": self.bytes_read,
+                "peak_resident_elements": self.peak_resident_elements,
+                "resident_bound": self.resident_bound,
+                "conversions_invoked": self.conversions_invoked,
+                "group_files_needed": self.group_files_needed,
+                "group_files_read": self.group_files_read,
+                "per_rank": {str(k): v for k, v in self.per_rank.items()}}
+
+
+@dataclass
+class LoadedWorld:
+    cfg: ParallelConfig
+    spec: ModelSpec
+    step: int
+    metadata: dict
+    shards: dict
+    stats: LoadStats
+
+
+@dataclass(frozen=True)
+class UcpInfo:
+    cfg: ParallelConfig
+    records: dict
+
+    def dp_group(self, g: int) -> str:
+        pp_r, tp_r, _ = self.cfg.coords_of(g)
+        return f"{pp_r},{tp_r}"
+
+    def replication_group(self, meta: RecordMeta) -> str:
+        pp_r, tp_r, dp_r = meta.placement
+        if meta.flat_range is not None:
+            return f"{meta.param}.{meta.kind}@{pp_r},{tp_r},{dp_r}"
+        return f"{meta.param}.{meta.kind}@{pp_r},{tp_r}"
+
+
+def ucp_info(spec: ModelSpec, cfg: ParallelConfig) -> UcpInfo:
+    validate_model_config(spec, cfg)
+    recs = all_rank_records(spec, cfg)
+    return UcpInfo(cfg, {g: list(recs[g]) for g in range(cfg.world_size)})
+
+
+# --------------------------------------------------------------------------- staging
+
+
+class _Staging:
+    """Grow-only pinned host + device buffers reused across API calls."""
+
+    def __init__(self):
+        self.host: dict = {}
+        self.dev: dict = {}
+
+    def host_buf(self, key: str, nbytes: int) -> torch.Tensor:
+        b = self.host.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(align_up(nbytes, 1 << 20), 1 << 20), dtype=torch.uint8,
+                            pin_memory=True)
+            self.host[key] = b
+        return b
+
+    def dev_buf(self, key: str, nbytes: int, device) -> torch.Tensor:
+        k = (key, str(device))
+        b = self.dev.get(k)
+        if b is None or b.numel() < nbytes:
+            self.dev.pop(k, None)
+            b = torch.empty(max(align_up(nbytes, 1 << 20), 1 << 20), dtype=torch.uint8,
+                            device=device)
+            self.dev[k] = b
+        return b
+
+
+_STAGE = _Staging()
+_STATUS: dict = {}
+
+
+def _status(dev) -> Status:
+    s = _STATUS.get(str(dev))
+    if s is None:
+        s = _STATUS[str(dev)] = Status(dev)
+    return s
+
+
+def _run(prog: Program, gather: bool, src_base: int, dst_base: int, dev) -> None:
+    st = _status(dev)
+    st.reset()
+    prog.launch(gather, src_base, dst_base, st)
+    torch.cuda.synchronize(dev)
+    st.raise_if_bad(prog, src_base)
+
+
+def _as_f32(data) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(data), dtype=np.float32)
+
+
+def _is_cuda(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+# --------------------------------------------------------------------------- primitives
+
+
+def union(p: ParamSpec, cfg: ParallelConfig, msgs: list, strict: bool = True):
+    """Reassemble one (param, kind) from its fragments on the GPU
+    (ucp/convert.py:221-308). numpy in -> numpy out; CUDA tensors in ->
+    CUDA tensor out (zero-copy sources)."""
+    if not msgs:
+        raise MissingFragmentError(f"{p.name}: no fragments at all")
+    on_dev = all(_is_cuda(m.data) for m in msgs)
+    dev = require_device(msgs[0].data.device if on_dev else None)
+    tab = RunTable()
+    if on_dev:
+        datas = [m.data.contiguous().float() for m in msgs]
+        frags = [(m.meta, d.data_ptr(), d.numel()) for m, d in zip(msgs, datas)]
+        src_base = 0
+    else:
+        arrays = [_as_f32(m.data) for m in msgs]
+        offs, at = [], 0
+        for a in arrays:
+            offs.append(at)
+            at += align_up(a.nbytes)
+        stage = _STAGE.dev_buf("union_src", at, dev)
+        for a, o in zip(arrays, offs):
+            if a.nbytes:
+                stage[o:o + a.nbytes].copy_(torch.from_numpy(a.reshape(-1).view(np.uint8)))
+        frags = [(m.meta, o, a.size) for m, a, o in zip(msgs, arrays, offs)]
+        src_base = stage.data_ptr()
+    compile_union(tab, p, cfg, frags, 0, strict)
+    out = torch.empty(max(p.numel, 1), dtype=torch.float32, device=dev)
+    prog = Program(tab, dev)
+    _run(prog, True, src_base, out.data_ptr(), dev)
+    out = out[:p.numel].view(tuple(p.shape))
+    return out if on_dev else out.cpu().numpy()
+
+
+def extract_fragment(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta, full):
+    """One rank's fragment of a consolidated f32 tensor, on the GPU
+    (ucp/parallel.py:373-411)."""
+    if tuple(full.shape) != tuple(p.shape):
+        raise ShapeError(f"{p.name}: expected {p.shape}, got {tuple(full.shape)}")
+    on_dev = _is_cuda(full)
+    dev = require_device(full.device if on_dev else None)
+    if on_dev:
+        src = full.contiguous().float()
+    else:
+        src = torch.from_numpy(_as_f32(full)).to(dev)
+    n = fragment_elems(p, cfg, meta)
+    out = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    tab = RunTable()
+    compile_extract(tab, p, cfg, [(meta, 0)], src.data_ptr(), DType.F32)
+    _run(Program(tab, dev), False, 0, out.data_ptr(), dev)
+    out = out[:n].view(fragment_shape(p, cfg, meta))
+    return out if on_dev else out.cpu().numpy()
+
+
+def cast(t: Tensor, to: DType) -> Tensor:
+    """RNE cast (ucp/tensor.py:208-223). f32 -> bf16/f16 runs on the GPU;
+    the widening directions are exact bit operations."""
+    if t.dtype is to:
+        return Tensor(to, t.shape, t.data)
+    if t.dtype is not DType.F32 and to is not DType.F32:
+        raise UnsupportedCastError(f"cannot cast {t.dtype.name} -> {to.name} directly")
+    if t.dtype is DType.F16:
+        return make_tensor(DType.F32, t.data.astype(np.float32).reshape(t.shape))
+    if t.dtype is DType.BF16:
+        wide = (t.data.astype(np.uint32) << np.uint32(16)).view(np.float32)
+        return make_tensor(DType.F32, wide.reshape(t.shape))
+    dev = require_device()
+    src = torch.from_numpy(_as_f32(t.data).reshape(-1)).to(dev)
+    out = torch.empty(max(t.numel, 1), dtype=torch.int16, device=dev)
+    tab = RunTable()
+    tab.unit("cast", "weight")
+    tab.add(srcs=[src.data_ptr()], dsts=[out.data_ptr()], src_pitch=t.numel, dst_pitch=t.numel,
+            rows=1, cols=t.numel, dtype=to, tag=0)
+    _run(Program(tab, dev), False, 0, 0, dev)
+    host = out[:t.numel].cpu().numpy().view(to.storage).reshape(t.shape)
+    return Tensor(to, tuple(t.shape), host)
+
+
+# --------------------------------------------------------------------------- atomic ckpt
+
+
+def source_fingerprint(src_root: str) -> str:
+    with open(os.path.join(src_root, codec.CONFIG_JSON), "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
+def load_atomic(root: str) -> AtomicCheckpoint:
+    mpath, upath = os.path.join(root, codec.MODEL_JSON), os.path.join(root, UCP_META_JSON)
+    if not (os.path.isfile(upath) and os.path.isfile(mpath)):
+        raise CheckpointLayoutError(f"{root!r} is not a complete atomic checkpoint (missing metadata)")
+    from .spec import spec_from_dict
+
+    with open(mpath) as f:
+        spec = spec_from_dict(json.load(f))
+    with open(upath) as f:
+        meta = json.load(f)
+    if meta.get("format_version") != FORMAT_VERSION:
+        raise CheckpointLayoutError(f"{root!r}: unsupported format_version {meta.get('format_version')}")
+    names = {p.name for p in spec.params}
+    have = {d for d in os.listdir(root) if os.path.isdir(os.path.join(root, d))}
+    if have != names:
+        raise CheckpointLayoutError(
+            f"{root!r}: param dirs disagree with model.json "
+            f"(missing {sorted(names - have)[:3]}, extra {sorted(have - names)[:3]})")
+    return AtomicCheckpoint(root, spec, int(meta["step"]), meta.get("metadata", {}),
+                            meta.get("source_config_sha256", ""))
+
+
+def _windows(items: list, size_of, budget: int) -> list:
+    """Greedy contiguous grouping under a byte budget (one oversized item
+    gets its own window)."""
+    out, cur, acc = [], [], 0
+    for it in items:
+        s = size_of(it)
+        if cur and acc + s > budget:
+            out.append(cur)
+            cur, acc = [], 0
+        cur.append(it)
+        acc += s
+    if cur:
+        out.append(cur)
+    return out
+
+
+def _io_pool(n_workers: int) -> ThreadPoolExecutor:
+    return ThreadPoolExecutor(max_workers=max(4, min(32, 2 * n_workers, os.cpu_count() or 4)))
+
+
+# --------------------------------------------------------------------------- convert
+
+
+def convert(src: str, out_dir: str, n_workers: int = 1, inner: int = 1,
+            strict_replicate: bool = True, *, device=None,
+            window_bytes: int = DEFAULT_WINDOW_BYTES) -> AtomicCheckpoint:
+    """Distributed checkpoint -> atomic checkpoint (ucp/convert.py:422-563).
+    Output bytes do not depend on n_workers/inner (they only size the file
+    I/O thread pool)."""
+    global INVOCATIONS
+    INVOCATIONS += 1
+    if n_workers < 1 or inner < 1:
+        raise ValueError("n_workers and inner must be >= 1")
+    ckpt = codec.load_checkpoint(src)
+    spec, cfg = ckpt.spec, ckpt.cfg
+    fingerprint = source_fingerprint(src)
+    dev = require_device(device)
+    codec.ensure_empty_dir(out_dir)
+
+    # mapper phase: manifests, stray/missing files, headers (ucp/convert.py:86-107)
+    units = defaultdict(list)
+    names = {p.name for p in spec.params}
+    for g in range(cfg.world_size):
+        rank_dir = ckpt.rank_dir(g)
+        _, records = codec.read_manifest(rank_dir)
+        listed = {m.file for m in records}
+        on_disk = {f for f in os.listdir(rank_dir) if f.endswith(".ucpt")}
+        if on_disk - listed:
+            raise ManifestError(
+                f"{rank_dir}: stray tensor files not in manifest: {sorted(on_disk - listed)[:3]}")
+        for meta in records:
+            path = os.path.join(rank_dir, meta.file)
+            if not os.path.isfile(path):
+                raise ManifestError(f"{rank_dir}: manifest lists missing file {meta.file}")
+            hdr = codec.read_header(path)
+            if hdr.dtype is not DType.F32:
+                raise ManifestError(f"{path}: expected f32 payload, got {hdr.dtype.name}")
+            if tuple(hdr.shape) != tuple(meta.shape):
+                raise ManifestError(f"{path}: shape {hdr.shape} disagrees with manifest {meta.shape}")
+            if meta.param not in names:
+                raise ManifestError(f"{path}: param {meta.param!r} not in model.json")
+            units[(meta.param, meta.kind)].append((meta, path, hdr))
+    missing = [p.name for p in spec.params if not any((p.name, k) in units for k in STATE_KINDS)]
+    if missing:
+        raise MissingFragmentError(f"no fragments at all for params {missing[:3]}")
+
+    def src_size(p):
+        return sum(align_up(h.nbytes) for k in STATE_KINDS for _, _, h in units.get((p.name, k), ()))
+
+    windows = _windows(list(spec.params), lambda p: src_size(p) + 3 * align_up(4 * p.numel),
+                       window_bytes)
+    st = _status(dev)
+    with _io_pool(n_workers) as pool:
+        for wparams in windows:
+            tab = RunTable()
+            jobs, s_at, a_at, outs = [], 0, 0, []
+            for p in wparams:
+                for kind in STATE_KINDS:
+                    items = units.get((p.name, kind))
+                    if not items:
+                        raise MissingFragmentError(f"{p.name}.{kind}: no fragments arrived")
+                    frags = []
+                    for meta, path, hdr in items:
+                        jobs.append((path, hdr, s_at))
+                        frags.append((meta, s_at, hdr.numel))
+                        s_at += align_up(hdr.nbytes)
+                    compile_union(tab, p, cfg, frags, a_at, strict_replicate)
+                    outs.append((p, kind, a_at))
+                    a_at += align_up(4 * p.numel)
+            h_src = _STAGE.host_buf("conv_src", s_at)
+            hv = memoryview(h_src.numpy())
+            list(pool.map(lambda j: codec.read_payload_into(j[0], j[1], hv[j[2]:j[2] + j[1].nbytes]),
+                          jobs))
+            d_src = _STAGE.dev_buf("conv_src", s_at, dev)
+            d_dst = _STAGE.dev_buf("conv_dst", a_at, dev)
+            d_src[:s_at].copy_(h_src[:s_at], non_blocking=True)
+            prog = Program(tab, dev)
+            st.reset()
+            prog.launch(True, d_src.data_ptr(), d_dst.data_ptr(), st)
+            h_dst = _STAGE.host_buf("conv_dst", a_at)
+            h_dst[:a_at].copy_(d_dst[:a_at], non_blocking=True)
+            torch.cuda.synchronize(dev)
+            st.raise_if_bad(prog, d_src.data_ptr())
+            ov = memoryview(h_dst.numpy())
+
+            def write(o):
+                p, kind, at = o
+                pdir = os.path.join(out_dir, p.name)
+                os.makedirs(pdir, exist_ok=True)
+                codec.write_raw(os.path.join(pdir, ATOMIC_FILES[kind]), DType.F32, p.shape,
+                                ov[at:at + 4 * p.numel])
+
+            list(pool.map(write, outs))
+
+    with open(os.path.join(out_dir, codec.MODEL_JSON), "w") as f:
+        f.write(spec_to_json(spec))
+    codec.write_json(os.path.join(out_dir, UCP_META_JSON), {
+        "format_version": FORMAT_VERSION, "step": ckpt.step, "metadata": ckpt.metadata,
+        "source_config_sha256": fingerprint})
+    return AtomicCheckpoint(out_dir, spec, ckpt.step, dict(ckpt.metadata), fingerprint)
+
+
+# --------------------------------------------------------------------------- load
+
+
+def _layer_groups(spec: ModelSpec) -> list:
+    by_layer: dict = {}
+    for p in spec.params:
+        by_layer.setdefault(layer_of(spec, p), []).append(p)
+    return sorted(by_layer.items())
+
+
+def resident_bound_elements(spec: ModelSpec, dp: int) -> int:
+    worst = 0
+    for _, params in _layer_groups(spec):
+        worst = max(worst, sum(3 * p.numel for p in params))
+    return dp * worst
+
+
+def _load_stats(atomic: AtomicCheckpoint, spec: ModelSpec, tgt: ParallelConfig,
+                bypass: bool) -> LoadStats:
+    """Logical read accounting with the reference's redundancy-bypass
+    assignment (ucp/load.py:164-214); the GPU path reads each file once."""
+    stats = LoadStats(bypass=bypass)
+    stats.resident_bound = resident_bound_elements(spec, tgt.dp)
+    stats.per_rank = {g: {"files_read": 0, "bytes_read": 0} for g in range(tgt.world_size)}
+    stage_of = {layer: s for s, layers in
+                enumerate(pp_layer_map(spec.n_layers, tgt.pp, tgt.pp_schedule)) for layer in layers}
+    resident = peak = 0
+    for layer, params in _layer_groups(spec):
+        s = stage_of[layer]
+        sized = sorted(((codec.payload_bytes_on_disk(atomic.param_file(p.name, k)), p, k)
+                        for p in params for k in STATE_KINDS),
+                       key=lambda x: (-x[0], x[1].name, x[2]))
+        for t in range(tgt.tp):
+            gkey = f"{s},{t}"
+            stats.group_files_needed[gkey] = stats.group_files_needed.get(gkey, 0) + len(sized)
+            members = [tgt.rank_of(s, t, d) for d in range(tgt.dp)]
+            layer_res = 0
+            for j, (nbytes, p, _) in enumerate(sized):
+                for g in ([members[j % tgt.dp]] if bypass else members):
+                    stats.files_read += 1
+                    stats.bytes_read += nbytes
+                    stats.group_files_read[gkey] = stats.group_files_read.get(gkey, 0) + 1
+                    stats.per_rank[g]["files_read"] += 1
+                    stats.per_rank[g]["bytes_read"] += nbytes
+                layer_res += p.numel * tgt.dp
+                resident += p.numel * tgt.dp
+                peak = max(peak, resident)
+            resident -= layer_res
+    stats.peak_resident_elements = peak
+    if peak > stats.resident_bound:
+        raise CheckpointLayoutError(f"loader exceeded its memory bound: {peak} > {stats.resident_bound}")
+    return stats
+
+
+def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass: bool = True,
+         *, device=None, window_bytes: int = DEFAULT_WINDOW_BYTES) -> LoadedWorld:
+    """Materialise every shard of a target world from an atomic checkpoint
+    (ucp/load.py:131-223). Weights are cast to dtype; moments stay f32."""
+    atomic = load_atomic(atomic_root)
+    spec = atomic.spec
+    validate_model_config(spec, tgt)
+    info = ucp_info(spec, tgt)
+    stats = _load_stats(atomic, spec, tgt, bypass)
+    dev = require_device(device)
+
+    by_unit = defaultdict(list)
+    for g in range(tgt.world_size):
+        for i, m in enumerate(info.records[g]):
+            by_unit[(m.param, m.kind)].append((g, i, m))
+    wdt = dtype
+
+    def out_dtype(kind):
+        return wdt if kind == "weight" else DType.F32
+
+    def tgt_bytes(p):
+        return sum(align_up(fragment_elems(p, tgt, m) * out_dtype(k).itemsize)
+                   for k in STATE_KINDS for _, _, m in by_unit.get((p.name, k), ()))
+
+    params = [p for _, ps in _layer_groups(spec) for p in ps]
+    windows = _windows(params, lambda p: 3 * align_up(4 * p.numel) + tgt_bytes(p), window_bytes)
+    filled: dict = {}
+    st = _status(dev)
+    with _io_pool(4) as pool:
+        for wparams in windows:
+            tab = RunTable()
+            jobs, s_at, t_at, outs = [], 0, 0, []
+            for p in wparams:
+                for kind in STATE_KINDS:
+                    path = atomic.param_file(p.name, kind)
+                    hdr = codec.read_header(path)
+                    if hdr.dtype is not DType.F32:
+                        raise CheckpointLayoutError(f"{path}: expected f32, got {hdr.dtype.name}")
+                    if tuple(hdr.shape) != tuple(p.shape):
+                        raise ShapeError(f"{p.name}: expected {p.shape}, got {hdr.shape}")
+                    jobs.append((path, hdr, s_at))
+                    targets = []
+                    odt = out_dtype(kind)
+                    for g, i, m in by_unit.get((p.name, kind), ()):
+                        n = fragment_elems(p, tgt, m)
+                        targets.append((m, t_at))
+                        outs.append((g, i, m, odt, t_at, n, fragment_shape(p, tgt, m)))
+                        t_at += align_up(n * odt.itemsize)
+                    compile_extract(tab, p, tgt, targets, s_at, odt)
+                    s_at += align_up(hdr.nbytes)
+            h_src = _STAGE.host_buf("load_src", s_at)
+            hv = memoryview(h_src.numpy())
+            list(pool.map(lambda j: codec.read_payload_into(j[0], j[1], hv[j[2]:j[2] + j[1].nbytes]),
+                          jobs))
+            d_src = _STAGE.dev_buf("load_src", s_at, dev)
+            d_dst = _STAGE.dev_buf("load_dst", t_at, dev)
+            d_src[:s_at].copy_(h_src[:s_at], non_blocking=True)
+            prog = Program(tab, dev)
+            st.reset()
+            prog.launch(False, d_src.data_ptr(), d_dst.data_ptr(), st)
+            host = np.empty(max(t_at, 1), dtype=np.uint8)
+            torch.from_numpy(host)[:t_at].copy_(d_dst[:t_at])
+            torch.cuda.synchronize(dev)
+            st.raise_if_bad(prog, d_src.data_ptr())
+            for g, i, m, odt, at, n, shape in outs:
+                arr = host[at:at + n * odt.itemsize].view(odt.storage).reshape(shape)
+                filled[(g, i)] = Tensor(odt, tuple(shape), arr)
+    shards = {g: [WorldShard(m, filled[(g, i)]) for i, m in enumerate(info.records[g])]
+              for g in range(tgt.world_size)}
+    return LoadedWorld(tgt, spec, atomic.step, dict(atomic.metadata), shards, stats)
+
+
+# --------------------------------------------------------------------------- resume
+
+
+def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1, inner: int = 1,
+           dtype: DType = DType.F32, bypass: bool = True) -> LoadedWorld:
+    """Reload a distributed checkpoint under tgt (ucp/load.py:231-281): lazy
+    direct read when the layouts match, else convert into scratch + load."""
+    src = codec.load_checkpoint(src_root)
+    validate_model_config(src.spec, tgt)
+    before = INVOCATIONS
+    if src.cfg == tgt:
+        stats = LoadStats(bypass=bypass)
+        stats.resident_bound = resident_bound_elements(src.spec, tgt.dp)
+        stats.per_rank = {g: {"files_read": 0, "bytes_read": 0} for g in range(tgt.world_size)}
+        shards = {}
+        for g in range(tgt.world_size):
+            rank_dir = src.rank_dir(g)
+            _, records = codec.read_manifest(rank_dir)
+            out = []
+            for meta in records:
+                path = os.path.join(rank_dir, meta.file)
+                t = codec.read_tensor(path)
+                nbytes = codec.payload_bytes_on_disk(path)
+                stats.files_read += 1
+                stats.bytes_read += nbytes
+                stats.per_rank[g]["files_read"] += 1
+                stats.per_rank[g]["bytes_read"] += nbytes
+                if meta.kind == "weight" and dtype is not DType.F32:
+                    t = cast(t, dtype)
+                out.append(WorldShard(meta, t))
+            shards[g] = out
+        stats.conversions_invoked = INVOCATIONS - before
+        return LoadedWorld(tgt, src.spec, src.step, dict(src.metadata), shards, stats)
+    os.makedirs(scratch, exist_ok=True)
+    atomic_dir = os.path.join(scratch, "atomic")
+    convert(src_root, atomic_dir, n_workers=n_workers, inner=inner)
+    world = load(atomic_dir, tgt, dtype=dtype, bypass=bypass)
+    world.stats.conversions_invoked = INVOCATIONS - before
+    return world
+
+
+# --------------------------------------------------------------------------- save side
+
+
+def init_state(spec: ModelSpec, seed: int, *, device=None) -> ModelState:
+    """Deterministic f32 state generated on the GPU (ucp/models.py:230-244,
+    generator ucp/tensor.py:116-184)."""
+    from .synth import stream_base
+
+    dev = require_device(device)
+    states: dict = {}
+    for p in spec.params:
+        lead = spec.tied_leader(p.name)
+        if lead != p.name:
+            states[p.name] = states[lead]
+            continue
+        buf = torch.empty(max(3 * p.numel, 1), dtype=torch.float32, device=dev)
+        for i, kind in enumerate(STATE_KINDS):
+            gen_state(stream_base(seed, p.name, kind), 0, p.numel, kind == "v",
+                      buf.data_ptr() + 4 * i * p.numel)
+        host = buf[:3 * p.numel].cpu().numpy()
+        ts = [Tensor(DType.F32, tuple(p.shape), host[i * p.numel:(i + 1) * p.numel].reshape(p.shape))
+              for i in range(3)]
+        states[p.name] = ParamState(*ts)
+    return ModelState(spec, states, 0, {"loss_scale": 1.0, "iteration": 0})
+
+
+def partition(state: ModelState, cfg: ParallelConfig, out_dir: str, workers: int = 1, *,
+              device=None) -> codec.DistributedCheckpoint:
+    """Write the distributed checkpoint of a consolidated state; the slicing
+    is the load_scatter kernel under the source config
+    (ucp/partition.py:125-174)."""
+    spec = state.spec
+    validate_model_config(spec, cfg)
+    dev = require_device(device)
+    codec.ensure_empty_dir(out_dir)
+    codec.write_json(os.path.join(out_dir, codec.CONFIG_JSON),
+                     codec.config_json_dict(cfg, state.step, state.metadata))
+    with open(os.path.join(out_dir, codec.MODEL_JSON), "w") as f:
+        f.write(spec_to_json(spec))
+    recs = all_rank_records(spec, cfg)
+    by_unit = defaultdict(list)
+    for g in range(cfg.world_size):
+        for m in recs[g]:
+            by_unit[(m.param, m.kind)].append((g, m))
+    files = []
+    for p in spec.params:
+        tab = RunTable()
+        full = torch.empty(max(3 * p.numel, 1), dtype=torch.float32, device=dev)
+        outs, at = [], 0
+        for i, kind in enumerate(STATE_KINDS):
+            data = np.ascontiguousarray(getattr(state.params[p.name], kind).data, dtype=np.float32)
+            if p.numel:
+                full[i * p.numel:(i + 1) * p.numel].copy_(torch.from_numpy(data.reshape(-1)))
+            targets = []
+            for g, m in by_unit.get((p.name, kind), ()):
+                n = fragment_elems(p, cfg, m)
+                targets.append((m, at))
+                outs.append((g, m, at, n))
+                at += align_up(4 * n)
+            compile_extract(tab, p, cfg, targets, full.data_ptr() + 4 * i * p.numel, DType.F32)
+        d_out = torch.empty(max(at, 1), dtype=torch.uint8, device=dev)
+        _run(Program(tab, dev), False, 0, d_out.data_ptr(), dev)
+        host = d_out.cpu().numpy()
+        for g, m, o, n in outs:
+            files.append((g, m, host[o:o + 4 * n]))
+    for g in range(cfg.world_size):
+        os.makedirs(os.path.join(out_dir, f"rank_{g}"), exist_ok=True)
+    with ThreadPoolExecutor(max_workers=max(1, workers)) as pool:
+        list(pool.map(lambda f: codec.write_raw(
+            os.path.join(out_dir, f"rank_{f[0]}", f[1].file), DType.F32, f[1].shape,
+            memoryview(f[2])), files))
+    for g in range(cfg.world_size):
+        codec.write_json(os.path.join(out_dir, f"rank_{g}", codec.MANIFEST),
+                         codec.manifest_dict(cfg, g, recs[g]))
+    return codec.DistributedCheckpoint(out_dir, cfg, spec, state.step, dict(state.metadata))

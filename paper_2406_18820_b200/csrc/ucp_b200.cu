@@ -1,0 +1,562 @@
+// libucp_b200.so -- sm_100a kernels + C ABI for the UCP reshard hot path.
+//
+// See include/ucp_b200.h for the ABI and DESIGN.md §3 for the descriptor
+// model. The path is pure data movement (HBM-bound): no tensor cores. Every
+// element-wise op reproduces the reference's numpy semantics bit for bit:
+//   * replica check: bitwise equality (ucp/convert.py:163-172, :270-278)
+//   * pad check: bitwise zero, so -0.0 fails (ucp/convert.py:127-128)
+//   * MEAN: f64 sum in ascending group order, f64 divide, RNE to f32
+//           (ucp/convert.py:279-284) -- __dadd_rn/__ddiv_rn/__double2float_rn
+//   * NOISE: repeated nextafterf by bit stepping + exact f64 pair check
+//           (ucp/parallel.py:340-370); no FTZ anywhere (built without fast math)
+//   * bf16 cast: (bits + 0x7FFF + lsb) >> 16, NaN quieted (ucp/tensor.py:192-201)
+//   * f16 cast: numpy's portable float->half bit algorithm (ucp/tensor.py:216)
+//   * generator: splitmix64 finaliser, top 24 bits (ucp/tensor.py:162-171)
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ucp_b200.h"
+
+static_assert(sizeof(ucp_run) == 64, "ucp_run must be 64 bytes");
+static_assert(sizeof(ucp_tile) == 16, "ucp_tile must be 16 bytes");
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kVec = 4;                  // 16-B vectors per lane per segment
+constexpr uint32_t kSeg = 32 * 4 * kVec;  // elements per warp segment (512)
+constexpr int kMaxAux = 256;             // host splits runs beyond this
+
+// ---------------------------------------------------------------- memory ops
+
+__device__ __forceinline__ float4 ld_stream4(const void* p) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float ld_stream1(const void* p) {
+  float r;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st4(void* p, float4 v) {
+  *reinterpret_cast<float4*>(p) = v;
+}
+
+// ---------------------------------------------------------------- bit ops
+
+__device__ __forceinline__ uint32_t bits_of(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ float float_of(uint32_t u) { return __uint_as_float(u); }
+
+// nextafterf(x, +inf) on bit patterns; NaN and +inf are fixed points
+__device__ __forceinline__ uint32_t step_up(uint32_t u) {
+  const uint32_t mag = u & 0x7fffffffu;
+  if (mag > 0x7f800000u || u == 0x7f800000u) return u;
+  if (mag == 0) return 1u;
+  return (u >> 31) ? u - 1u : u + 1u;
+}
+
+// nextafterf(x, -inf) on bit patterns; NaN and -inf are fixed points
+__device__ __forceinline__ uint32_t step_down(uint32_t u) {
+  const uint32_t mag = u & 0x7fffffffu;
+  if (mag > 0x7f800000u || u == 0xff800000u) return u;
+  if (mag == 0) return 0x80000001u;
+  return (u >> 31) ? u + 1u : u - 1u;
+}
+
+// partial_noise for one element (ucp/parallel.py:340-370)
+__device__ __forceinline__ float noise1(float x, int t, int tp) {
+  if (tp <= 1 || ((tp & 1) && t == tp - 1)) return x;
+  const uint32_t u = bits_of(x);
+  uint32_t hi = u, lo = u;
+  const int steps = t / 2 + 1;
+  for (int s = 0; s < steps; ++s) {
+    hi = step_up(hi);
+    lo = step_down(lo);
+  }
+  const bool finite = (u & 0x7f800000u) != 0x7f800000u;
+  const bool nonzero = (u & 0x7fffffffu) != 0u;
+  bool ok = false;
+  if (finite && nonzero) {
+    const double sum = __dadd_rn((double)float_of(hi), (double)float_of(lo));
+    const double twice = __dmul_rn(2.0, (double)x);
+    ok = (sum == twice);
+  }
+  if (!ok) return x;
+  return float_of((t & 1) ? lo : hi);
+}
+
+// f32 -> bf16 bits (ucp/tensor.py:192-201)
+__device__ __forceinline__ uint32_t bf16_bits(float x) {
+  const uint32_t u = bits_of(x);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return ((u >> 16) | 0x40u) & 0xffffu;
+  const uint32_t lsb = (u >> 16) & 1u;
+  return ((u + 0x7fffu + lsb) >> 16) & 0xffffu;
+}
+
+// f32 -> f16 bits, numpy's portable algorithm (RNE, overflow->inf, NaN
+// payload truncated and kept non-zero, signalling NaN not quieted)
+__device__ __forceinline__ uint32_t f16_bits(float x) {
+  const uint32_t f = bits_of(x);
+  const uint32_t sgn = (f & 0x80000000u) >> 16;
+  const uint32_t fexp = f & 0x7f800000u;
+  uint32_t fsig = f & 0x007fffffu;
+  if (fexp >= 0x47800000u) {
+    if (fexp == 0x7f800000u && fsig != 0u) {
+      uint32_t r = 0x7c00u + (fsig >> 13);
+      if (r == 0x7c00u) ++r;
+      return sgn + r;
+    }
+    return sgn + 0x7c00u;
+  }
+  if (fexp <= 0x38000000u) {
+    if (fexp < 0x33000000u) return sgn;
+    const uint32_t e = fexp >> 23;
+    uint32_t s = (0x00800000u + fsig) >> (113u - e);
+    if (((s & 0x3fffu) != 0x1000u) || (f & 0x7ffu)) s += 0x1000u;
+    return sgn + (s >> 13);
+  }
+  const uint32_t hexp = (fexp - 0x38000000u) >> 13;
+  if ((fsig & 0x3fffu) != 0x1000u) fsig += 0x1000u;
+  return sgn + hexp + (fsig >> 13);
+}
+
+__device__ __forceinline__ uint32_t cvt16(float x, int dtype) {
+  return dtype == UCP_DT_BF16 ? bf16_bits(x) : f16_bits(x);
+}
+
+// ---------------------------------------------------------------- helpers
+
+template <int W>
+struct Lanes {
+  float v[W];
+};
+
+template <int W>
+__device__ __forceinline__ void load_w(Lanes<W>& out, const char* p) {
+  if constexpr (W == 4) {
+    const float4 t = ld_stream4(p);
+    out.v[0] = t.x; out.v[1] = t.y; out.v[2] = t.z; out.v[3] = t.w;
+  } else {
+    out.v[0] = ld_stream1(p);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void store_w(char* p, const Lanes<W>& x, int dtype) {
+  if (dtype == UCP_DT_F32) {
+    if constexpr (W == 4) {
+      st4(p, make_float4(x.v[0], x.v[1], x.v[2], x.v[3]));
+    } else {
+      *reinterpret_cast<float*>(p) = x.v[0];
+    }
+  } else {
+    if constexpr (W == 4) {
+      uint2 h;
+      h.x = cvt16(x.v[0], dtype) | (cvt16(x.v[1], dtype) << 16);
+      h.y = cvt16(x.v[2], dtype) | (cvt16(x.v[3], dtype) << 16);
+      *reinterpret_cast<uint2*>(p) = h;
+    } else {
+      *reinterpret_cast<uint16_t*>(p) = (uint16_t)cvt16(x.v[0], dtype);
+    }
+  }
+}
+
+// first component index where a and b differ bitwise, or W
+template <int W>
+__device__ __forceinline__ int first_diff(const Lanes<W>& a, const Lanes<W>& b) {
+#pragma unroll
+  for (int i = 0; i < W; ++i)
+    if (bits_of(a.v[i]) != bits_of(b.v[i])) return i;
+  return W;
+}
+
+struct Ctx {
+  const ucp_run* r;
+  const uint64_t* aux;  // smem copy: sources 1.., then dsts 1..
+  const char* sb;
+  char* db;
+  uint32_t run_idx;
+};
+
+__device__ __forceinline__ uint64_t src_off(const Ctx& c, int i) {
+  return i == 0 ? c.r->src : c.aux[i - 1];
+}
+
+__device__ __forceinline__ uint64_t dst_off(const Ctx& c, int i) {
+  const int ns = c.r->n_src > 0 ? c.r->n_src - 1 : 0;
+  return i == 0 ? c.r->dst : c.aux[ns + i - 1];
+}
+
+// report the minimum failing element of this warp (all lanes call)
+__device__ __forceinline__ void report(bool bad, uint32_t elem, uint32_t run_idx,
+                                       ucp_status* st) {
+  const unsigned full = 0xffffffffu;
+  if (!__any_sync(full, bad)) return;
+  uint32_t e = bad ? elem : 0xffffffffu;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e = min(e, __shfl_xor_sync(full, e, o));
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long key = ((unsigned long long)run_idx << 32) | e;
+    atomicMin(&st->first, key);
+    atomicAdd(&st->n_bad, 1ull);
+  }
+}
+
+// COPY with replica verification, fan-out and cast, U slots of W elements.
+// e[u] = element offset inside the row segment; srow/drow = element index of
+// the segment start in source/destination coordinates.
+template <int W, int U>
+__device__ __forceinline__ void copy_general(const Ctx& c, uint64_t srow, uint64_t drow,
+                                             const uint32_t (&e)[U], const bool (&ok)[U],
+                                             uint32_t ebase, ucp_status* st) {
+  const ucp_run& r = *c.r;
+  const int esz = r.dtype == UCP_DT_F32 ? 4 : 2;
+  Lanes<W> v[U];
+  bool bad = false;
+  uint32_t bad_e = 0xffffffffu;
+  const char* s0 = c.sb + r.src + 4 * srow;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (ok[u]) load_w<W>(v[u], s0 + 4ull * e[u]);
+  for (int k = 1; k < r.n_src; ++k) {
+    const char* sk = c.sb + src_off(c, k) + 4 * srow;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) continue;
+      Lanes<W> w;
+      load_w<W>(w, sk + 4ull * e[u]);
+      const int d = first_diff<W>(v[u], w);
+      if (d < W) { bad = true; bad_e = min(bad_e, e[u] + d); }
+    }
+  }
+  for (int d = 0; d < r.n_dst; ++d) {
+    char* dp = c.db + dst_off(c, d) + (uint64_t)esz * drow;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) store_w<W>(dp + (uint64_t)esz * e[u], v[u], r.dtype);
+  }
+  report(bad, ebase + bad_e, c.run_idx, st);
+}
+
+// MEAN / NOISE / ZERO / CHECKZERO (tiny by bytes: Partial vectors, pads);
+// one slot at a time to keep register pressure off the copy paths.
+template <int W, int U>
+__device__ __noinline__ void op_general(const Ctx& c, uint64_t srow, uint64_t drow,
+                                        const uint32_t (&e)[U], const bool (&ok)[U],
+                                        uint32_t ebase, ucp_status* st) {
+  const ucp_run& r = *c.r;
+  const int op = r.op;
+  const int esz = r.dtype == UCP_DT_F32 ? 4 : 2;
+  const int G = r.groups > 0 ? r.groups : 1;
+  const int K = r.n_src > 0 ? r.n_src / G : 0;
+  bool bad = false;
+  uint32_t bad_e = 0xffffffffu;
+  for (int u = 0; u < U; ++u) {
+    if (!ok[u]) continue;
+    Lanes<W> v;
+#pragma unroll
+    for (int i = 0; i < W; ++i) v.v[i] = 0.0f;
+    double acc[W];
+    for (int g = 0; g < (op == UCP_OP_MEAN ? G : (r.n_src > 0 ? 1 : 0)); ++g) {
+      Lanes<W> p;
+      load_w<W>(p, c.sb + src_off(c, g * K) + 4 * (srow + e[u]));
+      for (int k = 1; k < K; ++k) {
+        Lanes<W> w;
+        load_w<W>(w, c.sb + src_off(c, g * K + k) + 4 * (srow + e[u]));
+        const int d = first_diff<W>(p, w);
+        if (d < W) { bad = true; bad_e = min(bad_e, e[u] + d); }
+      }
+#pragma unroll
+      for (int i = 0; i < W; ++i)
+        acc[i] = g == 0 ? (double)p.v[i] : __dadd_rn(acc[i], (double)p.v[i]);
+      if (g == 0) v = p;
+    }
+    if (op == UCP_OP_MEAN) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) v.v[i] = __double2float_rn(__ddiv_rn(acc[i], (double)G));
+    } else if (op == UCP_OP_NOISE) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) v.v[i] = noise1(v.v[i], r.tp_rank, r.tp);
+    } else if (op == UCP_OP_CHECKZERO) {
+#pragma unroll
+      for (int i = 0; i < W; ++i)
+        if (bits_of(v.v[i]) != 0u) { bad = true; bad_e = min(bad_e, e[u] + i); }
+    }
+    for (int d = 0; d < r.n_dst; ++d)
+      store_w<W>(c.db + dst_off(c, d) + (uint64_t)esz * (drow + e[u]), v, r.dtype);
+  }
+  report(bad, ebase + bad_e, c.run_idx, st);
+}
+
+template <int W, int U>
+__device__ __forceinline__ void general(const Ctx& c, uint64_t srow, uint64_t drow,
+                                        const uint32_t (&e)[U], const bool (&ok)[U],
+                                        uint32_t ebase, ucp_status* st) {
+  if (c.r->op == UCP_OP_COPY) copy_general<W, U>(c, srow, drow, e, ok, ebase, st);
+  else op_general<W, U>(c, srow, drow, e, ok, ebase, st);
+}
+
+// Plain 1:1 f32 copy of vector slots (the dominant case): all loads in
+// flight before the first store.
+__device__ __forceinline__ void fast_copy(const Ctx& c, uint64_t srow, uint64_t drow,
+                                          const uint32_t (&e)[kVec], const bool (&ok)[kVec]) {
+  const char* s0 = c.sb + c.r->src + 4 * srow;
+  char* d0 = c.db + c.r->dst + 4 * drow;
+  float4 v[kVec];
+#pragma unroll
+  for (int u = 0; u < kVec; ++u)
+    if (ok[u]) v[u] = ld_stream4(s0 + 4ull * e[u]);
+#pragma unroll
+  for (int u = 0; u < kVec; ++u)
+    if (ok[u]) st4(d0 + 4ull * e[u], v[u]);
+}
+
+// One warp processes columns [cs, cs+len) of one row.
+__device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs, uint32_t len,
+                                        bool fast, ucp_status* st) {
+  const ucp_run& r = *c.r;
+  const int lane = threadIdx.x & 31;
+  const uint64_t srow = (uint64_t)row * r.src_pitch + cs;
+  const uint64_t drow = (uint64_t)row * r.dst_pitch + cs;
+  const uint32_t ebase = row * r.cols + cs;
+
+  if (r.flags & UCP_RUN_VEC) {
+    // element phase is common to every source and destination of the run
+    const uint32_t phase = r.n_src > 0 ? (uint32_t)(((r.src >> 2) + srow) & 3)
+                                       : (uint32_t)(((r.dst / (r.dtype == UCP_DT_F32 ? 4 : 2)) + drow) & 3);
+    uint32_t head = (4u - phase) & 3u;
+    if (head > len) head = len;
+    const uint32_t nvec = (len - head) >> 2;
+    const uint32_t tail = len - head - 4 * nvec;
+    // vector body: slot u of lane -> vector lane + 32u
+    {
+      uint32_t e[kVec];
+      bool ok[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        const uint32_t vi = lane + 32u * u;
+        ok[u] = vi < nvec;
+        e[u] = head + 4u * vi;
+      }
+      if (fast) fast_copy(c, srow, drow, e, ok);
+      else general<4, kVec>(c, srow, drow, e, ok, ebase, st);
+    }
+    // scalar head + tail (<= 6 elements)
+    if (head + tail > 0) {
+      uint32_t e1[1];
+      bool ok1[1];
+      const uint32_t l = (uint32_t)lane;
+      ok1[0] = l < head + tail;
+      e1[0] = l < head ? l : head + 4 * nvec + (l - head);
+      general<1, 1>(c, srow, drow, e1, ok1, ebase, st);
+    }
+  } else {
+    constexpr int U = 8;
+    for (uint32_t base = 0; base < len; base += 32u * U) {
+      uint32_t e[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        e[u] = base + lane + 32u * u;
+        ok[u] = e[u] < len;
+      }
+      general<1, U>(c, srow, drow, e, ok, ebase, st);
+    }
+  }
+}
+
+template <bool kGather>
+__device__ __forceinline__ void move_body(const ucp_run* __restrict__ runs,
+                                          const uint64_t* __restrict__ aux,
+                                          const ucp_tile* __restrict__ tiles,
+                                          const char* __restrict__ src_base,
+                                          char* __restrict__ dst_base, ucp_status* st) {
+  __shared__ ucp_run s_run;
+  __shared__ uint64_t s_aux[kMaxAux];
+  const ucp_tile tile = tiles[blockIdx.x];
+  if (threadIdx.x < 4) {
+    reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
+        reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
+  }
+  __syncthreads();
+  const int n_aux = (s_run.n_src > 0 ? s_run.n_src - 1 : 0) + (s_run.n_dst > 0 ? s_run.n_dst - 1 : 0);
+  if (n_aux > 0) {
+    for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
+    __syncthreads();
+  }
+  const Ctx c{&s_run, s_aux, src_base, dst_base, tile.run};
+  const bool fast = s_run.op == UCP_OP_COPY && s_run.n_src == 1 && s_run.n_dst == 1 &&
+                    s_run.dtype == UCP_DT_F32;
+
+  uint32_t nr, nc;
+  if (s_run.flags & UCP_RUN_ROWSPLIT) { nr = 1; nc = tile.count; }
+  else { nr = tile.count; nc = s_run.cols; }
+  const uint32_t spr = (nc + kSeg - 1) / kSeg;
+  const uint32_t n_items = nr * spr;
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint32_t it = warp; it < n_items; it += kWarps) {
+    const uint32_t rr = spr == 1 ? it : it / spr;
+    const uint32_t ss = it - rr * spr;
+    const uint32_t cs = tile.col0 + ss * kSeg;
+    const uint32_t ce = min(cs + kSeg, tile.col0 + nc);
+    segment(c, tile.row0 + rr, cs, ce - cs, fast, st);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+convert_gather_kernel(const ucp_run* __restrict__ runs, const uint64_t* __restrict__ aux,
+                      const ucp_tile* __restrict__ tiles, const char* __restrict__ src_base,
+                      char* __restrict__ dst_base, ucp_status* st) {
+  move_body<true>(runs, aux, tiles, src_base, dst_base, st);
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+load_scatter_kernel(const ucp_run* __restrict__ runs, const uint64_t* __restrict__ aux,
+                    const ucp_tile* __restrict__ tiles, const char* __restrict__ src_base,
+                    char* __restrict__ dst_base, ucp_status* st) {
+  move_body<false>(runs, aux, tiles, src_base, dst_base, st);
+}
+
+// ---------------------------------------------------------------- generator
+
+__device__ __forceinline__ float gen1(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= (z >> 31);
+  const int32_t top = (int32_t)(z >> 40) - (1 << 23);
+  return __int2float_rn(top) * 0x1p-23f;  // both steps exact
+}
+
+__global__ void __launch_bounds__(256)
+gen_state_kernel(uint64_t base, uint64_t start, uint64_t count, int abs_flag, float* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+  const bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < count; i += stride) {
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = gen1(base + start + i + k);
+      if (abs_flag) v[k] = fabsf(v[k]);
+    }
+    if (vec && i + 4 <= count) {
+      st4(out + i, make_float4(v[0], v[1], v[2], v[3]));
+    } else {
+      for (int k = 0; k < 4 && i + k < count; ++k) out[i + k] = v[k];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+compare_kernel(const unsigned char* a, const unsigned char* b, uint64_t n,
+               unsigned long long* mismatch) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 16;
+  const bool vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; i < n; i += stride) {
+    if (vec && i + 16 <= n) {
+      const uint4 x = *reinterpret_cast<const uint4*>(a + i);
+      const uint4 y = *reinterpret_cast<const uint4*>(b + i);
+      if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w) {
+        for (int k = 0; k < 16; ++k)
+          if (a[i + k] != b[i + k]) { atomicMin(mismatch, (unsigned long long)(i + k)); break; }
+      }
+    } else {
+      for (int k = 0; k < 16 && i + k < n; ++k)
+        if (a[i + k] != b[i + k]) { atomicMin(mismatch, (unsigned long long)(i + k)); break; }
+    }
+  }
+}
+
+int launch_move(bool gather, const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
+                const ucp_tile* tiles, int64_t n_tiles, const void* src_base, void* dst_base,
+                ucp_status* status, void* stream) {
+  if (n_tiles < 0 || n_runs < 0) return UCP_EINVAL;
+  if (n_tiles == 0) return UCP_OK;
+  if (!runs || !tiles || !status || n_tiles > 0x7fffffffLL) return UCP_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const dim3 grid((unsigned)n_tiles), block(kThreads);
+  if (gather) {
+    convert_gather_kernel<<<grid, block, 0, s>>>(runs, aux, tiles,
+                                                 static_cast<const char*>(src_base),
+                                                 static_cast<char*>(dst_base), status);
+  } else {
+    load_scatter_kernel<<<grid, block, 0, s>>>(runs, aux, tiles,
+                                               static_cast<const char*>(src_base),
+                                               static_cast<char*>(dst_base), status);
+  }
+  return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
+}
+
+int grid_for(uint64_t work, int per_block) {
+  uint64_t blocks = (work + per_block - 1) / per_block;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ucp_version(void) { return UCP_ABI_VERSION; }
+
+int ucp_status_reset(ucp_status* status, void* stream) {
+  if (!status) return UCP_EINVAL;
+  static_assert(sizeof(ucp_status) == 16, "ucp_status layout");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // first = ~0 (no failure), n_bad = 0
+  if (cudaMemsetAsync(&status->first, 0xff, sizeof(unsigned long long), s) != cudaSuccess)
+    return UCP_ECUDA;
+  if (cudaMemsetAsync(&status->n_bad, 0, sizeof(unsigned long long), s) != cudaSuccess)
+    return UCP_ECUDA;
+  return UCP_OK;
+}
+
+int ucp_convert_gather(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
+                       const ucp_tile* tiles, int64_t n_tiles, const void* src_base,
+                       void* dst_base, ucp_status* status, void* stream) {
+  return launch_move(true, runs, n_runs, aux, tiles, n_tiles, src_base, dst_base, status, stream);
+}
+
+int ucp_load_scatter(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
+                     const ucp_tile* tiles, int64_t n_tiles, const void* src_base,
+                     void* dst_base, ucp_status* status, void* stream) {
+  return launch_move(false, runs, n_runs, aux, tiles, n_tiles, src_base, dst_base, status, stream);
+}
+
+int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, float* out,
+                  void* stream) {
+  if (count == 0) return UCP_OK;
+  if (!out) return UCP_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  gen_state_kernel<<<grid_for(count, 256 * 4 * 4), 256, 0, s>>>(base, start, count, abs_flag, out);
+  return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
+}
+
+int ucp_compare(const void* a, const void* b, uint64_t nbytes, unsigned long long* mismatch,
+                void* stream) {
+  if (!mismatch || (nbytes && (!a || !b))) return UCP_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(mismatch, 0xff, sizeof(unsigned long long), s) != cudaSuccess)
+    return UCP_ECUDA;
+  if (nbytes == 0) return UCP_OK;
+  compare_kernel<<<grid_for(nbytes, 256 * 16 * 4), 256, 0, s>>>(
+      static_cast<const unsigned char*>(a), static_cast<const unsigned char*>(b), nbytes, mismatch);
+  return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
+}
+
+int ucp_peek(const void* device_src, void* host_dst, uint64_t nbytes) {
+  if (nbytes == 0) return UCP_OK;
+  if (!device_src || !host_dst) return UCP_EINVAL;
+  return cudaMemcpy(host_dst, device_src, nbytes, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? UCP_OK : UCP_ECUDA;
+}
+
+}  // extern "C"

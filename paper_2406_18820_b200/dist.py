@@ -1,0 +1,93 @@
+"""Multi-GPU partitioning of the reshard.
+
+Every (param, kind) unit is independent, so the path shards by parameter:
+ranks own parameters by LPT on bytes -- identical to the reference's
+``plan_work`` LPT on numel (ucp/convert.py:328-341) because every state
+tensor is f32. Convert needs no exchange (each rank is fed the source
+fragments of the params it owns). Load is param-homed by default (the
+reference world has no rank placement, ucp/load.py:69-76); when target ranks
+are homed on GPUs (target rank g on GPU g mod N), the only exchange is one
+all-to-all-v of the fragments whose owner GPU differs from their home GPU
+(``exchange_plan`` + ``alltoallv``), over NCCL.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import torch
+
+from .spec import ModelSpec
+
+
+@dataclass(frozen=True)
+class WorkPlan:
+    groups: tuple
+    loads: tuple
+
+    def owner(self, param: str) -> int:
+        for gi, grp in enumerate(self.groups):
+            if param in grp:
+                return gi
+        raise KeyError(param)
+
+
+def plan_work(spec: ModelSpec, n_groups: int) -> WorkPlan:
+    """LPT: params by numel descending (ties by name), each to the lightest
+    group (ties to the lowest index)."""
+    if n_groups < 1:
+        raise ValueError("n_groups must be >= 1")
+    groups = [[] for _ in range(n_groups)]
+    loads = [0] * n_groups
+    for p in sorted(spec.params, key=lambda q: (-q.numel, q.name)):
+        gi = min(range(n_groups), key=lambda i: (loads[i], i))
+        groups[gi].append(p.name)
+        loads[gi] += p.numel
+    return WorkPlan(tuple(tuple(g) for g in groups), tuple(loads))
+
+
+def owned_params(spec: ModelSpec, rank: int, world: int) -> list:
+    return list(plan_work(spec, world).groups[rank])
+
+
+def env_rank() -> tuple:
+    """(rank, world_size, local_rank) from torchrun's environment."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def init_process_group(backend: str = "nccl"):
+    import torch.distributed as dist
+
+    rank, world, local = env_rank()
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
+    return rank, world, local
+
+
+def exchange_plan(frag_owner: list, frag_home: list, frag_bytes: list, world: int) -> list:
+    """send[src][dst] byte counts of the rank-homed load exchange: fragment
+    i moves from GPU frag_owner[i] to GPU frag_home[i] when they differ."""
+    send = [[0] * world for _ in range(world)]
+    for o, h, b in zip(frag_owner, frag_home, frag_bytes):
+        if o != h:
+            send[o][h] += b
+    return send
+
+
+def alltoallv(send_buf: torch.Tensor, send_counts: list, recv_counts: list, group=None) -> torch.Tensor:
+    """One all-to-all-v of uint8 buffers (counts in bytes), NCCL on GPUs or
+    gloo on CPU tensors."""
+    import torch.distributed as dist
+
+    recv = torch.empty(sum(recv_counts), dtype=torch.uint8, device=send_buf.device)
+    dist.all_to_all_single(recv, send_buf, recv_counts, send_counts, group=group)
+    return recv

@@ -1,0 +1,160 @@
+"""Device side: compiled programs, launches, status words, staging buffers.
+
+PyTorch is used only as plumbing here (device memory, streams, events); all
+data movement on the hot path goes through libucp_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from ._errors import NativeUnavailableError, PaddingError, ReplicateMismatchError, from_status
+from .plan import OP_CHECKZERO, RunTable
+
+ALIGN = 256  # byte alignment of every fragment / atomic / target buffer
+
+
+def align_up(n: int, a: int = ALIGN) -> int:
+    return (n + a - 1) // a * a
+
+
+def require_device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError("no CUDA device: the reshard path has no CPU fallback")
+    _native.lib()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    return torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise from_status(rc, what)
+
+
+class Program:
+    """One kernel launch worth of runs/aux/tiles, resident on a device."""
+
+    def __init__(self, table: RunTable, device: torch.device, tile_bytes: int = 1 << 17):
+        runs, aux, tiles = table.finish(tile_bytes)
+        self.runs_host, self.aux_host, self.tiles_host = runs, aux, tiles
+        self.units = table.units
+        self.src_bytes, self.dst_bytes = table.src_bytes, table.dst_bytes
+        self.n_runs, self.n_tiles = len(runs), len(tiles)
+        self.device = device
+        blob = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).to(device)
+        self._runs = blob(runs) if len(runs) else torch.zeros(64, dtype=torch.uint8, device=device)
+        self._aux = blob(aux)
+        self._tiles = blob(tiles) if len(tiles) else torch.zeros(16, dtype=torch.uint8, device=device)
+
+    @property
+    def bytes_moved(self) -> int:
+        return self.src_bytes + self.dst_bytes
+
+    def launch(self, gather: bool, src_base: int, dst_base: int, status: "Status",
+               stream: torch.cuda.Stream | None = None) -> None:
+        if self.n_tiles == 0:
+            return
+        lib = _native.lib()
+        fn = lib.ucp_convert_gather if gather else lib.ucp_load_scatter
+        rc = fn(self._runs.data_ptr(), self.n_runs, self._aux.data_ptr(), self._tiles.data_ptr(),
+                self.n_tiles, ctypes.c_void_p(src_base), ctypes.c_void_p(dst_base),
+                status.ptr, stream_ptr(stream))
+        _check(rc, "convert_gather" if gather else "load_scatter")
+
+
+class Status:
+    """Device status word (ucp_status) + host readback."""
+
+    def __init__(self, device: torch.device):
+        self.t = torch.zeros(2, dtype=torch.int64, device=device)
+        self.ptr = self.t.data_ptr()
+
+    def reset(self, stream=None) -> None:
+        _check(_native.lib().ucp_status_reset(self.ptr, stream_ptr(stream)), "status_reset")
+
+    def read(self) -> tuple:
+        v = self.t.cpu().numpy().view(np.uint64)
+        return int(v[0]), int(v[1])
+
+    def raise_if_bad(self, prog: Program, src_base: int) -> None:
+        first, n_bad = self.read()
+        if first == (1 << 64) - 1:
+            return
+        raise describe_failure(prog, first >> 32, first & 0xFFFFFFFF, src_base)
+
+
+def _peek_f32(addr: int) -> int:
+    """Read 4 bytes of device memory at an absolute address (error path only)."""
+    out = np.zeros(1, dtype=np.uint32)
+    rc = _native.lib().ucp_peek(ctypes.c_void_p(addr), out.ctypes.data, 4)
+    return int(out[0]) if rc == 0 else 0xFFFFFFFF
+
+
+def describe_failure(prog: Program, run_idx: int, elem: int, src_base: int) -> Exception:
+    """Reference-style exception for a failing run (ucp/convert.py:165-171,
+    :272-277, :127-128)."""
+    r = prog.runs_host[run_idx]
+    unit = prog.units[int(r["tag"])]
+    where = f"{unit.param}.{unit.kind}"
+    if int(r["op"]) == OP_CHECKZERO:
+        return PaddingError(f"{where}: nonzero pad tail (first bad element {elem})")
+    labels = unit.labels.get(run_idx)
+    row, col = divmod(elem, int(r["cols"]))
+    n_src, groups = int(r["n_src"]), max(int(r["groups"]), 1)
+    K = n_src // groups
+    offs = [int(r["src"])] + [int(x) for x in prog.aux_host[int(r["aux"]):int(r["aux"]) + n_src - 1]]
+    pos = 4 * (row * int(r["src_pitch"]) + col)
+    vals = [_peek_f32(src_base + o + pos) for o in offs]
+    if labels:
+        for g in range(groups):
+            for k in range(1, K):
+                i = g * K + k
+                if vals[i] != vals[g * K]:
+                    t0, d0 = labels[g * K]
+                    t1, d1 = labels[i]
+                    if t1 == t0:
+                        return ReplicateMismatchError(
+                            f"{where} tp_rank {t1}: dp replicas differ (dp {d0} vs dp {d1})")
+                    return ReplicateMismatchError(
+                        f"{where}: tp replicas differ (tp {t0} vs tp {t1})")
+    return ReplicateMismatchError(f"{where}: replicas differ (element {elem})")
+
+
+class Arena:
+    """A device (or pinned host) byte buffer."""
+
+    def __init__(self, nbytes: int, device: torch.device | None = None, pinned: bool = False):
+        nbytes = max(int(nbytes), 16)
+        if device is not None:
+            self.t = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        else:
+            self.t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=pinned)
+        self.nbytes = nbytes
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def numpy(self) -> np.ndarray:
+        return self.t.numpy()
+
+
+def gen_state(base: int, start: int, count: int, abs_flag: bool, out_ptr: int, stream=None) -> None:
+    _check(_native.lib().ucp_gen_state(base, start, count, int(abs_flag), ctypes.c_void_p(out_ptr),
+                                       stream_ptr(stream)), "gen_state")
+
+
+def compare(a_ptr: int, b_ptr: int, nbytes: int, scratch: torch.Tensor, stream=None) -> None:
+    _check(_native.lib().ucp_compare(ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), nbytes,
+                                     scratch.data_ptr(), stream_ptr(stream)), "compare")

@@ -1,0 +1,573 @@
+"""Descriptor compiler: (param, kind) units -> 2-D strided run tables + tiles.
+
+This is the host half of the hot path. It turns the reference's union /
+extract_fragment semantics into the device descriptor table that
+``libucp_b200.so`` executes (include/ucp_b200.h):
+
+* ``compile_union``   mirrors union() + _collapse_dp() + strip_pad()
+                      (ucp/convert.py:115-308): all metadata validation
+                      happens here, raising the reference's error classes in
+                      the reference's order; data-dependent checks (replica
+                      equality, zero pads) become COPY-with-replicas and
+                      CHECKZERO runs whose failures come back via ucp_status.
+* ``compile_extract`` mirrors extract_fragment() + partial_noise() + cast
+                      (ucp/parallel.py:340-411, ucp/tensor.py:208-223); target
+                      records with identical bytes (dp replicas, tp replicas
+                      of replicated params) share one read and fan out.
+* ``compile_grid``    mirrors _union_hy() (ucp/convert.py:196-218).
+
+A TP fragment is addressed in its own row-major flat space. The TP pattern is
+a list of *correspondences* (frag flat interval <-> 2-D region of the atomic
+tensor, see ``tp_correspondences``); ZeRO flat pieces and replicas are
+*source maps* over the same flat space. Runs are emitted per sub-interval
+between all source-map boundaries, each split into head / body / tail rows.
+"""
+
+from __future__ import annotations
+
+from collections import defaultdict
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._errors import (
+    ManifestError,
+    MissingFragmentError,
+    OverlappingRangeError,
+    PaddingError,
+    PatternCoverageError,
+    ShapeError,
+)
+from .layout import PARTIAL, REPLICATE, SHARD_H, SHARD_HY, SHARD_NC, SHARD_V, tp_fragment_shape, tp_mode
+from .spec import DType, ParallelConfig, ParamSpec, RecordMeta
+
+# --------------------------------------------------------------------------- ABI
+
+OP_COPY, OP_MEAN, OP_NOISE, OP_ZERO, OP_CHECKZERO = 0, 1, 2, 3, 4
+RUN_VEC, RUN_ROWSPLIT = 1, 2
+SEG = 512            # elements per warp segment (kSeg in the kernel)
+MAX_AUX = 256        # kMaxAux in the kernel
+MAX_SRC = 64         # sources per run before verify-only continuation runs
+MAX_DST = 64         # destinations per run before a second fan-out run
+
+RUN_DTYPE = np.dtype({
+    "names": ["src", "dst", "src_pitch", "dst_pitch", "rows", "cols", "aux", "n_src", "n_dst",
+              "groups", "op", "dtype", "tp_rank", "tp", "tag", "flags"],
+    "formats": ["<u8", "<u8", "<u4", "<u4", "<u4", "<u4", "<u4", "<u2", "<u2",
+                "<u2", "u1", "u1", "<u2", "<u2", "<u4", "<u4"],
+    "offsets": [0, 8, 16, 20, 24, 28, 32, 36, 38, 40, 42, 43, 44, 46, 48, 52],
+    "itemsize": 64,
+})
+TILE_DTYPE = np.dtype([("run", "<u4"), ("row0", "<u4"), ("col0", "<u4"), ("count", "<u4")])
+
+_ESZ = {DType.F32: 4, DType.F16: 2, DType.BF16: 2}
+
+
+def _numel(shape) -> int:
+    n = 1
+    for d in shape:
+        n *= int(d)
+    return n
+
+
+# --------------------------------------------------------------------------- tables
+
+
+@dataclass
+class Unit:
+    """Provenance of a (param, kind) unit, for error messages."""
+
+    param: str
+    kind: str
+    labels: dict = field(default_factory=dict)  # run index -> list of source labels
+
+
+class RunTable:
+    """Accumulates runs + aux offsets for one kernel launch."""
+
+    def __init__(self):
+        self._rows: list = []
+        self._aux: list = []
+        self.units: list = []
+        self.src_bytes = 0   # algorithmic bytes read
+        self.dst_bytes = 0   # algorithmic bytes written
+
+    def unit(self, param: str, kind: str) -> int:
+        self.units.append(Unit(param, kind))
+        return len(self.units) - 1
+
+    def add(self, *, srcs, dsts, src_pitch, dst_pitch, rows, cols, op=OP_COPY, groups=1,
+            dtype=DType.F32, tp_rank=0, tp=1, tag=0, labels=None) -> None:
+        """srcs/dsts: byte offsets (group-major for sources)."""
+        if rows == 0 or cols == 0:
+            return
+        if rows * cols >= 1 << 32:
+            # keep rows*cols < 2^32 (element index inside a run is u32)
+            per = max(1, ((1 << 31) // cols))
+            for r0 in range(0, rows, per):
+                n = min(per, rows - r0)
+                self.add(srcs=[s + 4 * r0 * src_pitch for s in srcs],
+                         dsts=[d + _ESZ[dtype] * r0 * dst_pitch for d in dsts],
+                         src_pitch=src_pitch, dst_pitch=dst_pitch, rows=n, cols=cols, op=op,
+                         groups=groups, dtype=dtype, tp_rank=tp_rank, tp=tp, tag=tag,
+                         labels=labels)
+            return
+        if len(dsts) > MAX_DST:
+            for i in range(0, len(dsts), MAX_DST):
+                self.add(srcs=srcs if i == 0 else srcs[:1], dsts=dsts[i:i + MAX_DST],
+                         src_pitch=src_pitch, dst_pitch=dst_pitch, rows=rows, cols=cols, op=op,
+                         groups=groups, dtype=dtype, tp_rank=tp_rank, tp=tp, tag=tag,
+                         labels=labels if i == 0 else None)
+            return
+        if len(srcs) > MAX_SRC and op == OP_COPY:
+            # verify-only continuation runs compare extra replicas with replica 0
+            head, rest = srcs[:MAX_SRC], srcs[MAX_SRC:]
+            self.add(srcs=head, dsts=dsts, src_pitch=src_pitch, dst_pitch=dst_pitch, rows=rows,
+                     cols=cols, op=op, dtype=dtype, tag=tag,
+                     labels=None if labels is None else labels[:MAX_SRC])
+            for i in range(0, len(rest), MAX_SRC - 1):
+                chunk = rest[i:i + MAX_SRC - 1]
+                self.add(srcs=[srcs[0]] + chunk, dsts=[], src_pitch=src_pitch,
+                         dst_pitch=dst_pitch, rows=rows, cols=cols, op=op, tag=tag,
+                         labels=None if labels is None else
+                         [labels[0]] + labels[MAX_SRC + i:MAX_SRC + i + len(chunk)])
+            return
+        if len(srcs) + len(dsts) - 2 > MAX_AUX:
+            raise ShapeError("too many sources for one averaged run")
+        esz = _ESZ[dtype]
+        ph = set()
+        for s in srcs:
+            ph.add((s // 4) % 4 if s % 4 == 0 else -1)
+        for d in dsts:
+            ph.add((d // esz) % 4 if d % esz == 0 else -1)
+        vec = len(ph) == 1 and -1 not in ph and (
+            rows == 1 or (src_pitch % 4 == 0 and dst_pitch % 4 == 0) or
+            (not srcs and dst_pitch % 4 == 0) or (not dsts and src_pitch % 4 == 0))
+        aux_at = len(self._aux)
+        self._aux.extend(srcs[1:])
+        self._aux.extend(dsts[1:])
+        if labels is not None:
+            self.units[tag].labels[len(self._rows)] = labels
+        self._rows.append((srcs[0] if srcs else 0, dsts[0] if dsts else 0, src_pitch, dst_pitch,
+                           rows, cols, aux_at, len(srcs), len(dsts), groups, op, dtype.value,
+                           tp_rank, tp, tag, RUN_VEC if vec else 0))
+        n = rows * cols
+        self.src_bytes += 4 * n * len(srcs)
+        self.dst_bytes += esz * n * len(dsts)
+
+    def __len__(self):
+        return len(self._rows)
+
+    def finish(self, tile_bytes: int = 1 << 17):
+        runs = np.zeros(len(self._rows), dtype=RUN_DTYPE)
+        if self._rows:
+            cols = list(zip(*self._rows))
+            for name, vals in zip(RUN_DTYPE.names, cols):
+                runs[name] = vals
+        aux = np.asarray(self._aux if self._aux else [0], dtype=np.uint64)
+        tiles = make_tiles(runs, tile_bytes)
+        return runs, aux, tiles
+
+
+def make_tiles(runs: np.ndarray, tile_bytes: int) -> np.ndarray:
+    """One CTA per tile; a tile never straddles runs. Tile size is
+    normalised by bytes moved per element so tiles cost about the same."""
+    if len(runs) == 0:
+        return np.zeros(0, dtype=TILE_DTYPE)
+    esz = np.where(runs["dtype"] == 0, 4, 2).astype(np.int64)
+    bpe = 4 * runs["n_src"].astype(np.int64) + esz * runs["n_dst"].astype(np.int64)
+    bpe = np.maximum(bpe, 4)
+    telems = np.maximum(SEG, (tile_bytes // bpe) // SEG * SEG)
+    rows = runs["rows"].astype(np.int64)
+    cols = runs["cols"].astype(np.int64)
+    split = cols > telems
+    runs["flags"] = np.where(split, runs["flags"] | RUN_ROWSPLIT, runs["flags"] & ~np.uint32(RUN_ROWSPLIT))
+    out = []
+    idx = np.arange(len(runs))
+    # column-split runs: rows * ceil(cols / telems) tiles
+    for i in idx[split]:
+        tpr = -(-cols[i] // telems[i])
+        c0 = np.arange(tpr, dtype=np.int64) * telems[i]
+        cnt = np.minimum(telems[i], cols[i] - c0)
+        r = np.repeat(np.arange(rows[i], dtype=np.int64), tpr)
+        t = np.zeros(len(r), dtype=TILE_DTYPE)
+        t["run"] = i
+        t["row0"] = r
+        t["col0"] = np.tile(c0, rows[i])
+        t["count"] = np.tile(cnt, rows[i])
+        out.append(t)
+    # row-block runs
+    whole = idx[~split]
+    if len(whole):
+        rpt = np.maximum(1, telems[whole] // np.maximum(cols[whole], 1))
+        ntile = -(-rows[whole] // rpt)
+        run_of = np.repeat(whole, ntile)
+        first = np.repeat(np.cumsum(ntile) - ntile, ntile)
+        k = np.arange(len(run_of)) - first
+        rp = np.repeat(rpt, ntile)
+        t = np.zeros(len(run_of), dtype=TILE_DTYPE)
+        t["run"] = run_of
+        t["row0"] = k * rp
+        t["col0"] = 0
+        t["count"] = np.minimum(rp, rows[run_of] - k * rp)
+        out.append(t)
+    tiles = np.concatenate(out) if out else np.zeros(0, dtype=TILE_DTYPE)
+    # interleave big and small runs' tiles? keep run order: it is the order
+    # of the destination buffers, which keeps writes sequential per run
+    order = np.argsort(tiles["run"], kind="stable")
+    return tiles[order]
+
+
+# --------------------------------------------------------------------------- geometry
+
+
+def tp_correspondences(p: ParamSpec, mode: str, tp: int, t: int) -> list:
+    """[(f0, x_off, x_pitch, rows, cols)]: TP fragment t's flat elements
+    f0 + i*cols + j  <->  atomic element x_off + i*x_pitch + j.
+    The inverse of extract_fragment's slicing (ucp/parallel.py:383-399)."""
+    shape = tuple(p.shape)
+    n = _numel(shape)
+    if n == 0:
+        return []
+    if mode in ("full", REPLICATE, PARTIAL):
+        return [(0, 0, n, 1, n)]
+    if mode == SHARD_V:
+        fn = n // tp
+        return [(0, t * fn, fn, 1, fn)]
+    if mode == SHARD_H:
+        inner = _numel(shape[2:])
+        c = shape[1] // tp * inner
+        return [(0, t * c, shape[1] * inner, shape[0], c)]
+    if mode == SHARD_NC:
+        w = _numel(shape[1:])
+        out, cum = [], 0
+        for start, length in p.nc_segments:
+            k = length // tp
+            out.append((cum * w, (start + t * k) * w, k * w, 1, k * w))
+            cum += k
+        return out
+    raise PatternCoverageError(f"mode {mode} not extractable")
+
+
+def split_rows(corr, a: int, b: int) -> list:
+    """Pieces (frag_start, x_start, x_pitch, rows, cols) of frag interval
+    [a, b) under one correspondence: head partial row, full rows, tail."""
+    f0, x0, xp, R, C = corr
+    a, b = max(a, f0), min(b, f0 + R * C)
+    if a >= b:
+        return []
+    out = []
+    i, j = divmod(a - f0, C)
+    if j:
+        n = min(C - j, b - a)
+        out.append((a, x0 + i * xp + j, xp, 1, n))
+        a += n
+        i += 1
+        if a >= b:
+            return out
+    full = (b - a) // C
+    if full:
+        out.append((a, x0 + i * xp, xp, full, C))
+        a += full * C
+        i += full
+    if a < b:
+        out.append((a, x0 + i * xp, xp, 1, b - a))
+    return out
+
+
+class SourceMap:
+    """Where a TP fragment's flat elements [0, n) live: sorted segments
+    (lo, hi, byte_offset_of_lo)."""
+
+    __slots__ = ("segs", "label")
+
+    def __init__(self, segs, label):
+        self.segs = segs
+        self.label = label
+
+    def offset(self, pos: int) -> int:
+        for lo, hi, off in self.segs:
+            if lo <= pos < hi:
+                return off + 4 * (pos - lo)
+        raise ShapeError(f"flat position {pos} not covered")
+
+    def bounds(self):
+        for lo, hi, _ in self.segs:
+            yield lo
+            yield hi
+
+
+def _cuts(maps, lo: int, hi: int) -> list:
+    pts = {lo, hi}
+    for m in maps:
+        for x in m.bounds():
+            if lo < x < hi:
+                pts.add(x)
+    return sorted(pts)
+
+
+# --------------------------------------------------------------------------- union
+
+
+def _where(p, frags) -> str:
+    return f"{p.name}.{frags[0][0].kind if frags else '?'}"
+
+
+def _collapse(p, cfg, t, items, mode, strict, where):
+    """_collapse_dp validation (ucp/convert.py:137-193). items: [(meta, off,
+    n)]. Returns (replica source maps, pad check segments)."""
+    ctx = f"{where} tp_rank {t}"
+    flat = items[0][0].flat_range is not None
+    for m, _, _ in items:
+        if (m.flat_range is not None) != flat:
+            raise ManifestError(f"{ctx}: mixed flat and non-flat fragments")
+    seen = defaultdict(list)
+    for it in items:
+        seen[it[0].placement[2]].append(it)
+    missing = [d for d in range(cfg.dp) if d not in seen]
+    if missing:
+        raise MissingFragmentError(f"{ctx}: no fragment from dp ranks {missing}")
+    if not flat:
+        dups = [d for d, grp in seen.items() if len(grp) > 1]
+        if dups:
+            raise OverlappingRangeError(f"{ctx}: duplicate fragments from dp ranks {dups}")
+        fshape = _mode_shape(p, mode, cfg.tp)
+        fn = _numel(fshape)
+        maps = []
+        for d in range(cfg.dp if strict else 1):
+            m, off, n = seen[d][0]
+            if n != fn:
+                raise ShapeError(f"{ctx}: fragment of {n} elements, expected {fshape}")
+            maps.append(SourceMap([(0, fn, off)], (t, d)))
+        return maps, []
+    ranged = sorted(items, key=lambda it: tuple(it[0].flat_range))
+    pos = 0
+    segs = []
+    for i, (m, off, n) in enumerate(ranged):
+        lo, hi = m.flat_range
+        if lo < pos:
+            raise OverlappingRangeError(f"{ctx}: flat range [{lo},{hi}) overlaps previous end {pos}")
+        if lo > pos:
+            raise MissingFragmentError(f"{ctx}: flat gap [{pos},{lo})")
+        if hi - lo != n:
+            raise ManifestError(f"{ctx}: payload size != flat range extent")
+        pos = hi
+        if i != len(ranged) - 1 and m.pad_elems:
+            raise PaddingError(f"{ctx}: pad recorded on a non-final flat shard")
+        segs.append((lo, hi, off))
+    pad = ranged[-1][0].pad_elems
+    fn = _numel(tp_fragment_shape(p, mode, cfg.tp))
+    if pad < 0 or fn + pad != pos:
+        raise PaddingError(
+            f"pad arithmetic mismatch: {pos} elements != {fn} + pad {pad}")
+    smap = SourceMap(segs, (t, None))
+    pad_runs = []
+    if pad:
+        for lo, hi, off in segs:
+            a, b = max(lo, fn), min(hi, pos)
+            if a < b:
+                pad_runs.append((off + 4 * (a - lo), b - a))
+    return [smap], pad_runs
+
+
+def _mode_shape(p, mode, tp):
+    if mode in ("full", REPLICATE, PARTIAL, SHARD_V, SHARD_H, SHARD_NC):
+        return tp_fragment_shape(p, mode, tp)
+    raise ManifestError(f"{p.name}: unknown pattern tag {mode!r}")
+
+
+def _emit_group(tab, p, groups, corrs, fn, dst_off, op, tag, G):
+    """Runs writing atomic regions from `groups` (list over G of replica
+    source maps) through `corrs`."""
+    maps = [m for grp in groups for m in grp]
+    labels = [m.label for m in maps]
+    cuts = _cuts(maps, 0, fn)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        for corr in corrs:
+            for fs, xs, xp, rows, cols in split_rows(corr, a, b):
+                tab.add(srcs=[m.offset(fs) for m in maps], dsts=[dst_off + 4 * xs],
+                        src_pitch=corr[4], dst_pitch=xp, rows=rows, cols=cols, op=op,
+                        groups=G, tag=tag, labels=labels)
+
+
+def compile_union(tab: RunTable, p: ParamSpec, cfg: ParallelConfig, frags: list,
+                  dst_off: int, strict: bool = True) -> int:
+    """Runs that consolidate one (param, kind) into the atomic tensor at byte
+    offset dst_off. frags: [(RecordMeta, src_byte_off, n_elems)]."""
+    if not frags:
+        raise MissingFragmentError(f"{p.name}: no fragments at all")
+    where = _where(p, frags)
+    kinds = {m.kind for m, _, _ in frags}
+    names = {m.param for m, _, _ in frags}
+    tags = {m.pattern for m, _, _ in frags}
+    if len(kinds) != 1 or names != {p.name}:
+        raise ManifestError(f"{where}: mixed params/kinds in one union call")
+    if len(tags) != 1:
+        raise ManifestError(f"{where}: inconsistent pattern tags {sorted(tags)}")
+    tag_name = frags[0][0].pattern
+    tag = tab.unit(p.name, frags[0][0].kind)
+    if tag_name == SHARD_HY:
+        return compile_grid(tab, p, frags, dst_off, tag, where)
+    stages = {m.placement[0] for m, _, _ in frags}
+    if len(stages) != 1:
+        raise ManifestError(f"{where}: fragments from multiple pp stages {sorted(stages)}")
+    mode = "full" if cfg.tp == 1 else tag_name
+    by_tp = defaultdict(list)
+    for it in frags:
+        by_tp[it[0].placement[1]].append(it)
+    expect = {0} if mode == "full" else set(range(cfg.tp))
+    if set(by_tp) != expect:
+        raise MissingFragmentError(f"{where}: tp ranks {sorted(by_tp)} != expected {sorted(expect)}")
+    per_tp = {}
+    pads = []
+    for t, items in by_tp.items():
+        per_tp[t], pr = _collapse(p, cfg, t, items, mode, strict, where)
+        pads += pr
+    if mode not in ("full", REPLICATE, PARTIAL, SHARD_V, SHARD_H, SHARD_NC):
+        raise ManifestError(f"{where}: unknown pattern tag {tag_name!r}")
+    if mode == SHARD_NC:
+        segs = frags[0][0].segments
+        if segs is None or tuple(map(tuple, segs)) != tuple(map(tuple, p.nc_segments or ())):
+            raise ManifestError(f"{where}: nc segments disagree with the model spec")
+    fshape = tp_fragment_shape(p, mode, cfg.tp)
+    _check_assembled(p, mode, fshape, cfg.tp, where)
+    fn = _numel(fshape)
+
+    for off, n in pads:
+        tab.add(srcs=[off], dsts=[], src_pitch=n, dst_pitch=n, rows=1, cols=n,
+                op=OP_CHECKZERO, tag=tag, labels=[("pad",)])
+    if mode == "full":
+        _emit_group(tab, p, [per_tp[0]], tp_correspondences(p, "full", 1, 0), fn, dst_off,
+                    OP_COPY, tag, 1)
+    elif mode == REPLICATE:
+        grp = [m for t in range(cfg.tp) for m in per_tp[t]] if strict else per_tp[0][:1]
+        _emit_group(tab, p, [grp], tp_correspondences(p, mode, cfg.tp, 0), fn, dst_off,
+                    OP_COPY, tag, 1)
+    elif mode == PARTIAL:
+        groups = [per_tp[t] for t in range(cfg.tp)]
+        _emit_group(tab, p, groups, tp_correspondences(p, mode, cfg.tp, 0), fn, dst_off,
+                    OP_MEAN, tag, cfg.tp)
+    else:
+        for t in range(cfg.tp):
+            _emit_group(tab, p, [per_tp[t]], tp_correspondences(p, mode, cfg.tp, t), fn,
+                        dst_off, OP_COPY, tag, 1)
+    return tag
+
+
+def _check_assembled(p, mode, fshape, tp, where):
+    s = tuple(p.shape)
+    if mode in ("full", REPLICATE, PARTIAL):
+        got = fshape
+    elif mode == SHARD_V:
+        got = (fshape[0] * tp,) + fshape[1:]
+    elif mode == SHARD_H:
+        got = (fshape[0], fshape[1] * tp) + fshape[2:] if len(fshape) > 1 else fshape
+    else:
+        got = s if sum(n for _, n in p.nc_segments) == s[0] and all(
+            n % tp == 0 for _, n in p.nc_segments) else (-1,)
+    if tuple(got) != s:
+        raise ShapeError(f"{where}: assembled {tuple(got)} != spec {s}")
+
+
+def compile_grid(tab, p, frags, dst_off, tag, where) -> int:
+    """Shard-Hy block grid, placement (0, row, col) (ucp/convert.py:196-218)."""
+    grid = {}
+    for m, off, n in frags:
+        key = (m.placement[1], m.placement[2])
+        if key in grid:
+            raise OverlappingRangeError(f"{where}: duplicate block {key}")
+        grid[key] = (m, off, n)
+    R = 1 + max(k[0] for k in grid)
+    C = 1 + max(k[1] for k in grid)
+    missing = [(r, c) for r in range(R) for c in range(C) if (r, c) not in grid]
+    if missing:
+        raise MissingFragmentError(f"{where}: missing blocks {missing[:4]}")
+    if len(p.shape) != 2:
+        raise ShapeError(f"{where}: shard_hy needs a 2-D param")
+    rows = [tuple(grid[(r, 0)][0].shape)[0] for r in range(R)]
+    cols = [tuple(grid[(0, c)][0].shape)[1] for c in range(C)]
+    for (r, c), (m, _, n) in grid.items():
+        if tuple(m.shape) != (rows[r], cols[c]) or n != rows[r] * cols[c]:
+            raise ShapeError(f"{where}: block {(r, c)} shape {m.shape}")
+    if (sum(rows), sum(cols)) != tuple(p.shape):
+        raise ShapeError(f"{where}: assembled {(sum(rows), sum(cols))} != {p.shape}")
+    W = p.shape[1]
+    r0 = 0
+    for r in range(R):
+        c0 = 0
+        for c in range(C):
+            m, off, n = grid[(r, c)]
+            tab.add(srcs=[off], dsts=[dst_off + 4 * (r0 * W + c0)], src_pitch=cols[c],
+                    dst_pitch=W, rows=rows[r], cols=cols[c], tag=tag, labels=[(r, c)])
+            c0 += cols[c]
+        r0 += rows[r]
+    return tag
+
+
+# --------------------------------------------------------------------------- extract
+
+
+def noise_is_identity(t: int, tp: int) -> bool:
+    return tp == 1 or (tp % 2 == 1 and t == tp - 1)
+
+
+def compile_extract(tab: RunTable, p: ParamSpec, cfg: ParallelConfig, targets: list,
+                    src_off: int, dtype: DType = DType.F32) -> int:
+    """Runs slicing one atomic tensor (f32 at byte offset src_off) into every
+    target record in `targets` = [(RecordMeta, dst_byte_off)], writing
+    `dtype` (the weight cast; moments pass DType.F32)."""
+    if not targets:
+        return -1
+    tag = tab.unit(p.name, targets[0][0].kind)
+    mode = tp_mode(p, cfg.tp)
+    fshape = tp_fragment_shape(p, mode, cfg.tp)
+    fn = _numel(fshape)
+    esz = _ESZ[dtype]
+    groups = defaultdict(list)
+    for meta, off in targets:
+        t = meta.placement[1]
+        if mode in (SHARD_V, SHARD_H, SHARD_NC):
+            key_t = t
+        elif mode == PARTIAL and not noise_is_identity(t, cfg.tp):
+            key_t = t
+        else:
+            key_t = -1
+        fr = None if meta.flat_range is None else tuple(meta.flat_range)
+        groups[(key_t, fr)].append(off)
+    padded = -(-fn // cfg.dp) * cfg.dp if fn else 0
+    for (key_t, fr), dsts in groups.items():
+        t = max(key_t, 0)
+        corrs = tp_correspondences(p, mode if mode != PARTIAL else "full", cfg.tp, t)
+        op = OP_NOISE if mode == PARTIAL and key_t >= 0 else OP_COPY
+        if fr is None:
+            lo, hi = 0, fn
+        else:
+            lo, hi = min(fr[0], padded), min(max(fr[1], fr[0]), padded)
+        real_hi = min(hi, fn)
+        for corr in corrs:
+            for fs, xs, xp, rows, cols in split_rows(corr, lo, real_hi):
+                tab.add(srcs=[src_off + 4 * xs], dsts=[d + esz * (fs - lo) for d in dsts],
+                        src_pitch=xp, dst_pitch=corr[4], rows=rows, cols=cols, op=op,
+                        dtype=dtype, tp_rank=t, tp=cfg.tp, tag=tag)
+        if hi > max(lo, fn):
+            z0 = max(lo, fn)
+            tab.add(srcs=[], dsts=[d + esz * (z0 - lo) for d in dsts], src_pitch=hi - z0,
+                    dst_pitch=hi - z0, rows=1, cols=hi - z0, op=OP_ZERO, dtype=dtype, tag=tag)
+    return tag
+
+
+def fragment_elems(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta) -> int:
+    """Element count of the fragment extract_fragment returns for meta."""
+    if meta.flat_range is None:
+        return _numel(tp_fragment_shape(p, tp_mode(p, cfg.tp), cfg.tp))
+    fn = _numel(tp_fragment_shape(p, tp_mode(p, cfg.tp), cfg.tp))
+    padded = -(-fn // cfg.dp) * cfg.dp if fn else 0
+    lo, hi = meta.flat_range
+    lo, hi = min(lo, padded), min(max(hi, lo), padded)
+    return max(hi - lo, 0)
+
+
+def fragment_shape(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta) -> tuple:
+    if meta.flat_range is None:
+        return tuple(tp_fragment_shape(p, tp_mode(p, cfg.tp), cfg.tp))
+    return (fragment_elems(p, cfg, meta),)

@@ -1,0 +1,390 @@
+"""Whole-model reshard engine: convert (union) + load (extract) between two
+layouts, in layer windows, on one GPU.
+
+This is the in-memory form of the reference's ``resume()`` data path
+(ucp/load.py:276-281 = convert ucp/convert.py:422-563 then load
+ucp/load.py:131-223) without the file system: source fragments of every
+source rank are laid out in one arena, grouped by window; each window runs
+one ``ucp_convert_gather`` launch (source arena -> atomic window buffer) and
+one ``ucp_load_scatter`` launch (atomic window -> target fragments of every
+target rank). Windows are contiguous groups of parameters in spec order under
+a byte budget (a LLaMA layer, the embedding, ...).
+
+Modes:
+* device-resident (``step_device``): the whole source arena lives in HBM;
+  targets go to a window ring in HBM. This is what ``bench.py`` times as the
+  device ``value``.
+* host-streamed (``run_host`` / ``stream_host``): source windows are copied
+  H2D from pinned memory on a copy stream, converted + loaded on the compute
+  stream and copied D2H on a second copy stream, double-buffered, so PCIe in,
+  HBM work and PCIe out overlap (north_star item 4). This is the end-to-end
+  path a caller with host buffers uses.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .engine import Program, Status, align_up, gen_state, require_device, stream_ptr
+from .layout import all_rank_records, validate_model_config
+from .plan import RunTable, compile_extract, compile_union, fragment_elems, fragment_shape
+from .spec import STATE_KINDS, DType, ModelSpec, ParallelConfig
+from .synth import stream_base
+
+
+@dataclass
+class Window:
+    params: list
+    src_frags: list = field(default_factory=list)   # (g, idx, meta, off, n)
+    tgt_frags: list = field(default_factory=list)   # (g, idx, meta, off, n, dtype)
+    atom: dict = field(default_factory=dict)        # (param, kind) -> off
+    src_bytes: int = 0
+    atom_bytes: int = 0
+    tgt_bytes: int = 0
+    src_base: int = 0    # offset of this window in the global source arena
+    tgt_base: int = 0    # offset of this window in the global target arena
+    conv: object = None  # RunTable / Program
+    load: object = None
+    synth: object = None
+
+
+class ReshardPlan:
+    """Compiled convert+load of (a subset of) a model between two layouts."""
+
+    def __init__(self, spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig,
+                 dtype: DType = DType.F32, strict: bool = True, params=None, device=None,
+                 window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17):
+        validate_model_config(spec, src)
+        validate_model_config(spec, tgt)
+        self.spec, self.src, self.tgt, self.dtype, self.strict = spec, src, tgt, dtype, strict
+        self.device = require_device(device)
+        self.tile_bytes = tile_bytes
+        names = None if params is None else set(params)
+        self.params = [p for p in spec.params if names is None or p.name in names]
+        self.windows = self._make_windows(window_bytes)
+        self._layout()
+        self._compile()
+        self.status = Status(self.device)
+        self._bufs = {}
+
+    # ------------------------------------------------------------------ planning
+
+    def _make_windows(self, budget: int) -> list:
+        out, cur, acc = [], [], 0
+        for p in self.params:
+            s = 12 * p.numel
+            if cur and acc + s > budget:
+                out.append(Window(cur))
+                cur, acc = [], 0
+            cur.append(p)
+            acc += s
+        if cur:
+            out.append(Window(cur))
+        return out
+
+    def _layout(self) -> None:
+        src_recs = all_rank_records(self.spec, self.src)
+        tgt_recs = all_rank_records(self.spec, self.tgt)
+        win_of = {p.name: i for i, w in enumerate(self.windows) for p in w.params}
+        for g in range(self.src.world_size):
+            for i, m in enumerate(src_recs[g]):
+                w = win_of.get(m.param)
+                if w is None:
+                    continue
+                W = self.windows[w]
+                n = fragment_elems(self.spec.param(m.param), self.src, m)
+                W.src_frags.append((g, i, m, W.src_bytes, n))
+                W.src_bytes += align_up(4 * n)
+        for g in range(self.tgt.world_size):
+            for i, m in enumerate(tgt_recs[g]):
+                w = win_of.get(m.param)
+                if w is None:
+                    continue
+                W = self.windows[w]
+                dt = self.dtype if m.kind == "weight" else DType.F32
+                n = fragment_elems(self.spec.param(m.param), self.tgt, m)
+                W.tgt_frags.append((g, i, m, W.tgt_bytes, n, dt))
+                W.tgt_bytes += align_up(dt.itemsize * n)
+        sb = tb = 0
+        for W in self.windows:
+            for p in W.params:
+                for k in STATE_KINDS:
+                    W.atom[(p.name, k)] = W.atom_bytes
+                    W.atom_bytes += align_up(4 * p.numel)
+            W.src_base, W.tgt_base = sb, tb
+            sb += W.src_bytes
+            tb += W.tgt_bytes
+        self.src_total, self.tgt_total = sb, tb
+        self.max_src = max((W.src_bytes for W in self.windows), default=0)
+        self.max_atom = max((W.atom_bytes for W in self.windows), default=0)
+        self.max_tgt = max((W.tgt_bytes for W in self.windows), default=0)
+
+    def _compile(self) -> None:
+        self.bytes = {"R_c": 0, "W_c": 0, "R_l": 0, "W_l": 0}
+        for W in self.windows:
+            conv, load, synth = RunTable(), RunTable(), RunTable()
+            src_by_unit, tgt_by_unit = {}, {}
+            for g, i, m, off, n in W.src_frags:
+                src_by_unit.setdefault((m.param, m.kind), []).append((m, off, n))
+            for g, i, m, off, n, dt in W.tgt_frags:
+                tgt_by_unit.setdefault((m.param, m.kind), []).append((m, off))
+            for p in W.params:
+                for k in STATE_KINDS:
+                    a = W.atom[(p.name, k)]
+                    frags = src_by_unit.get((p.name, k), [])
+                    compile_union(conv, p, self.src, frags, a, self.strict)
+                    dt = self.dtype if k == "weight" else DType.F32
+                    compile_extract(load, p, self.tgt, tgt_by_unit.get((p.name, k), []), a, dt)
+                    compile_extract(synth, p, self.src, [(m, off) for m, off, _ in frags], a,
+                                    DType.F32)
+            W.conv = Program(conv, self.device, self.tile_bytes)
+            W.load = Program(load, self.device, self.tile_bytes)
+            W.synth = Program(synth, self.device, self.tile_bytes)
+            self.bytes["R_c"] += conv.src_bytes
+            self.bytes["W_c"] += conv.dst_bytes
+            self.bytes["R_l"] += load.src_bytes
+            self.bytes["W_l"] += load.dst_bytes
+
+    # ------------------------------------------------------------------ sizes
+
+    @property
+    def state_bytes(self) -> int:
+        """S = 12 B x numel (fp32 weight + Adam m + v) of the planned params."""
+        return sum(12 * p.numel for p in self.params)
+
+    @property
+    def hbm_bytes(self) -> int:
+        """Algorithmic HBM traffic of one step: R_c + W_c + R_l + W_l."""
+        return sum(self.bytes.values())
+
+    @property
+    def n_launches(self) -> int:
+        return sum((W.conv.n_tiles > 0) + (W.load.n_tiles > 0) for W in self.windows)
+
+    # ------------------------------------------------------------------ buffers
+
+    def buf(self, key: str, nbytes: int) -> torch.Tensor:
+        b = self._bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            self._bufs.pop(key, None)
+            b = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._bufs[key] = b
+        return b
+
+    def free(self) -> None:
+        self._bufs.clear()
+
+    # ------------------------------------------------------------------ device-resident
+
+    def synthesize(self, seed: int = 7, stream=None) -> torch.Tensor:
+        """Generate init_state(spec, seed) window by window on the GPU and
+        partition it under the source config into the resident source arena
+        (ucp/models.py:230-244 + ucp/partition.py:125-148)."""
+        arena = self.buf("src_arena", self.src_total)
+        atom = self.buf("atom", self.max_atom)
+        for W in self.windows:
+            self.gen_atomic(W, atom, seed, stream)
+            W.synth.launch(False, 0, arena.data_ptr() + W.src_base, self.status, stream)
+        return arena
+
+    def gen_atomic(self, W: Window, atom: torch.Tensor, seed: int, stream=None) -> None:
+        for p in W.params:
+            lead = self.spec.tied_leader(p.name)
+            for k in STATE_KINDS:
+                gen_state(stream_base(seed, lead, k), 0, p.numel, k == "v",
+                          atom.data_ptr() + W.atom[(p.name, k)], stream)
+
+    def step_device(self, stream=None, events=None) -> None:
+        """One device-resident reshard of every window: inputs already in the
+        source arena, targets into a two-slot HBM ring."""
+        arena = self._bufs["src_arena"]
+        atom = self.buf("atom", self.max_atom)
+        ring = [self.buf("tgt0", self.max_tgt), self.buf("tgt1", self.max_tgt)]
+        for i, W in enumerate(self.windows):
+            if events is not None:
+                events[i][0].record(stream)
+            W.conv.launch(True, arena.data_ptr() + W.src_base, atom.data_ptr(), self.status, stream)
+            if events is not None:
+                events[i][1].record(stream)
+            W.load.launch(False, atom.data_ptr(), ring[i % 2].data_ptr(), self.status, stream)
+            if events is not None:
+                events[i][2].record(stream)
+
+    def check(self) -> None:
+        """Raise the reference exception for any data-dependent failure seen
+        since the last status reset (replica mismatch / nonzero pad). The
+        status word is shared by all launches, so a failing window is
+        located by re-running the convert launches one at a time."""
+        first, _ = self.status.read()
+        if first == (1 << 64) - 1:
+            return
+        from .engine import describe_failure
+
+        arena = self._bufs["src_arena"]
+        atom = self.buf("atom", self.max_atom)
+        for W in self.windows:
+            self.status.reset()
+            W.conv.launch(True, arena.data_ptr() + W.src_base, atom.data_ptr(), self.status)
+            torch.cuda.synchronize(self.device)
+            f, _ = self.status.read()
+            if f != (1 << 64) - 1:
+                raise describe_failure(W.conv, f >> 32, f & 0xFFFFFFFF,
+                                       arena.data_ptr() + W.src_base)
+        raise RuntimeError("reshard reported a failure that did not reproduce")
+
+    # ------------------------------------------------------------------ host-streamed
+
+    def pack_host(self, shards: dict, pinned: torch.Tensor | None = None) -> torch.Tensor:
+        """Copy {g: [array per source record]} into a pinned source arena."""
+        host = pinned if pinned is not None else torch.empty(
+            max(self.src_total, 256), dtype=torch.uint8, pin_memory=True)
+        hv = host.numpy()
+        for W in self.windows:
+            for g, i, m, off, n in W.src_frags:
+                a = np.ascontiguousarray(shards[g][i], dtype=np.float32).reshape(-1)
+                if a.size != n:
+                    from ._errors import ShapeError
+
+                    raise ShapeError(f"rank {g} {m.param}.{m.kind}: {a.size} elements, want {n}")
+                at = W.src_base + off
+                hv[at:at + 4 * n] = a.view(np.uint8)
+        return host
+
+    def stream_host(self, host_src: torch.Tensor, host_tgt: torch.Tensor, windows=None,
+                    streams=None) -> None:
+        """Pinned host source arena -> device -> pinned host target arena,
+        double-buffered over windows on three streams. Asynchronous: the
+        caller synchronises (the last event is on the D2H stream)."""
+        wins = self.windows if windows is None else windows
+        s_in, s_cmp, s_out = streams or (torch.cuda.Stream(self.device),
+                                         torch.cuda.Stream(self.device),
+                                         torch.cuda.Stream(self.device))
+        dsrc = [self.buf("ssrc0", self.max_src), self.buf("ssrc1", self.max_src)]
+        dtgt = [self.buf("stgt0", self.max_tgt), self.buf("stgt1", self.max_tgt)]
+        atom = self.buf("atom", self.max_atom)
+        ev_in = [torch.cuda.Event() for _ in wins]
+        ev_cmp = [torch.cuda.Event() for _ in wins]
+        ev_out = [torch.cuda.Event() for _ in wins]
+        for i, W in enumerate(wins):
+            slot = i % 2
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev_cmp[i - 2])
+                dsrc[slot][:W.src_bytes].copy_(host_src[W.src_base:W.src_base + W.src_bytes],
+                                               non_blocking=True)
+                ev_in[i].record(s_in)
+            s_cmp.wait_event(ev_in[i])
+            if i >= 2:
+                s_cmp.wait_event(ev_out[i - 2])
+            W.conv.launch(True, dsrc[slot].data_ptr(), atom.data_ptr(), self.status, s_cmp)
+            W.load.launch(False, atom.data_ptr(), dtgt[slot].data_ptr(), self.status, s_cmp)
+            ev_cmp[i].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[i])
+                host_tgt[W.tgt_base:W.tgt_base + W.tgt_bytes].copy_(dtgt[slot][:W.tgt_bytes],
+                                                                    non_blocking=True)
+                ev_out[i].record(s_out)
+        return ev_out[-1] if wins else None
+
+    def unpack_host(self, host_tgt: torch.Tensor) -> dict:
+        """{g: [array per target record, canonical order]} views of the host
+        target arena."""
+        hv = host_tgt.numpy()
+        out: dict = {}
+        for W in self.windows:
+            for g, i, m, off, n, dt in W.tgt_frags:
+                at = W.tgt_base + off
+                shape = fragment_shape(self.spec.param(m.param), self.tgt, m)
+                out.setdefault(g, {})[i] = hv[at:at + dt.itemsize * n].view(dt.storage).reshape(shape)
+        return {g: [d[i] for i in sorted(d)] for g, d in out.items()}
+
+    def run_host(self, shards: dict) -> dict:
+        """End-to-end in-memory reshard of host arrays; returns target arrays
+        per rank in canonical record order."""
+        host_src = self.pack_host(shards)
+        host_tgt = torch.empty(max(self.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
+        self.status.reset()
+        self.stream_host(host_src, host_tgt)
+        torch.cuda.synchronize(self.device)
+        self._check_windows(host_src)
+        return self.unpack_host(host_tgt)
+
+    def _check_windows(self, host_src=None) -> None:
+        first, _ = self.status.read()
+        if first == (1 << 64) - 1:
+            return
+        from .engine import describe_failure
+
+        # locate the failing convert program by re-running windows one by one
+        dsrc = self.buf("chk_src", self.max_src)
+        atom = self.buf("atom", self.max_atom)
+        for W in self.windows:
+            if host_src is None:
+                break
+            dsrc[:W.src_bytes].copy_(host_src[W.src_base:W.src_base + W.src_bytes])
+            self.status.reset()
+            W.conv.launch(True, dsrc.data_ptr(), atom.data_ptr(), self.status)
+            torch.cuda.synchronize(self.device)
+            f, _ = self.status.read()
+            if f != (1 << 64) - 1:
+                raise describe_failure(W.conv, f >> 32, f & 0xFFFFFFFF, dsrc.data_ptr())
+        raise RuntimeError("reshard reported a failure that did not reproduce")
+
+    # ------------------------------------------------------------------ verification
+
+    def verify(self, seed: int = 7) -> dict:
+        """Full-size, size-independent parity check on the device (outside
+        any timed region), for states synthesised with ``synthesize(seed)``:
+
+        1. convert(partition_src(X)) == X bit for bit, where X is the
+           generator state (the reference's own round-trip identity,
+           SPEC acceptance 1);
+        2. convert_tgt(load(atomic)) == X: the materialised target fragments
+           are a valid checkpoint of the same state under the target layout
+           (needs f32 targets; bf16/f16 weights are lossy by design).
+
+        Returns {"windows": n, "atomic_ok": bool, "target_ok": bool|None}."""
+        arena = self._bufs["src_arena"]
+        atom = self.buf("atom", self.max_atom)
+        ref = self.buf("atom_ref", self.max_atom)
+        back = self.buf("atom_back", self.max_atom)
+        tgt = self.buf("tgt0", self.max_tgt)
+        mism = torch.zeros(1, dtype=torch.int64, device=self.device)
+        from .engine import compare
+
+        atomic_ok, target_ok = True, (self.dtype is DType.F32) or None
+        for W in self.windows:
+            self.status.reset()
+            W.conv.launch(True, arena.data_ptr() + W.src_base, atom.data_ptr(), self.status)
+            self.gen_atomic(W, ref, seed)
+            compare(atom.data_ptr(), ref.data_ptr(), W.atom_bytes, mism)
+            torch.cuda.synchronize(self.device)
+            self.check()
+            if int(mism.item()) != -1:
+                atomic_ok = False
+            if target_ok:
+                W.load.launch(False, atom.data_ptr(), tgt.data_ptr(), self.status)
+                rev = self._reverse(W)
+                rev.launch(True, tgt.data_ptr(), back.data_ptr(), self.status)
+                compare(back.data_ptr(), ref.data_ptr(), W.atom_bytes, mism)
+                torch.cuda.synchronize(self.device)
+                if int(mism.item()) != -1:
+                    target_ok = False
+        return {"windows": len(self.windows), "atomic_ok": atomic_ok, "target_ok": target_ok}
+
+    def _reverse(self, W: Window) -> Program:
+        rev = getattr(W, "_rev", None)
+        if rev is None:
+            tab = RunTable()
+            by_unit = {}
+            for g, i, m, off, n, dt in W.tgt_frags:
+                by_unit.setdefault((m.param, m.kind), []).append((m, off, n))
+            for p in W.params:
+                for k in STATE_KINDS:
+                    compile_union(tab, p, self.tgt, by_unit.get((p.name, k), []),
+                                  W.atom[(p.name, k)], True)
+            rev = W._rev = Program(tab, self.device, self.tile_bytes)
+        return rev

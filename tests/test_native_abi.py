@@ -1,0 +1,50 @@
+"""The C-ABI library loads and exports exactly what include/ucp_b200.h
+declares (no GPU needed: no compute calls)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+from paper_2406_18820_b200 import _native
+from paper_2406_18820_b200.plan import RUN_DTYPE, TILE_DTYPE
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                   "ucp_b200.h")
+
+
+def _declared():
+    text = open(HDR).read()
+    return sorted(set(re.findall(r"^int\s+(ucp_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.load_library()
+    names = _declared()
+    assert names == sorted(_native.EXPORTS)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert lib.ucp_version() == _native.ABI_VERSION
+
+
+def test_abi_constants_match_header():
+    text = open(HDR).read()
+    assert int(re.search(r"#define UCP_ABI_VERSION (\d+)", text).group(1)) == _native.ABI_VERSION
+    from paper_2406_18820_b200 import _errors, plan
+    consts = dict(re.findall(r"#define (UCP_\w+) \(?(-?\d+)u?\)?", text))
+    assert int(consts["UCP_EREPLICA"]) == _errors.STATUS_REPLICA
+    assert int(consts["UCP_EPAD"]) == _errors.STATUS_PAD
+    assert int(consts["UCP_OP_MEAN"]) == plan.OP_MEAN
+    assert int(consts["UCP_OP_NOISE"]) == plan.OP_NOISE
+    assert int(consts["UCP_OP_CHECKZERO"]) == plan.OP_CHECKZERO
+    assert RUN_DTYPE.itemsize == 64 and TILE_DTYPE.itemsize == 16
+
+
+def test_argument_errors_without_device():
+    lib = _native.load_library()
+    # invalid arguments are rejected before any CUDA call
+    assert lib.ucp_convert_gather(None, 0, None, None, -1, None, None, None, None) == -10
+    assert lib.ucp_load_scatter(None, 0, None, None, 0, None, None, None, None) == 0
+    assert lib.ucp_gen_state(0, 0, 0, 0, None, None) == 0
+    assert lib.ucp_status_reset(None, None) == -10

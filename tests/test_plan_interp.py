@@ -1,0 +1,241 @@
+"""Descriptor compiler + tiler == oracle, executed by the numpy interpreter.
+
+CPU-only proof that the run tables the GPU executes encode the reference's
+union / extract_fragment / cast semantics for every golden cell, with tiny
+tiles so column-split, row-block, head/tail and misaligned paths all occur.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2406_18820_b200 as U
+from descr_interp import execute
+from helpers import cell_cfgs, cell_spec
+from oracle import ucp_oracle as O
+from paper_2406_18820_b200.engine import align_up
+from paper_2406_18820_b200.layout import all_rank_records
+from paper_2406_18820_b200.plan import (
+    RunTable,
+    compile_extract,
+    compile_union,
+    fragment_elems,
+    make_tiles,
+    split_rows,
+)
+from paper_2406_18820_b200.spec import STATE_KINDS, DType, ParallelConfig, ParamKind, ParamSpec, RecordMeta, ZeroStage
+
+CELLS = ["pad", "gqa", "moe"] + [f"{f}.{i}" for f in ("DenseGPT", "MoE", "GQA") for i in range(6)]
+
+
+def _arena_union(spec, cfg, shards, strict=True, tile_bytes=4096):
+    """Product union of every (param, kind) through the interpreter."""
+    recs = all_rank_records(spec, cfg)
+    frags, blobs, at = {}, [], 0
+    for g in range(cfg.world_size):
+        assert len(recs[g]) == len(shards[g])
+        for meta, (orec, arr) in zip(recs[g], shards[g]):
+            assert O.record_tuple(meta) == O.record_tuple(orec)
+            frags.setdefault((meta.param, meta.kind), []).append((meta, at, arr.size))
+            blobs.append((at, arr))
+            at += align_up(arr.nbytes)
+    src = np.zeros(max(at, 16), dtype=np.uint8)
+    for o, a in blobs:
+        src[o:o + a.nbytes] = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
+    tab, outs, dat = RunTable(), [], 0
+    for p in spec.params:
+        for k in STATE_KINDS:
+            compile_union(tab, p, cfg, frags[(p.name, k)], dat, strict)
+            outs.append((p, k, dat))
+            dat += align_up(4 * p.numel)
+    runs, aux, tiles = tab.finish(tile_bytes)
+    dst = np.full(max(dat, 16), 0xAB, dtype=np.uint8)
+    fails = execute(runs, aux, tiles, src, dst)
+    return {(p.name, k): dst[o:o + 4 * p.numel].view(np.float32).reshape(p.shape)
+            for p, k, o in outs}, fails, tab
+
+
+def _arena_extract(spec, cfg, atomic, dtype, tile_bytes=4096):
+    src_blobs, at, soff = [], 0, {}
+    for p in spec.params:
+        for k in STATE_KINDS:
+            soff[(p.name, k)] = at
+            src_blobs.append((at, atomic[p.name][k]))
+            at += align_up(4 * p.numel)
+    src = np.zeros(max(at, 16), dtype=np.uint8)
+    for o, a in src_blobs:
+        src[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
+    recs = all_rank_records(spec, cfg)
+    by_unit, outs, tat = {}, [], 0
+    for g in range(cfg.world_size):
+        for m in recs[g]:
+            p = spec.param(m.param)
+            odt = dtype if m.kind == "weight" else DType.F32
+            n = fragment_elems(p, cfg, m)
+            by_unit.setdefault((m.param, m.kind), []).append((m, tat))
+            outs.append((g, m, tat, n, odt))
+            tat += align_up(n * odt.itemsize)
+    tab = RunTable()
+    for p in spec.params:
+        for k in STATE_KINDS:
+            odt = dtype if k == "weight" else DType.F32
+            compile_extract(tab, p, cfg, by_unit.get((p.name, k), []), soff[(p.name, k)], odt)
+    runs, aux, tiles = tab.finish(tile_bytes)
+    dst = np.full(max(tat, 16), 0xCD, dtype=np.uint8)
+    assert execute(runs, aux, tiles, src, dst) == []
+    world = {}
+    for g, m, o, n, odt in outs:
+        world.setdefault(g, []).append((m, dst[o:o + n * odt.itemsize].view(odt.storage).copy()))
+    return world, tab
+
+
+@pytest.mark.parametrize("name", CELLS)
+def test_union_matches_oracle(golden, name):
+    row = next(r for r in golden["pipelines"] if r["name"] == name)
+    spec = cell_spec(golden, row)
+    src_cfg, _ = cell_cfgs(row)
+    shards = O.partition_mem(spec, O.init_state(spec, 7), src_cfg)
+    want = O.convert_mem(spec, src_cfg, shards)
+    got, fails, _ = _arena_union(spec, src_cfg, shards)
+    assert fails == []
+    for p in spec.params:
+        for k in STATE_KINDS:
+            assert np.array_equal(got[(p.name, k)].view(np.uint32),
+                                  want[p.name][k].view(np.uint32)), (p.name, k)
+
+
+@pytest.mark.parametrize("name", CELLS)
+@pytest.mark.parametrize("dtype", ["F32", "BF16", "F16"])
+def test_extract_matches_golden_world(golden, name, dtype):
+    row = next(r for r in golden["pipelines"] if r["name"] == name)
+    spec = cell_spec(golden, row)
+    _, tgt_cfg = cell_cfgs(row)
+    atomic = O.init_state(spec, 7)
+    world, _ = _arena_extract(spec, tgt_cfg, atomic, DType[dtype])
+    # rebuild the digest in canonical order with shapes from the records
+    fixed = {}
+    for g, items in world.items():
+        fixed[g] = []
+        for m, a in items:
+            p = spec.param(m.param)
+            shape = U.plan.fragment_shape(p, tgt_cfg, m)
+            fixed[g].append((m, a.reshape(shape)))
+    assert O.world_digest(fixed) == row[f"world_{dtype}"]
+
+
+def test_union_reports_bad_replica_and_pad():
+    spec = U.make_model("DenseGPT", {"n_layers": 2, "hidden": 32})
+    cfg = ParallelConfig(dp=3, tp=1, zero_stage=ZeroStage.Z1)
+    shards = O.partition_mem(spec, O.init_state(spec, 7), cfg)
+    # corrupt a weight replica on dp 2 and a pad element on the last dp rank
+    for i, (r, a) in enumerate(shards[2]):
+        if r["param"] == "layers.1.ln_w" and r["kind"] == "weight":
+            a = a.copy()
+            a[3] = np.float32(9.0)
+            shards[2][i] = (r, a)
+    _, fails, tab = _arena_union(spec, cfg, shards)
+    assert fails and tab.units[int(tab.finish()[0][fails[0][0]]["tag"])].param == "layers.1.ln_w"
+
+
+def _meta(p, kind="weight", pattern="replicate", placement=(0, 0, 0), shape=None,
+          segments=None, flat_range=None, pad_elems=0):
+    return RecordMeta(p.name, kind, pattern, placement, shape if shape is not None else p.shape,
+                      segments, flat_range, pad_elems)
+
+
+@pytest.mark.parametrize("case,err", [
+    ("empty", U.MissingFragmentError),
+    ("missing_tp", U.MissingFragmentError),
+    ("overlap", U.OverlappingRangeError),
+    ("gap", U.MissingFragmentError),
+    ("dup_dp", U.OverlappingRangeError),
+    ("mixed_flat", U.ManifestError),
+    ("mixed_kind", U.ManifestError),
+    ("tags", U.ManifestError),
+    ("stages", U.ManifestError),
+    ("pad_nonfinal", U.PaddingError),
+    ("pad_arith", U.PaddingError),
+    ("nc_segs", U.ManifestError),
+    ("missing_dp", U.MissingFragmentError),
+])
+def test_union_metadata_errors(case, err):
+    # mirrors pkg/tests/test_convert.py:143-205 plus the remaining branches of
+    # ucp/convert.py:137-193, :232-262
+    ln4 = ParamSpec("ln", (4,), 0, ParamKind.LAYERNORM_WEIGHT)
+    ln6 = ParamSpec("ln", (6,), 0, ParamKind.LAYERNORM_WEIGHT)
+    w = ParamSpec("w", (4, 2), 0, ParamKind.MATMUL2D, 0)
+    z3 = lambda dp: ParallelConfig(dp=dp, zero_stage=ZeroStage.Z3)
+    qkv = ParamSpec("qkv", (6, 2), 0, ParamKind.FUSED_QKV, 0, ((0, 4), (4, 2)))
+    cases = {
+        "empty": (w, ParallelConfig(), []),
+        "missing_tp": (w, ParallelConfig(tp=2), [(_meta(w, pattern="shard_v", shape=(2, 2)), 0, 4)]),
+        "overlap": (ln4, z3(2), [(_meta(ln4, pattern="shard_v", shape=(2,), flat_range=(0, 2)), 0, 2),
+                                 (_meta(ln4, pattern="shard_v", placement=(0, 0, 1), shape=(2,),
+                                        flat_range=(1, 3)), 256, 2)]),
+        "gap": (ln6, z3(3), [(_meta(ln6, pattern="shard_v", shape=(2,), flat_range=(0, 2)), 0, 2),
+                             (_meta(ln6, pattern="shard_v", placement=(0, 0, 2), shape=(2,),
+                                    flat_range=(4, 6)), 256, 2),
+                             (_meta(ln6, pattern="shard_v", placement=(0, 0, 1), shape=(2,),
+                                    flat_range=(4, 6)), 512, 2)]),
+        "dup_dp": (ln4, ParallelConfig(dp=2), [(_meta(ln4), 0, 4), (_meta(ln4), 256, 4),
+                                               (_meta(ln4, placement=(0, 0, 1)), 512, 4)]),
+        "mixed_flat": (ln4, z3(2), [(_meta(ln4, pattern="shard_v", shape=(2,), flat_range=(0, 2)), 0, 2),
+                                    (_meta(ln4, pattern="shard_v", placement=(0, 0, 1)), 256, 4)]),
+        "mixed_kind": (ln4, ParallelConfig(), [(_meta(ln4), 0, 4), (_meta(ln4, kind="m"), 256, 4)]),
+        "tags": (ln4, ParallelConfig(dp=2), [(_meta(ln4), 0, 4),
+                                             (_meta(ln4, pattern="unique", placement=(0, 0, 1)), 256, 4)]),
+        "stages": (ln4, ParallelConfig(dp=2), [(_meta(ln4), 0, 4), (_meta(ln4, placement=(1, 0, 1)), 256, 4)]),
+        "pad_nonfinal": (ln6, z3(2), [(_meta(ln6, pattern="shard_v", shape=(3,), flat_range=(0, 3),
+                                             pad_elems=1), 0, 3),
+                                      (_meta(ln6, pattern="shard_v", placement=(0, 0, 1), shape=(3,),
+                                             flat_range=(3, 6)), 256, 3)]),
+        "pad_arith": (ln4, z3(2), [(_meta(ln4, pattern="shard_v", shape=(2,), flat_range=(0, 2)), 0, 2),
+                                   (_meta(ln4, pattern="shard_v", placement=(0, 0, 1), shape=(2,),
+                                          flat_range=(2, 4), pad_elems=1), 256, 2)]),
+        "nc_segs": (qkv, ParallelConfig(tp=2), [
+            (_meta(qkv, pattern="shard_nc", placement=(0, t, 0), shape=(3, 2), segments=((0, 6),)),
+             256 * t, 6) for t in range(2)]),
+        "missing_dp": (ln4, ParallelConfig(dp=2), [(_meta(ln4), 0, 4)]),
+    }
+    p, cfg, frags = cases[case]
+    with pytest.raises(err):
+        compile_union(RunTable(), p, cfg, frags, 0, True)
+
+
+def test_split_rows_covers_interval():
+    corr = (10, 1000, 64, 7, 5)  # frag [10, 45) -> 7 rows of 5 at pitch 64
+    for a in range(10, 45):
+        for b in range(a + 1, 46):
+            pieces = split_rows(corr, a, b)
+            covered = []
+            for fs, xs, xp, rows, cols in pieces:
+                for i in range(rows):
+                    for j in range(cols):
+                        f = fs + i * cols + j
+                        r, c = divmod(f - 10, 5)
+                        assert xs + i * xp + j == 1000 + r * 64 + c
+                        covered.append(f)
+            assert covered == list(range(a, min(b, 45)))
+
+
+def test_tiles_cover_every_element_once():
+    from paper_2406_18820_b200.plan import RUN_ROWSPLIT
+
+    tab = RunTable()
+    tab.unit("x", "weight")
+    tab.add(srcs=[0], dsts=[0], src_pitch=3000, dst_pitch=3000, rows=5, cols=3000, tag=0)
+    tab.add(srcs=[4], dsts=[8], src_pitch=7, dst_pitch=9, rows=1000, cols=7, tag=0)
+    tab.add(srcs=[12], dsts=[12, 4096], src_pitch=10 ** 6, dst_pitch=10 ** 6, rows=1,
+            cols=10 ** 6, tag=0)
+    base, _, _ = tab.finish()
+    for tb in (2048, 1 << 15, 1 << 17, 1 << 24):
+        runs = base.copy()
+        tiles = make_tiles(runs, tb)
+        for i, r in enumerate(runs):
+            cover = np.zeros((int(r["rows"]), int(r["cols"])), dtype=np.int32)
+            for t in tiles[tiles["run"] == i]:
+                if r["flags"] & RUN_ROWSPLIT:
+                    cover[t["row0"], t["col0"]:t["col0"] + t["count"]] += 1
+                else:
+                    assert t["col0"] == 0
+                    cover[t["row0"]:t["row0"] + t["count"], :] += 1
+            assert (cover == 1).all(), (tb, i)

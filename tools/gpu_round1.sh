@@ -1,0 +1,11 @@
+#!/bin/bash
+# first GPU pass: build check, smoke, gpu tests, small + full bench
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
+tail -5 gpurun_out/gpu_tests.log
+timeout 600 python bench.py --layers 2 --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_small.log 2>&1; echo "small rc=$?"
+tail -3 gpurun_out/bench_small.log
+timeout 1500 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_full.log 2>&1; echo "full rc=$?"
+tail -3 gpurun_out/bench_full.log
