@@ -187,7 +187,7 @@ class ReshardPlan:
         atom = self.buf("atom", self.max_atom)
         for W in self.windows:
             self.gen_atomic(W, atom, seed, stream)
-            W.synth.launch(False, 0, arena.data_ptr() + W.src_base, self.status, stream)
+            W.synth.launch(False, atom.data_ptr(), arena.data_ptr() + W.src_base, self.status, stream)
         return arena
 
     def gen_atomic(self, W: Window, atom: torch.Tensor, seed: int, stream=None) -> None:

@@ -311,8 +311,9 @@ def test_reshard_plan_device_verify_llama_slice():
     sub = ReshardPlan(spec, src, tgt, params=list(atomic_full))
     shards = {}
     for g in range(src.world_size):
-        shards[g] = [O.extract(spec.param(m.param), src, m, atomic_full[m.param][m.kind])
-                     for m in U.enumerate_rank_records(spec, src, g) if m.param in atomic_full]
+        shards[g] = {i: O.extract(spec.param(m.param), src, m, atomic_full[m.param][m.kind])
+                     for i, m in enumerate(U.enumerate_rank_records(spec, src, g))
+                     if m.param in atomic_full}
     out = sub.run_host(shards)
     for g in range(tgt.world_size):
         recs = [m for m in U.enumerate_rank_records(spec, tgt, g) if m.param in atomic_full]
