@@ -60,6 +60,13 @@ extern "C" {
 #define UCP_DT_F16 1
 #define UCP_DT_BF16 2
 
+/* tile classes: tiles are sorted by class, each class runs its own kernel */
+#define UCP_CLASS_VEC_F32 0   /* COPY, UCP_RUN_VEC, f32 destinations */
+#define UCP_CLASS_VEC_BF16 1  /* COPY, UCP_RUN_VEC, bf16 destinations */
+#define UCP_CLASS_VEC_F16 2   /* COPY, UCP_RUN_VEC, f16 destinations */
+#define UCP_CLASS_GENERAL 3   /* everything else (MEAN/NOISE/ZERO/CHECKZERO, scalar runs) */
+#define UCP_NCLASS 4
+
 /* run flags */
 #define UCP_RUN_VEC 1u       /* every src/dst row start shares one 16-B phase */
 #define UCP_RUN_ROWSPLIT 2u  /* tiles cut columns of single rows */
@@ -106,10 +113,11 @@ int ucp_status_reset(ucp_status* status, void* stream);
 /*
  * Consolidate fragments into atomic tensors (union). One launch covers any
  * number of (param, kind) units. src_base: base of the source-fragment arena;
- * dst_base: base of the atomic arena. aux: n_aux uint64 byte offsets.
+ * dst_base: base of the atomic arena. aux: uint64 byte offsets. tiles: device
+ * array sorted by class; class_counts: HOST array of UCP_NCLASS tile counts.
  */
 int ucp_convert_gather(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                       const ucp_tile* tiles, int64_t n_tiles, const void* src_base,
+                       const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
                        void* dst_base, ucp_status* status, void* stream);
 
 /*
@@ -117,7 +125,7 @@ int ucp_convert_gather(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
  * partial noise + weight cast), fanning each read out to n_dst replicas.
  */
 int ucp_load_scatter(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                     const ucp_tile* tiles, int64_t n_tiles, const void* src_base,
+                     const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
                      void* dst_base, ucp_status* status, void* stream);
 
 /*

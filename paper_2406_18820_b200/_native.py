@@ -28,8 +28,8 @@ _P = _c.c_void_p
 _SIGS = {
     "ucp_version": (_c.c_int, []),
     "ucp_status_reset": (_c.c_int, [_P, _P]),
-    "ucp_convert_gather": (_c.c_int, [_P, _c.c_int64, _P, _P, _c.c_int64, _P, _P, _P, _P]),
-    "ucp_load_scatter": (_c.c_int, [_P, _c.c_int64, _P, _P, _c.c_int64, _P, _P, _P, _P]),
+    "ucp_convert_gather": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
+    "ucp_load_scatter": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "ucp_gen_state": (_c.c_int, [_c.c_uint64, _c.c_uint64, _c.c_uint64, _c.c_int, _P, _P]),
     "ucp_compare": (_c.c_int, [_P, _P, _c.c_uint64, _P, _P]),
     "ucp_peek": (_c.c_int, [_P, _P, _c.c_uint64]),

@@ -303,24 +303,9 @@ __device__ __forceinline__ void general(const Ctx& c, uint64_t srow, uint64_t dr
   else op_general<W, U>(c, srow, drow, e, ok, ebase, st);
 }
 
-// Plain 1:1 f32 copy of vector slots (the dominant case): all loads in
-// flight before the first store.
-__device__ __forceinline__ void fast_copy(const Ctx& c, uint64_t srow, uint64_t drow,
-                                          const uint32_t (&e)[kVec], const bool (&ok)[kVec]) {
-  const char* s0 = c.sb + c.r->src + 4 * srow;
-  char* d0 = c.db + c.r->dst + 4 * drow;
-  float4 v[kVec];
-#pragma unroll
-  for (int u = 0; u < kVec; ++u)
-    if (ok[u]) v[u] = ld_stream4(s0 + 4ull * e[u]);
-#pragma unroll
-  for (int u = 0; u < kVec; ++u)
-    if (ok[u]) st4(d0 + 4ull * e[u], v[u]);
-}
-
-// One warp processes columns [cs, cs+len) of one row.
+// One warp processes columns [cs, cs+len) of one row (general kernel).
 __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs, uint32_t len,
-                                        bool fast, ucp_status* st) {
+                                        ucp_status* st) {
   const ucp_run& r = *c.r;
   const int lane = threadIdx.x & 31;
   const uint64_t srow = (uint64_t)row * r.src_pitch + cs;
@@ -345,8 +330,7 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
         ok[u] = vi < nvec;
         e[u] = head + 4u * vi;
       }
-      if (fast) fast_copy(c, srow, drow, e, ok);
-      else general<4, kVec>(c, srow, drow, e, ok, ebase, st);
+      general<4, kVec>(c, srow, drow, e, ok, ebase, st);
     }
     // scalar head + tail (<= 6 elements)
     if (head + tail > 0) {
@@ -372,15 +356,17 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
   }
 }
 
-template <bool kGather>
-__device__ __forceinline__ void move_body(const ucp_run* __restrict__ runs,
-                                          const uint64_t* __restrict__ aux,
-                                          const ucp_tile* __restrict__ tiles,
-                                          const char* __restrict__ src_base,
-                                          char* __restrict__ dst_base, ucp_status* st) {
-  __shared__ ucp_run s_run;
-  __shared__ uint64_t s_aux[kMaxAux];
-  const ucp_tile tile = tiles[blockIdx.x];
+// ---------------------------------------------------------------- tile prologue
+
+struct TileGeom {
+  uint32_t row0, col0, nr, nc, spr, n_items;
+};
+
+// Load the tile's run (and its aux offsets) into shared memory.
+__device__ __forceinline__ TileGeom tile_prologue(const ucp_run* __restrict__ runs,
+                                                  const uint64_t* __restrict__ aux,
+                                                  const ucp_tile& tile, ucp_run& s_run,
+                                                  uint64_t* s_aux) {
   if (threadIdx.x < 4) {
     reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
         reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
@@ -391,37 +377,147 @@ __device__ __forceinline__ void move_body(const ucp_run* __restrict__ runs,
     for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
     __syncthreads();
   }
-  const Ctx c{&s_run, s_aux, src_base, dst_base, tile.run};
-  const bool fast = s_run.op == UCP_OP_COPY && s_run.n_src == 1 && s_run.n_dst == 1 &&
-                    s_run.dtype == UCP_DT_F32;
+  TileGeom g;
+  g.row0 = tile.row0;
+  g.col0 = tile.col0;
+  if (s_run.flags & UCP_RUN_ROWSPLIT) { g.nr = 1; g.nc = tile.count; }
+  else { g.nr = tile.count; g.nc = s_run.cols; }
+  g.spr = (g.nc + kSeg - 1) / kSeg;
+  g.n_items = g.nr * g.spr;
+  return g;
+}
 
-  uint32_t nr, nc;
-  if (s_run.flags & UCP_RUN_ROWSPLIT) { nr = 1; nc = tile.count; }
-  else { nr = tile.count; nc = s_run.cols; }
-  const uint32_t spr = (nc + kSeg - 1) / kSeg;
-  const uint32_t n_items = nr * spr;
-  const uint32_t warp = threadIdx.x >> 5;
-  for (uint32_t it = warp; it < n_items; it += kWarps) {
-    const uint32_t rr = spr == 1 ? it : it / spr;
-    const uint32_t ss = it - rr * spr;
-    const uint32_t cs = tile.col0 + ss * kSeg;
-    const uint32_t ce = min(cs + kSeg, tile.col0 + nc);
-    segment(c, tile.row0 + rr, cs, ce - cs, fast, st);
+// ---------------------------------------------------------------- vector kernel
+//
+// COPY runs whose sources and destinations share one 16-B phase
+// (UCP_RUN_VEC): n_src >= 1 bit-identical replicas (strict check), n_dst
+// destinations (fan-out), destination dtype DT. This is >99.9% of the bytes of
+// every BASELINE config. Register budget: 4 float4 of primary + 4 float4 of
+// replica per lane, no local memory.
+
+template <int DT>
+__device__ __forceinline__ void store4(char* p, const float4& v) {
+  if constexpr (DT == UCP_DT_F32) {
+    st4(p, v);
+  } else {
+    uint2 h;
+    h.x = cvt16(v.x, DT) | (cvt16(v.y, DT) << 16);
+    h.y = cvt16(v.z, DT) | (cvt16(v.w, DT) << 16);
+    *reinterpret_cast<uint2*>(p) = h;
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
-convert_gather_kernel(const ucp_run* __restrict__ runs, const uint64_t* __restrict__ aux,
-                      const ucp_tile* __restrict__ tiles, const char* __restrict__ src_base,
-                      char* __restrict__ dst_base, ucp_status* st) {
-  move_body<true>(runs, aux, tiles, src_base, dst_base, st);
+template <int DT>
+__device__ __forceinline__ void store1(char* p, float v) {
+  if constexpr (DT == UCP_DT_F32) *reinterpret_cast<float*>(p) = v;
+  else *reinterpret_cast<uint16_t*>(p) = (uint16_t)cvt16(v, DT);
 }
 
+__device__ __forceinline__ int diff4(const float4& a, const float4& b) {
+  if (bits_of(a.x) != bits_of(b.x)) return 0;
+  if (bits_of(a.y) != bits_of(b.y)) return 1;
+  if (bits_of(a.z) != bits_of(b.z)) return 2;
+  if (bits_of(a.w) != bits_of(b.w)) return 3;
+  return 4;
+}
+
+template <int DT>
 __global__ void __launch_bounds__(kThreads, 4)
-load_scatter_kernel(const ucp_run* __restrict__ runs, const uint64_t* __restrict__ aux,
-                    const ucp_tile* __restrict__ tiles, const char* __restrict__ src_base,
-                    char* __restrict__ dst_base, ucp_status* st) {
-  move_body<false>(runs, aux, tiles, src_base, dst_base, st);
+vec_kernel(const ucp_run* __restrict__ runs, const uint64_t* __restrict__ aux,
+           const ucp_tile* __restrict__ tiles, const char* __restrict__ sb,
+           char* __restrict__ db, ucp_status* st) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  __shared__ ucp_run s_run;
+  __shared__ uint64_t s_aux[kMaxAux];
+  const ucp_tile tile = tiles[blockIdx.x];
+  const TileGeom g = tile_prologue(runs, aux, tile, s_run, s_aux);
+  const int ns = s_run.n_src, nd = s_run.n_dst;
+  const uint64_t s0 = s_run.src, d0 = s_run.dst;
+  const uint32_t sp = s_run.src_pitch, dpch = s_run.dst_pitch, cols = s_run.cols;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
+    const uint32_t rr = g.spr == 1 ? it : it / g.spr;
+    const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, g.col0 + g.nc) - cs;
+    const uint32_t row = g.row0 + rr;
+    const uint64_t srow = (uint64_t)row * sp + cs;
+    const uint64_t drow = (uint64_t)row * dpch + cs;
+    const uint32_t phase = (uint32_t)(((s0 >> 2) + srow) & 3);
+    uint32_t head = (4u - phase) & 3u;
+    if (head > len) head = len;
+    const uint32_t nvec = (len - head) >> 2;
+    const uint32_t tail = len - head - 4 * nvec;
+    bool bad = false;
+    uint32_t bad_e = 0xffffffffu;
+
+    // vector body: lane owns vectors lane + 32u
+    const uint64_t so = 4 * (srow + head), dofs = (uint64_t)ESZ * (drow + head);
+    float4 v[kVec];
+#pragma unroll
+    for (int u = 0; u < kVec; ++u)
+      if (lane + 32u * u < nvec) v[u] = ld_stream4(sb + s0 + so + 16ull * (lane + 32u * u));
+    for (int k = 1; k < ns; ++k) {
+      const char* pk = sb + s_aux[k - 1] + so;
+      float4 w[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (lane + 32u * u < nvec) w[u] = ld_stream4(pk + 16ull * (lane + 32u * u));
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        if (lane + 32u * u < nvec) {
+          const int d = diff4(v[u], w[u]);
+          if (d < 4) { bad = true; bad_e = min(bad_e, head + 4 * (lane + 32u * u) + d); }
+        }
+      }
+    }
+    for (int d = 0; d < nd; ++d) {
+      char* pd = db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + dofs;
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (lane + 32u * u < nvec) store4<DT>(pd + (uint64_t)ESZ * 4 * (lane + 32u * u), v[u]);
+    }
+
+    // scalar head + tail (<= 6 elements, lanes 0..head+tail-1)
+    if (head + tail) {
+      const bool ok = lane < head + tail;
+      const uint32_t e = lane < head ? lane : head + 4 * nvec + (lane - head);
+      float x = 0.0f;
+      if (ok) x = ld_stream1(sb + s0 + 4 * (srow + e));
+      for (int k = 1; k < ns; ++k) {
+        if (ok) {
+          const float y = ld_stream1(sb + s_aux[k - 1] + 4 * (srow + e));
+          if (bits_of(x) != bits_of(y)) { bad = true; bad_e = min(bad_e, e); }
+        }
+      }
+      for (int d = 0; d < nd; ++d)
+        if (ok) store1<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + (uint64_t)ESZ * (drow + e), x);
+    }
+    report(bad, row * cols + cs + bad_e, tile.run, st);
+  }
+}
+
+// ---------------------------------------------------------------- general kernel
+//
+// Everything else: MEAN / NOISE / ZERO / CHECKZERO runs and phase-mismatched
+// runs (scalar path). Tiny by bytes (Partial vectors, pads, dp=3 cells).
+
+__global__ void __launch_bounds__(kThreads)
+general_kernel(const ucp_run* __restrict__ runs, const uint64_t* __restrict__ aux,
+               const ucp_tile* __restrict__ tiles, const char* __restrict__ sb,
+               char* __restrict__ db, ucp_status* st) {
+  __shared__ ucp_run s_run;
+  __shared__ uint64_t s_aux[kMaxAux];
+  const ucp_tile tile = tiles[blockIdx.x];
+  const TileGeom g = tile_prologue(runs, aux, tile, s_run, s_aux);
+  const Ctx c{&s_run, s_aux, sb, db, tile.run};
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
+    const uint32_t rr = it / g.spr;
+    const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
+    const uint32_t ce = min(cs + kSeg, g.col0 + g.nc);
+    segment(c, g.row0 + rr, cs, ce - cs, st);
+  }
 }
 
 // ---------------------------------------------------------------- generator
@@ -474,22 +570,33 @@ compare_kernel(const unsigned char* a, const unsigned char* b, uint64_t n,
   }
 }
 
-int launch_move(bool gather, const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                const ucp_tile* tiles, int64_t n_tiles, const void* src_base, void* dst_base,
+int launch_move(const ucp_run* runs, int64_t n_runs, const uint64_t* aux, const ucp_tile* tiles,
+                const int64_t* class_counts, const void* src_base, void* dst_base,
                 ucp_status* status, void* stream) {
-  if (n_tiles < 0 || n_runs < 0) return UCP_EINVAL;
-  if (n_tiles == 0) return UCP_OK;
-  if (!runs || !tiles || !status || n_tiles > 0x7fffffffLL) return UCP_EINVAL;
+  if (n_runs < 0 || !class_counts) return UCP_EINVAL;
+  int64_t total = 0;
+  for (int c = 0; c < UCP_NCLASS; ++c) {
+    if (class_counts[c] < 0 || class_counts[c] > 0x7fffffffLL) return UCP_EINVAL;
+    total += class_counts[c];
+  }
+  if (total == 0) return UCP_OK;
+  if (!runs || !tiles || !status) return UCP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const dim3 grid((unsigned)n_tiles), block(kThreads);
-  if (gather) {
-    convert_gather_kernel<<<grid, block, 0, s>>>(runs, aux, tiles,
-                                                 static_cast<const char*>(src_base),
-                                                 static_cast<char*>(dst_base), status);
-  } else {
-    load_scatter_kernel<<<grid, block, 0, s>>>(runs, aux, tiles,
-                                               static_cast<const char*>(src_base),
-                                               static_cast<char*>(dst_base), status);
+  const char* sb = static_cast<const char*>(src_base);
+  char* db = static_cast<char*>(dst_base);
+  int64_t at = 0;
+  for (int c = 0; c < UCP_NCLASS; ++c) {
+    const int64_t n = class_counts[c];
+    if (n == 0) continue;
+    const dim3 grid((unsigned)n), block(kThreads);
+    const ucp_tile* t = tiles + at;
+    switch (c) {
+      case UCP_CLASS_VEC_F32: vec_kernel<UCP_DT_F32><<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
+      case UCP_CLASS_VEC_BF16: vec_kernel<UCP_DT_BF16><<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
+      case UCP_CLASS_VEC_F16: vec_kernel<UCP_DT_F16><<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
+      default: general_kernel<<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
+    }
+    at += n;
   }
   return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
 }
@@ -520,15 +627,15 @@ int ucp_status_reset(ucp_status* status, void* stream) {
 }
 
 int ucp_convert_gather(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                       const ucp_tile* tiles, int64_t n_tiles, const void* src_base,
+                       const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
                        void* dst_base, ucp_status* status, void* stream) {
-  return launch_move(true, runs, n_runs, aux, tiles, n_tiles, src_base, dst_base, status, stream);
+  return launch_move(runs, n_runs, aux, tiles, class_counts, src_base, dst_base, status, stream);
 }
 
 int ucp_load_scatter(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                     const ucp_tile* tiles, int64_t n_tiles, const void* src_base,
+                     const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
                      void* dst_base, ucp_status* status, void* stream) {
-  return launch_move(false, runs, n_runs, aux, tiles, n_tiles, src_base, dst_base, status, stream);
+  return launch_move(runs, n_runs, aux, tiles, class_counts, src_base, dst_base, status, stream);
 }
 
 int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, float* out,

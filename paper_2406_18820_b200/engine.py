@@ -46,8 +46,9 @@ class Program:
     """One kernel launch worth of runs/aux/tiles, resident on a device."""
 
     def __init__(self, table: RunTable, device: torch.device, tile_bytes: int = 1 << 17):
-        runs, aux, tiles = table.finish(tile_bytes)
+        runs, aux, tiles, counts = table.finish_classed(tile_bytes)
         self.runs_host, self.aux_host, self.tiles_host = runs, aux, tiles
+        self.class_counts = np.ascontiguousarray(counts, dtype=np.int64)
         self.units = table.units
         self.src_bytes, self.dst_bytes = table.src_bytes, table.dst_bytes
         self.n_runs, self.n_tiles = len(runs), len(tiles)
@@ -68,8 +69,8 @@ class Program:
         lib = _native.lib()
         fn = lib.ucp_convert_gather if gather else lib.ucp_load_scatter
         rc = fn(self._runs.data_ptr(), self.n_runs, self._aux.data_ptr(), self._tiles.data_ptr(),
-                self.n_tiles, ctypes.c_void_p(src_base), ctypes.c_void_p(dst_base),
-                status.ptr, stream_ptr(stream))
+                self.class_counts.ctypes.data, ctypes.c_void_p(src_base),
+                ctypes.c_void_p(dst_base), status.ptr, stream_ptr(stream))
         _check(rc, "convert_gather" if gather else "load_scatter")
 
 

@@ -45,6 +45,8 @@ from .spec import DType, ParallelConfig, ParamSpec, RecordMeta
 
 OP_COPY, OP_MEAN, OP_NOISE, OP_ZERO, OP_CHECKZERO = 0, 1, 2, 3, 4
 RUN_VEC, RUN_ROWSPLIT = 1, 2
+CLASS_VEC_F32, CLASS_VEC_BF16, CLASS_VEC_F16, CLASS_GENERAL = 0, 1, 2, 3
+NCLASS = 4
 SEG = 512            # elements per warp segment (kSeg in the kernel)
 MAX_AUX = 256        # kMaxAux in the kernel
 MAX_SRC = 64         # sources per run before verify-only continuation runs
@@ -167,6 +169,26 @@ class RunTable:
         aux = np.asarray(self._aux if self._aux else [0], dtype=np.uint64)
         tiles = make_tiles(runs, tile_bytes)
         return runs, aux, tiles
+
+    def finish_classed(self, tile_bytes: int = 1 << 17):
+        """(runs, aux, tiles sorted by kernel class, per-class tile counts)."""
+        runs, aux, tiles = self.finish(tile_bytes)
+        cls = run_classes(runs)
+        tcls = cls[tiles["run"]] if len(tiles) else np.zeros(0, dtype=np.int64)
+        order = np.argsort(tcls, kind="stable")
+        counts = np.bincount(tcls, minlength=NCLASS).astype(np.int64) if len(tiles) else \
+            np.zeros(NCLASS, dtype=np.int64)
+        return runs, aux, tiles[order], counts
+
+
+def run_classes(runs: np.ndarray) -> np.ndarray:
+    """Kernel class of each run (UCP_CLASS_* in include/ucp_b200.h): the
+    vector kernels take COPY runs with a shared 16-B phase; everything else
+    goes to the general kernel."""
+    vec = ((runs["flags"] & RUN_VEC) != 0) & (runs["op"] == OP_COPY) & (runs["n_src"] >= 1)
+    by_dt = np.select([runs["dtype"] == DType.F32.value, runs["dtype"] == DType.BF16.value],
+                      [CLASS_VEC_F32, CLASS_VEC_BF16], CLASS_VEC_F16)
+    return np.where(vec, by_dt, CLASS_GENERAL).astype(np.int64)
 
 
 def make_tiles(runs: np.ndarray, tile_bytes: int) -> np.ndarray:

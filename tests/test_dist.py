@@ -1,0 +1,102 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): LPT ownership and the
+rank-homed all-to-all-v exchange plan."""
+
+import os
+import socket
+from itertools import product
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2406_18820_b200 as U
+from paper_2406_18820_b200.dist import alltoallv, exchange_plan, owned_params, plan_work
+from paper_2406_18820_b200.spec import ModelSpec, ParamKind, ParamSpec
+
+
+def _spec(costs):
+    return ModelSpec("synthetic", 0, (), tuple(
+        ParamSpec(f"p{i:02d}", (c,), 0, ParamKind.LAYERNORM_WEIGHT) for i, c in enumerate(costs)))
+
+
+def test_plan_work_textbook():
+    # pkg/tests/test_convert.py:211-217
+    plan = plan_work(_spec([100, 60, 40, 30, 20, 10]), 2)
+    assert sorted(plan.loads) == [130, 130]
+    assert {frozenset(g) for g in plan.groups} == {frozenset({"p00", "p03"}),
+                                                   frozenset({"p01", "p02", "p04", "p05"})}
+
+
+def test_plan_work_ties_deterministic():
+    plan = plan_work(_spec([8, 8, 8, 8]), 2)
+    assert plan.groups == (("p00", "p02"), ("p01", "p03"))
+
+
+@pytest.mark.parametrize("costs,k", [([5, 7, 3, 9, 2, 2, 6], 2), ([1, 60, 33, 17, 17], 3),
+                                     ([12, 11, 10, 9, 8, 7, 6], 3)])
+def test_plan_work_lpt_bound(costs, k):
+    plan = plan_work(_spec(costs), k)
+    best = min(max(sum(c for c, w in zip(costs, a) if w == i) for i in range(k))
+               for a in product(range(k), repeat=len(costs)))
+    assert max(plan.loads) * 3 <= 4 * best + 2
+
+
+def test_owned_params_partition_llama():
+    spec = U.llama_spec("7b")
+    for world in (1, 2, 4, 8):
+        parts = [owned_params(spec, r, world) for r in range(world)]
+        flat = [n for p in parts for n in p]
+        assert sorted(flat) == sorted(p.name for p in spec.params)
+        loads = [sum(spec.param(n).numel for n in p) for p in parts]
+        assert max(loads) / (sum(loads) / world) < 1.05  # good balance at 7B
+
+
+def test_exchange_plan_counts():
+    send = exchange_plan([0, 0, 1, 1, 1], [0, 1, 0, 1, 0], [10, 20, 30, 40, 50], 2)
+    assert send == [[0, 20], [80, 0]]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = U.llama_spec("7b", n_layers=2)
+        mine = owned_params(spec, rank, world)
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+        # rank r sends (r*10 + d) repeated (d+1) times to rank d
+        send_counts = [d + 1 for d in range(world)]
+        send = torch.cat([torch.full((d + 1,), rank * 10 + d, dtype=torch.uint8)
+                          for d in range(world)])
+        recv_counts = [rank + 1] * world
+        recv = alltoallv(send, send_counts, recv_counts)
+        q.put((rank, got, recv.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_ownership_and_alltoallv():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spec = U.llama_spec("7b", n_layers=2)
+    for rank, parts, recv in res:
+        assert sorted(n for p in parts for n in p) == sorted(p.name for p in spec.params)
+        want = []
+        for s in range(world):
+            want += [s * 10 + rank] * (rank + 1)
+        assert recv == want

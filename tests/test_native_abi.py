@@ -38,13 +38,20 @@ def test_abi_constants_match_header():
     assert int(consts["UCP_OP_MEAN"]) == plan.OP_MEAN
     assert int(consts["UCP_OP_NOISE"]) == plan.OP_NOISE
     assert int(consts["UCP_OP_CHECKZERO"]) == plan.OP_CHECKZERO
+    assert int(consts["UCP_NCLASS"]) == plan.NCLASS
+    assert int(consts["UCP_CLASS_GENERAL"]) == plan.CLASS_GENERAL
+    assert int(consts["UCP_CLASS_VEC_BF16"]) == plan.CLASS_VEC_BF16
     assert RUN_DTYPE.itemsize == 64 and TILE_DTYPE.itemsize == 16
 
 
 def test_argument_errors_without_device():
     lib = _native.load_library()
     # invalid arguments are rejected before any CUDA call
-    assert lib.ucp_convert_gather(None, 0, None, None, -1, None, None, None, None) == -10
-    assert lib.ucp_load_scatter(None, 0, None, None, 0, None, None, None, None) == 0
+    import numpy as np
+    bad = np.array([0, -1, 0, 0], dtype=np.int64)
+    zero = np.zeros(4, dtype=np.int64)
+    assert lib.ucp_convert_gather(None, 0, None, None, bad.ctypes.data, None, None, None, None) == -10
+    assert lib.ucp_convert_gather(None, 0, None, None, None, None, None, None, None) == -10
+    assert lib.ucp_load_scatter(None, 0, None, None, zero.ctypes.data, None, None, None, None) == 0
     assert lib.ucp_gen_state(0, 0, 0, 0, None, None) == 0
     assert lib.ucp_status_reset(None, None) == -10

@@ -239,3 +239,17 @@ def test_tiles_cover_every_element_once():
                     assert t["col0"] == 0
                     cover[t["row0"]:t["row0"] + t["count"], :] += 1
             assert (cover == 1).all(), (tb, i)
+
+
+def test_finish_classed_partitions_tiles():
+    from paper_2406_18820_b200.plan import CLASS_GENERAL, NCLASS, run_classes
+
+    spec = U.make_model("DenseGPT", {"n_layers": 2, "hidden": 32})
+    cfg = ParallelConfig(dp=3, tp=2, zero_stage=ZeroStage.Z1)
+    atomic = O.init_state(spec, 7)
+    _, tab = _arena_extract(spec, cfg, atomic, DType.BF16)
+    runs, aux, tiles, counts = tab.finish_classed(4096)
+    assert counts.sum() == len(tiles) and len(counts) == NCLASS
+    cls = run_classes(runs)[tiles["run"]]
+    assert (np.diff(cls) >= 0).all()
+    assert counts[CLASS_GENERAL] > 0  # noise + misaligned dp=3 pieces
