@@ -162,7 +162,9 @@ class ReshardPlan:
 
     @property
     def n_launches(self) -> int:
-        return sum((W.conv.n_tiles > 0) + (W.load.n_tiles > 0) for W in self.windows)
+        """Kernel launches of one step (one per non-empty tile class)."""
+        return sum(int((W.conv.class_counts > 0).sum() + (W.load.class_counts > 0).sum())
+                   for W in self.windows)
 
     # ------------------------------------------------------------------ buffers
 
