@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--unfused", action="store_true",
+                    help="separate convert and load launches (atomic re-read from HBM)")
     ap.add_argument("--cpu-threads", type=int, default=os.cpu_count())
     return ap.parse_args()
 
@@ -237,7 +239,8 @@ def run_ours(args):
     spec, src, tgt, desc = bench_config(args.config, args.layers)
     mine = owned_params(spec, rank, world) if world > 1 else None
     plan = ReshardPlan(spec, src, tgt, params=mine, device=dev,
-                       window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024)
+                       window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024,
+                       fused=not args.unfused)
     S_local = plan.state_bytes
     plan.synthesize(7)
     torch.cuda.synchronize()
@@ -259,7 +262,7 @@ def run_ours(args):
     plan.check()
 
     nW = len(plan.windows)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nW)]
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nW)]
            for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
@@ -276,9 +279,11 @@ def run_ours(args):
     clk = clocks.stop()
     plan.check()
     ms_local = t0.elapsed_time(t1) / args.steps
-    conv_ms = sum(e[0].elapsed_time(e[1]) for st in evs for e in st) / args.steps
-    load_ms = sum(e[1].elapsed_time(e[2]) for st in evs for e in st) / args.steps
+    fused_ms = sum(e[0].elapsed_time(e[1]) for st in evs for e in st) / args.steps
+    conv_ms = sum(e[1].elapsed_time(e[2]) for st in evs for e in st) / args.steps
+    load_ms = sum(e[2].elapsed_time(e[3]) for st in evs for e in st) / args.steps
 
+    fused_bytes = sum(plan.fused_bytes.values())
     conv_bytes = plan.bytes["R_c"] + plan.bytes["W_c"]
     load_bytes = plan.bytes["R_l"] + plan.bytes["W_l"]
     if world > 1:
@@ -292,9 +297,12 @@ def run_ours(args):
     value = S / (ms / 1e3) / GB
 
     peak, peak_src = measured_peak()
-    dom = "convert_gather" if conv_ms >= load_ms else "load_scatter"
-    dom_bytes, dom_ms = (conv_bytes, conv_ms) if dom == "convert_gather" else (load_bytes, load_ms)
-    launches = sum(1 for W in plan.windows if (W.conv if dom == "convert_gather" else W.load).n_tiles)
+    stages = {"reshard_fused": (fused_bytes, fused_ms, "fused"),
+              "convert_gather": (conv_bytes, conv_ms, "conv"),
+              "load_scatter": (load_bytes, load_ms, "load")}
+    dom = max(stages, key=lambda k: stages[k][1])
+    dom_bytes, dom_ms, attr = stages[dom]
+    launches = sum(1 for W in plan.windows if getattr(W, attr).n_tiles)
     achieved = (dom_bytes / launches) / (dom_ms / launches / 1e3) / GB
     ratio = ncu_traffic_ratio(args.config)
     traffic = None
@@ -304,12 +312,16 @@ def run_ours(args):
                 "frac": achieved / peak, "traffic": traffic, "kernel": dom,
                 "bytes_per_launch": dom_bytes / launches, "ms_per_launch": dom_ms / launches,
                 "launches_per_step": launches, "peak_source": peak_src,
-                "per_stage": {"convert_gather": {"ms": conv_ms, "hbm_bytes": conv_bytes,
-                                                 "GBps": conv_bytes / (conv_ms / 1e3) / GB,
-                                                 "frac": conv_bytes / (conv_ms / 1e3) / GB / peak},
+                "per_stage": {"reshard_fused": {"ms": fused_ms, "hbm_bytes": fused_bytes,
+                                                "GBps": fused_bytes / (fused_ms / 1e3) / GB if fused_ms else 0,
+                                                "frac": fused_bytes / (fused_ms / 1e3) / GB / peak if fused_ms else 0,
+                                                "units_fused": plan.n_fused_units, "units": plan.n_units},
+                              "convert_gather": {"ms": conv_ms, "hbm_bytes": conv_bytes,
+                                                 "GBps": conv_bytes / (conv_ms / 1e3) / GB if conv_bytes else 0,
+                                                 "frac": conv_bytes / (conv_ms / 1e3) / GB / peak if conv_bytes else 0},
                               "load_scatter": {"ms": load_ms, "hbm_bytes": load_bytes,
-                                               "GBps": load_bytes / (load_ms / 1e3) / GB,
-                                               "frac": load_bytes / (load_ms / 1e3) / GB / peak},
+                                               "GBps": load_bytes / (load_ms / 1e3) / GB if load_bytes else 0,
+                                               "frac": load_bytes / (load_ms / 1e3) / GB / peak if load_bytes else 0},
                               "step_hbm_frac": plan.hbm_bytes / (ms_local / 1e3) / GB / peak}}
     gpu_launches = args.steps * plan.n_launches
 
@@ -399,7 +411,13 @@ def run_ours(args):
           "config": {"workload": desc, "config": args.config, "src": format_config_string(src),
                      "tgt": format_config_string(tgt), "state_bytes": int(S),
                      "hbm_bytes_per_step_rank0": int(plan.hbm_bytes),
-                     "bytes": {k: int(v) for k, v in plan.bytes.items()}, "windows": nW,
+                     "bytes": {k: int(v) for k, v in plan.bytes.items()},
+                     "fused_bytes": {k: int(v) for k, v in plan.fused_bytes.items()},
+                     "mode": "unfused" if args.unfused else "fused convert+load (atomic written once, never re-read)",
+                     "unfused_algorithmic_bytes": "R_c + W_c + R_l + W_l = %d" % int(
+                         plan.bytes["R_c"] + plan.bytes["W_c"] + plan.fused_bytes["R"] + 2 * plan.fused_bytes["W_atom"]
+                         + plan.bytes["R_l"] + plan.bytes["W_l"] + plan.fused_bytes["W_tgt"]),
+                     "windows": nW,
                      "parallelism": f"param-sharded x{world}", "l2": "inputs larger than L2 "
                      f"({plan.src_total / GB:.1f} GB source arena per rank)",
                      "strict_replicate": True},

@@ -91,6 +91,32 @@ typedef struct ucp_run {
   uint32_t pad_;
 } ucp_run;             /* 64 bytes */
 
+/*
+ * Fused reshard run (convert + load in one pass): rows x cols
+ * f32 elements read from n_src bit-identical replicas (strict check), written
+ * once to the atomic tensor (f32, atom_pitch; skipped when atom == UINT64_MAX)
+ * and fanned out to n_dst target fragments (dtype, dst_pitch). The atomic
+ * bytes are never read back: the load half consumes them from registers.
+ */
+typedef struct ucp_xrun {
+  uint64_t src;        /* byte offset from src_base of replica 0's (0,0) */
+  uint64_t atom;       /* byte offset from atom_base, or UINT64_MAX */
+  uint64_t dst;        /* byte offset from dst_base of target 0's (0,0) */
+  uint32_t src_pitch;  /* elements */
+  uint32_t atom_pitch;
+  uint32_t dst_pitch;
+  uint32_t rows;
+  uint32_t cols;
+  uint32_t aux;        /* sources 1..n_src-1, then targets 1..n_dst-1 */
+  uint16_t n_src;
+  uint16_t n_dst;
+  uint8_t dtype;       /* UCP_DT_* of the targets */
+  uint8_t pad0_;
+  uint16_t pad1_;
+  uint32_t tag;
+  uint32_t flags;      /* UCP_RUN_VEC is required; UCP_RUN_ROWSPLIT as for ucp_run */
+} ucp_xrun;            /* 64 bytes */
+
 typedef struct ucp_tile {
   uint32_t run;
   uint32_t row0;
@@ -135,6 +161,15 @@ int ucp_load_scatter(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
  */
 int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, float* out,
                   void* stream);
+
+/*
+ * Fused convert + load (the in-memory resume() path, ucp/load.py:276-281):
+ * class_counts has UCP_NCLASS entries; only the three VEC classes (target
+ * dtype f32 / bf16 / f16) are valid, tiles sorted by class.
+ */
+int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
+                      const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
+                      void* atom_base, void* dst_base, ucp_status* status, void* stream);
 
 /* Byte-compare two device buffers; *mismatch (device) receives the first
  * differing byte index or ~0. Used by the checker paths of the bench. */

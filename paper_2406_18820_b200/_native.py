@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 # exported symbols declared in include/ucp_b200.h
 EXPORTS = ("ucp_version", "ucp_status_reset", "ucp_convert_gather", "ucp_load_scatter",
-           "ucp_gen_state", "ucp_compare", "ucp_peek")
+           "ucp_reshard_fused", "ucp_gen_state", "ucp_compare", "ucp_peek")
 ABI_VERSION = 1
 
 _lib = None
@@ -30,6 +30,7 @@ _SIGS = {
     "ucp_status_reset": (_c.c_int, [_P, _P]),
     "ucp_convert_gather": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "ucp_load_scatter": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
+    "ucp_reshard_fused": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ucp_gen_state": (_c.c_int, [_c.c_uint64, _c.c_uint64, _c.c_uint64, _c.c_int, _P, _P]),
     "ucp_compare": (_c.c_int, [_P, _P, _c.c_uint64, _P, _P]),
     "ucp_peek": (_c.c_int, [_P, _P, _c.c_uint64]),

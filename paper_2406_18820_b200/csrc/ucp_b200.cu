@@ -20,6 +20,7 @@
 
 static_assert(sizeof(ucp_run) == 64, "ucp_run must be 64 bytes");
 static_assert(sizeof(ucp_tile) == 16, "ucp_tile must be 16 bytes");
+static_assert(sizeof(ucp_xrun) == 64, "ucp_xrun must be 64 bytes");
 
 namespace {
 
@@ -522,6 +523,125 @@ __device__ __forceinline__ void general_body(const ucp_run* __restrict__ runs,
   }
 }
 
+// ---------------------------------------------------------------- fused kernel
+//
+// convert + load in one pass: each element is read once per source replica,
+// verified, written once to the atomic tensor and once per target replica.
+// HBM traffic R_c + W_c + W_l instead of R_c + 2 S + W_l.
+
+template <int DT>
+__device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
+                                           const uint64_t* __restrict__ aux,
+                                           const ucp_tile* __restrict__ tiles,
+                                           const char* __restrict__ sb, char* __restrict__ ab,
+                                           char* __restrict__ db, ucp_status* st) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  __shared__ ucp_xrun s_run;
+  __shared__ uint64_t s_aux[kMaxAux];
+  const ucp_tile tile = tiles[blockIdx.x];
+  if (threadIdx.x < 4) {
+    reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
+        reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
+  }
+  __syncthreads();
+  const int ns = s_run.n_src, nd = s_run.n_dst;
+  const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
+  if (n_aux > 0) {
+    for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
+    __syncthreads();
+  }
+  uint32_t nr, nc;
+  if (s_run.flags & UCP_RUN_ROWSPLIT) { nr = 1; nc = tile.count; }
+  else { nr = tile.count; nc = s_run.cols; }
+  const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nr * spr;
+  const uint64_t s0 = s_run.src, a0 = s_run.atom, d0 = s_run.dst;
+  const bool atom_on = a0 != ~0ull;
+  const uint32_t sp = s_run.src_pitch, ap = s_run.atom_pitch, dpch = s_run.dst_pitch;
+  const uint32_t cols = s_run.cols;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (uint32_t it = warp; it < n_items; it += kWarps) {
+    const uint32_t rr = spr == 1 ? it : it / spr;
+    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
+    const uint32_t row = tile.row0 + rr;
+    const uint64_t srow = (uint64_t)row * sp + cs;
+    const uint64_t arow = (uint64_t)row * ap + cs;
+    const uint64_t drow = (uint64_t)row * dpch + cs;
+    const uint32_t phase = (uint32_t)(((s0 >> 2) + srow) & 3);
+    uint32_t head = (4u - phase) & 3u;
+    if (head > len) head = len;
+    const uint32_t nvec = (len - head) >> 2;
+    const uint32_t tail = len - head - 4 * nvec;
+    bool bad = false;
+    uint32_t bad_e = 0xffffffffu;
+
+    const uint64_t so = 4 * (srow + head);
+    float4 v[kVec];
+#pragma unroll
+    for (int u = 0; u < kVec; ++u)
+      if (lane + 32u * u < nvec) v[u] = ld_stream4(sb + s0 + so + 16ull * (lane + 32u * u));
+    for (int k = 1; k < ns; ++k) {
+      const char* pk = sb + s_aux[k - 1] + so;
+      float4 w[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (lane + 32u * u < nvec) w[u] = ld_stream4(pk + 16ull * (lane + 32u * u));
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        if (lane + 32u * u < nvec) {
+          const int d = diff4(v[u], w[u]);
+          if (d < 4) { bad = true; bad_e = min(bad_e, head + 4 * (lane + 32u * u) + d); }
+        }
+      }
+    }
+    if (atom_on) {
+      char* pa = ab + a0 + 4 * (arow + head);
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (lane + 32u * u < nvec) st4(pa + 16ull * (lane + 32u * u), v[u]);
+    }
+    const uint64_t dofs = (uint64_t)ESZ * (drow + head);
+    for (int d = 0; d < nd; ++d) {
+      char* pd = db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + dofs;
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (lane + 32u * u < nvec) store4<DT>(pd + (uint64_t)ESZ * 4 * (lane + 32u * u), v[u]);
+    }
+    if (head + tail) {
+      const bool ok = lane < head + tail;
+      const uint32_t e = lane < head ? lane : head + 4 * nvec + (lane - head);
+      float x = 0.0f;
+      if (ok) x = ld_stream1(sb + s0 + 4 * (srow + e));
+      for (int k = 1; k < ns; ++k) {
+        if (ok) {
+          const float y = ld_stream1(sb + s_aux[k - 1] + 4 * (srow + e));
+          if (bits_of(x) != bits_of(y)) { bad = true; bad_e = min(bad_e, e); }
+        }
+      }
+      if (ok && atom_on) *reinterpret_cast<float*>(ab + a0 + 4 * (arow + e)) = x;
+      for (int d = 0; d < nd; ++d)
+        if (ok) store1<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + (uint64_t)ESZ * (drow + e), x);
+    }
+    report(bad, row * cols + cs + bad_e, tile.run, st);
+  }
+}
+
+#define UCP_FUSED_ARGS                                                                     \
+  const ucp_xrun *__restrict__ runs, const uint64_t *__restrict__ aux,                      \
+      const ucp_tile *__restrict__ tiles, const char *__restrict__ sb, char *__restrict__ ab, \
+      char *__restrict__ db, ucp_status *st
+
+__global__ void __launch_bounds__(kThreads, 4) reshard_fused_f32(UCP_FUSED_ARGS) {
+  fused_body<UCP_DT_F32>(runs, aux, tiles, sb, ab, db, st);
+}
+__global__ void __launch_bounds__(kThreads, 4) reshard_fused_bf16(UCP_FUSED_ARGS) {
+  fused_body<UCP_DT_BF16>(runs, aux, tiles, sb, ab, db, st);
+}
+__global__ void __launch_bounds__(kThreads, 4) reshard_fused_f16(UCP_FUSED_ARGS) {
+  fused_body<UCP_DT_F16>(runs, aux, tiles, sb, ab, db, st);
+}
+
 // ---------------------------------------------------------------- entry kernels
 // Distinct names per stage and destination dtype so launch lists and ncu
 // filters read like the pipeline: convert_gather_* (union) and
@@ -675,6 +795,36 @@ int ucp_load_scatter(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
                      const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
                      void* dst_base, ucp_status* status, void* stream) {
   return launch_move(false, runs, n_runs, aux, tiles, class_counts, src_base, dst_base, status, stream);
+}
+
+int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
+                      const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
+                      void* atom_base, void* dst_base, ucp_status* status, void* stream) {
+  if (n_runs < 0 || !class_counts) return UCP_EINVAL;
+  int64_t total = 0;
+  for (int c = 0; c < UCP_NCLASS; ++c) {
+    if (class_counts[c] < 0 || class_counts[c] > 0x7fffffffLL) return UCP_EINVAL;
+    total += class_counts[c];
+  }
+  if (class_counts[UCP_CLASS_GENERAL] != 0) return UCP_EINVAL;
+  if (total == 0) return UCP_OK;
+  if (!runs || !tiles || !status) return UCP_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const char* sb = static_cast<const char*>(src_base);
+  char* ab = static_cast<char*>(atom_base);
+  char* db = static_cast<char*>(dst_base);
+  int64_t at = 0;
+  for (int c = 0; c < UCP_CLASS_GENERAL; ++c) {
+    const int64_t n = class_counts[c];
+    if (n == 0) continue;
+    const dim3 grid((unsigned)n), block(kThreads);
+    const ucp_tile* t = tiles + at;
+    if (c == UCP_CLASS_VEC_F32) reshard_fused_f32<<<grid, block, 0, s>>>(runs, aux, t, sb, ab, db, status);
+    else if (c == UCP_CLASS_VEC_BF16) reshard_fused_bf16<<<grid, block, 0, s>>>(runs, aux, t, sb, ab, db, status);
+    else reshard_fused_f16<<<grid, block, 0, s>>>(runs, aux, t, sb, ab, db, status);
+    at += n;
+  }
+  return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
 }
 
 int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, float* out,

@@ -62,6 +62,10 @@ class Program:
     def bytes_moved(self) -> int:
         return self.src_bytes + self.dst_bytes
 
+    @property
+    def n_launches(self) -> int:
+        return int((self.class_counts > 0).sum())
+
     def launch(self, gather: bool, src_base: int, dst_base: int, status: "Status",
                stream: torch.cuda.Stream | None = None) -> None:
         if self.n_tiles == 0:
@@ -72,6 +76,42 @@ class Program:
                 self.class_counts.ctypes.data, ctypes.c_void_p(src_base),
                 ctypes.c_void_p(dst_base), status.ptr, stream_ptr(stream))
         _check(rc, "convert_gather" if gather else "load_scatter")
+
+
+class XProgram:
+    """One ucp_reshard_fused launch: fused convert+load runs on a device."""
+
+    def __init__(self, table, device: torch.device, tile_bytes: int = 1 << 17):
+        runs, aux, tiles, counts = table.finish_classed(tile_bytes)
+        self.runs_host, self.aux_host, self.tiles_host = runs, aux, tiles
+        self.class_counts = np.ascontiguousarray(counts, dtype=np.int64)
+        self.units = table.units
+        self.src_bytes, self.atom_bytes, self.dst_bytes = (table.src_bytes, table.atom_bytes,
+                                                           table.dst_bytes)
+        self.n_runs, self.n_tiles = len(runs), len(tiles)
+        self.device = device
+        blob = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).to(device)
+        self._runs = blob(runs) if len(runs) else torch.zeros(64, dtype=torch.uint8, device=device)
+        self._aux = blob(aux)
+        self._tiles = blob(tiles) if len(tiles) else torch.zeros(16, dtype=torch.uint8, device=device)
+
+    @property
+    def bytes_moved(self) -> int:
+        return self.src_bytes + self.atom_bytes + self.dst_bytes
+
+    @property
+    def n_launches(self) -> int:
+        return int((self.class_counts > 0).sum())
+
+    def launch(self, src_base: int, atom_base: int, dst_base: int, status: "Status",
+               stream: torch.cuda.Stream | None = None) -> None:
+        if self.n_tiles == 0:
+            return
+        rc = _native.lib().ucp_reshard_fused(
+            self._runs.data_ptr(), self.n_runs, self._aux.data_ptr(), self._tiles.data_ptr(),
+            self.class_counts.ctypes.data, ctypes.c_void_p(src_base), ctypes.c_void_p(atom_base),
+            ctypes.c_void_p(dst_base), status.ptr, stream_ptr(stream))
+        _check(rc, "reshard_fused")
 
 
 class Status:
@@ -108,11 +148,12 @@ def describe_failure(prog: Program, run_idx: int, elem: int, src_base: int) -> E
     r = prog.runs_host[run_idx]
     unit = prog.units[int(r["tag"])]
     where = f"{unit.param}.{unit.kind}"
-    if int(r["op"]) == OP_CHECKZERO:
+    fused = "atom" in r.dtype.names
+    if not fused and int(r["op"]) == OP_CHECKZERO:
         return PaddingError(f"{where}: nonzero pad tail (first bad element {elem})")
     labels = unit.labels.get(run_idx)
     row, col = divmod(elem, int(r["cols"]))
-    n_src, groups = int(r["n_src"]), max(int(r["groups"]), 1)
+    n_src, groups = int(r["n_src"]), 1 if fused else max(int(r["groups"]), 1)
     K = n_src // groups
     offs = [int(r["src"])] + [int(x) for x in prog.aux_host[int(r["aux"]):int(r["aux"]) + n_src - 1]]
     pos = 4 * (row * int(r["src_pitch"]) + col)

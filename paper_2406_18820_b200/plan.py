@@ -61,6 +61,15 @@ RUN_DTYPE = np.dtype({
     "itemsize": 64,
 })
 TILE_DTYPE = np.dtype([("run", "<u4"), ("row0", "<u4"), ("col0", "<u4"), ("count", "<u4")])
+XRUN_DTYPE = np.dtype({
+    "names": ["src", "atom", "dst", "src_pitch", "atom_pitch", "dst_pitch", "rows", "cols", "aux",
+              "n_src", "n_dst", "dtype", "tag", "flags"],
+    "formats": ["<u8", "<u8", "<u8", "<u4", "<u4", "<u4", "<u4", "<u4", "<u4", "<u2", "<u2", "u1",
+                "<u4", "<u4"],
+    "offsets": [0, 8, 16, 24, 28, 32, 36, 40, 44, 48, 50, 52, 56, 60],
+    "itemsize": 64,
+})
+NO_ATOM = (1 << 64) - 1
 
 _ESZ = {DType.F32: 4, DType.F16: 2, DType.BF16: 2}
 
@@ -191,13 +200,15 @@ def run_classes(runs: np.ndarray) -> np.ndarray:
     return np.where(vec, by_dt, CLASS_GENERAL).astype(np.int64)
 
 
-def make_tiles(runs: np.ndarray, tile_bytes: int) -> np.ndarray:
+def make_tiles(runs: np.ndarray, tile_bytes: int, extra_bpe=None) -> np.ndarray:
     """One CTA per tile; a tile never straddles runs. Tile size is
     normalised by bytes moved per element so tiles cost about the same."""
     if len(runs) == 0:
         return np.zeros(0, dtype=TILE_DTYPE)
     esz = np.where(runs["dtype"] == 0, 4, 2).astype(np.int64)
     bpe = 4 * runs["n_src"].astype(np.int64) + esz * runs["n_dst"].astype(np.int64)
+    if extra_bpe is not None:
+        bpe = bpe + extra_bpe
     bpe = np.maximum(bpe, 4)
     telems = np.maximum(SEG, (tile_bytes // bpe) // SEG * SEG)
     rows = runs["rows"].astype(np.int64)
@@ -593,3 +604,182 @@ def fragment_shape(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta) -> tuple
     if meta.flat_range is None:
         return tuple(tp_fragment_shape(p, tp_mode(p, cfg.tp), cfg.tp))
     return (fragment_elems(p, cfg, meta),)
+
+
+# --------------------------------------------------------------------------- fused
+
+
+class XRunTable:
+    """Fused convert+load runs (ucp_xrun) for one ucp_reshard_fused launch."""
+
+    def __init__(self):
+        self._rows: list = []
+        self._aux: list = []
+        self.units: list = []
+        self.src_bytes = 0
+        self.atom_bytes = 0
+        self.dst_bytes = 0
+
+    def unit(self, param: str, kind: str) -> int:
+        self.units.append(Unit(param, kind))
+        return len(self.units) - 1
+
+    def add(self, *, srcs, atom, dsts, src_pitch, atom_pitch, dst_pitch, rows, cols, dtype, tag,
+            labels=None) -> None:
+        if rows == 0 or cols == 0:
+            return
+        if labels is not None:
+            self.units[tag].labels[len(self._rows)] = labels
+        aux_at = len(self._aux)
+        self._aux.extend(srcs[1:])
+        self._aux.extend(dsts[1:])
+        self._rows.append((srcs[0], atom, dsts[0] if dsts else 0, src_pitch, atom_pitch, dst_pitch,
+                           rows, cols, aux_at, len(srcs), len(dsts), dtype.value, tag, RUN_VEC))
+        n = rows * cols
+        self.src_bytes += 4 * n * len(srcs)
+        self.atom_bytes += 0 if atom == NO_ATOM else 4 * n
+        self.dst_bytes += _ESZ[dtype] * n * len(dsts)
+
+    def __len__(self):
+        return len(self._rows)
+
+    def finish_classed(self, tile_bytes: int = 1 << 17):
+        runs = np.zeros(len(self._rows), dtype=XRUN_DTYPE)
+        if self._rows:
+            for name, vals in zip(XRUN_DTYPE.names, zip(*self._rows)):
+                runs[name] = vals
+        aux = np.asarray(self._aux if self._aux else [0], dtype=np.uint64)
+        extra = np.where(runs["atom"] == np.uint64(NO_ATOM), 0, 4).astype(np.int64)
+        tiles = make_tiles(runs, tile_bytes, extra)
+        cls = np.select([runs["dtype"] == DType.F32.value, runs["dtype"] == DType.BF16.value],
+                        [CLASS_VEC_F32, CLASS_VEC_BF16], CLASS_VEC_F16).astype(np.int64)
+        tcls = cls[tiles["run"]] if len(tiles) else np.zeros(0, dtype=np.int64)
+        order = np.argsort(tcls, kind="stable")
+        counts = np.bincount(tcls, minlength=NCLASS).astype(np.int64) if len(tiles) else \
+            np.zeros(NCLASS, dtype=np.int64)
+        return runs, aux, tiles[order], counts
+
+
+def _rects(x0, xp, rows, cols, exts, ep, esz, R, W):
+    """Pieces of one run's atomic-side region as rectangles of the [R, W] grid:
+    (r0, c0, rows, cols, ext offsets at (r0, c0), ext pitch)."""
+    if rows == 1:
+        out = []
+        for fs, xs, _, r, c in split_rows((0, 0, W, R, W), x0, x0 + cols):
+            sh = esz * (fs - x0)
+            out.append((xs // W, xs % W, r, c, [e + sh for e in exts], W if r > 1 else c))
+        return out
+    if xp != W:
+        return None
+    return [(x0 // W, x0 % W, rows, cols, list(exts), ep)]
+
+
+def compile_fused(fx: XRunTable, rest_conv: RunTable, rest_load: RunTable, p: ParamSpec,
+                  src: ParallelConfig, frags: list, atom_off: int, tgt: ParallelConfig,
+                  targets: list, dtype: DType = DType.F32, strict: bool = True,
+                  materialize: bool = True) -> bool:
+    """Fused convert+load of one (param, kind): every atomic element is
+    gathered (with replica checks), written to the atomic tensor at atom_off
+    (unless materialize=False) and scattered to its target fragments in the
+    same pass. Validation and error behaviour are compile_union's and
+    compile_extract's (they run first). Units that cannot fuse (Partial
+    mean/noise, phase-mismatched pieces, very wide fan-in/out) are emitted
+    unfused into rest_conv / rest_load instead. Returns True when fused."""
+    conv, load = RunTable(), RunTable()
+    compile_union(conv, p, src, frags, atom_off, strict)
+    compile_extract(load, p, tgt, targets, atom_off, dtype)
+    n = _numel(p.shape)
+    W = _numel(p.shape[1:]) if len(p.shape) > 1 else max(n, 1)
+    R = n // W if W else 0
+    esz = _ESZ[dtype]
+    crects, lrects, extra_conv, extra_load = [], [], [], []
+    ok = n > 0
+    for i, r in enumerate(conv._rows):
+        (s0, d0, sp, dp, rows, cols, aux, ns, nd, groups, op, dt, tpr, tp, tag, flags) = r
+        if op == OP_CHECKZERO:
+            extra_conv.append(i)
+            continue
+        if op != OP_COPY or not (flags & RUN_VEC) or ns > MAX_SRC:
+            ok = False
+            break
+        srcs = [s0] + conv._aux[aux:aux + ns - 1]
+        got = _rects((d0 - atom_off) // 4, dp, rows, cols, srcs, sp, 4, R, W)
+        if got is None:
+            ok = False
+            break
+        crects += [(g, i) for g in got]
+    if ok:
+        for i, r in enumerate(load._rows):
+            (s0, d0, sp, dp, rows, cols, aux, ns, nd, groups, op, dt, tpr, tp, tag, flags) = r
+            if op == OP_ZERO:
+                extra_load.append(i)
+                continue
+            if op != OP_COPY or not (flags & RUN_VEC) or nd > MAX_DST:
+                ok = False
+                break
+            dsts = [d0] + load._aux[aux + ns - 1:aux + ns - 1 + nd - 1]
+            got = _rects((s0 - atom_off) // 4, sp, rows, cols, dsts, dp, esz, R, W)
+            if got is None:
+                ok = False
+                break
+            lrects += [(g, i) for g in got]
+    cells = []
+    if ok:
+        for (a, ai) in crects:
+            ar0, ac0, ar, ac, aext, aep = a
+            for (b, bi) in lrects:
+                br0, bc0, br, bc, bext, bep = b
+                r0, r1 = max(ar0, br0), min(ar0 + ar, br0 + br)
+                c0, c1 = max(ac0, bc0), min(ac0 + ac, bc0 + bc)
+                if r0 >= r1 or c0 >= c1:
+                    continue
+                srcs = [e + 4 * ((r0 - ar0) * aep + (c0 - ac0)) for e in aext]
+                dsts = [e + esz * ((r0 - br0) * bep + (c0 - bc0)) for e in bext]
+                atom = atom_off + 4 * (r0 * W + c0)
+                ph = {(x // 4) % 4 for x in srcs} | {(atom // 4) % 4} | {(x // esz) % 4 for x in dsts}
+                pit = r1 - r0 == 1 or (aep % 4 == 0 and bep % 4 == 0 and W % 4 == 0)
+                if len(ph) != 1 or not pit or any(x % 4 for x in srcs) or any(x % esz for x in dsts):
+                    ok = False
+                    break
+                cells.append((srcs, atom, dsts, aep, bep, r1 - r0, c1 - c0, ai))
+            if not ok:
+                break
+        if ok and sum(c[5] * c[6] for c in cells) != n:
+            ok = False
+    if not ok:
+        _absorb(rest_conv, conv)
+        _absorb(rest_load, load)
+        return False
+    tag = fx.unit(p.name, frags[0][0].kind)
+    for srcs, atom, dsts, sp, dp, rows, cols, ci in cells:
+        fx.add(srcs=srcs, atom=atom if materialize else NO_ATOM, dsts=dsts, src_pitch=sp,
+               atom_pitch=W, dst_pitch=dp, rows=rows, cols=cols, dtype=dtype, tag=tag,
+               labels=conv.units[0].labels.get(ci) if conv.units else None)
+    for i in extra_conv:
+        _absorb_row(rest_conv, conv, i)
+    for i in extra_load:
+        _absorb_row(rest_load, load, i)
+    return True
+
+
+def _absorb_row(dst: RunTable, src: RunTable, i: int) -> None:
+    (s0, d0, sp, dp, rows, cols, aux, ns, nd, groups, op, dt, tpr, tp, tag, flags) = src._rows[i]
+    unit = src.units[tag]
+    key = (id(src), tag)
+    new_tag = dst._adopted.get(key) if hasattr(dst, "_adopted") else None
+    if new_tag is None:
+        if not hasattr(dst, "_adopted"):
+            dst._adopted = {}
+        new_tag = dst.unit(unit.param, unit.kind)
+        dst._adopted[key] = new_tag
+    nsx = max(ns - 1, 0)
+    srcs = ([s0] + src._aux[aux:aux + nsx]) if ns else []
+    dsts = ([d0] + src._aux[aux + nsx:aux + nsx + nd - 1]) if nd else []
+    dst.add(srcs=srcs, dsts=dsts, src_pitch=sp, dst_pitch=dp, rows=rows, cols=cols, op=op,
+            groups=groups, dtype=DType(dt), tp_rank=tpr, tp=tp, tag=new_tag,
+            labels=unit.labels.get(i))
+
+
+def _absorb(dst: RunTable, src: RunTable) -> None:
+    for i in range(len(src._rows)):
+        _absorb_row(dst, src, i)

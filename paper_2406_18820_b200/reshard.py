@@ -28,9 +28,17 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .engine import Program, Status, align_up, gen_state, require_device, stream_ptr
+from .engine import Program, Status, XProgram, align_up, gen_state, require_device, stream_ptr
 from .layout import all_rank_records, validate_model_config
-from .plan import RunTable, compile_extract, compile_union, fragment_elems, fragment_shape
+from .plan import (
+    RunTable,
+    XRunTable,
+    compile_extract,
+    compile_fused,
+    compile_union,
+    fragment_elems,
+    fragment_shape,
+)
 from .spec import STATE_KINDS, DType, ModelSpec, ParallelConfig
 from .synth import stream_base
 
@@ -46,9 +54,10 @@ class Window:
     tgt_bytes: int = 0
     src_base: int = 0    # offset of this window in the global source arena
     tgt_base: int = 0    # offset of this window in the global target arena
-    conv: object = None  # RunTable / Program
+    conv: object = None  # Program (unfused mode: everything; fused mode: the rest)
     load: object = None
     synth: object = None
+    fused: object = None  # XProgram (fused mode)
 
 
 class ReshardPlan:
@@ -56,10 +65,12 @@ class ReshardPlan:
 
     def __init__(self, spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig,
                  dtype: DType = DType.F32, strict: bool = True, params=None, device=None,
-                 window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17):
+                 window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17, fused: bool = False,
+                 materialize_atomic: bool = True):
         validate_model_config(spec, src)
         validate_model_config(spec, tgt)
         self.spec, self.src, self.tgt, self.dtype, self.strict = spec, src, tgt, dtype, strict
+        self.fused_mode, self.materialize = fused, materialize_atomic
         self.device = require_device(device)
         self.tile_bytes = tile_bytes
         names = None if params is None else set(params)
@@ -124,8 +135,11 @@ class ReshardPlan:
 
     def _compile(self) -> None:
         self.bytes = {"R_c": 0, "W_c": 0, "R_l": 0, "W_l": 0}
+        self.fused_bytes = {"R": 0, "W_atom": 0, "W_tgt": 0}
+        self.n_fused_units = self.n_units = 0
         for W in self.windows:
             conv, load, synth = RunTable(), RunTable(), RunTable()
+            fx = XRunTable()
             src_by_unit, tgt_by_unit = {}, {}
             for g, i, m, off, n in W.src_frags:
                 src_by_unit.setdefault((m.param, m.kind), []).append((m, off, n))
@@ -135,14 +149,25 @@ class ReshardPlan:
                 for k in STATE_KINDS:
                     a = W.atom[(p.name, k)]
                     frags = src_by_unit.get((p.name, k), [])
-                    compile_union(conv, p, self.src, frags, a, self.strict)
                     dt = self.dtype if k == "weight" else DType.F32
-                    compile_extract(load, p, self.tgt, tgt_by_unit.get((p.name, k), []), a, dt)
+                    tg = tgt_by_unit.get((p.name, k), [])
+                    self.n_units += 1
+                    if self.fused_mode:
+                        self.n_fused_units += compile_fused(
+                            fx, conv, load, p, self.src, frags, a, self.tgt, tg, dt, self.strict,
+                            self.materialize)
+                    else:
+                        compile_union(conv, p, self.src, frags, a, self.strict)
+                        compile_extract(load, p, self.tgt, tg, a, dt)
                     compile_extract(synth, p, self.src, [(m, off) for m, off, _ in frags], a,
                                     DType.F32)
             W.conv = Program(conv, self.device, self.tile_bytes)
             W.load = Program(load, self.device, self.tile_bytes)
             W.synth = Program(synth, self.device, self.tile_bytes)
+            W.fused = XProgram(fx, self.device, self.tile_bytes)
+            self.fused_bytes["R"] += fx.src_bytes
+            self.fused_bytes["W_atom"] += fx.atom_bytes
+            self.fused_bytes["W_tgt"] += fx.dst_bytes
             self.bytes["R_c"] += conv.src_bytes
             self.bytes["W_c"] += conv.dst_bytes
             self.bytes["R_l"] += load.src_bytes
@@ -157,13 +182,14 @@ class ReshardPlan:
 
     @property
     def hbm_bytes(self) -> int:
-        """Algorithmic HBM traffic of one step: R_c + W_c + R_l + W_l."""
-        return sum(self.bytes.values())
+        """Algorithmic HBM traffic of one step: R_c + W_c + R_l + W_l of the
+        unfused runs plus R + W_atom + W_tgt of the fused ones."""
+        return sum(self.bytes.values()) + sum(self.fused_bytes.values())
 
     @property
     def n_launches(self) -> int:
         """Kernel launches of one step (one per non-empty tile class)."""
-        return sum(int((W.conv.class_counts > 0).sum() + (W.load.class_counts > 0).sum())
+        return sum(W.conv.n_launches + W.load.n_launches + W.fused.n_launches
                    for W in self.windows)
 
     # ------------------------------------------------------------------ buffers
@@ -201,19 +227,25 @@ class ReshardPlan:
 
     def step_device(self, stream=None, events=None) -> None:
         """One device-resident reshard of every window: inputs already in the
-        source arena, targets into a two-slot HBM ring."""
+        source arena, targets into a two-slot HBM ring. events[i] (optional)
+        gets 4 CUDA events around the fused / convert / load launches."""
         arena = self._bufs["src_arena"]
         atom = self.buf("atom", self.max_atom)
         ring = [self.buf("tgt0", self.max_tgt), self.buf("tgt1", self.max_tgt)]
         for i, W in enumerate(self.windows):
-            if events is not None:
-                events[i][0].record(stream)
-            W.conv.launch(True, arena.data_ptr() + W.src_base, atom.data_ptr(), self.status, stream)
-            if events is not None:
-                events[i][1].record(stream)
+            ev = events[i] if events is not None else None
+            src_ptr = arena.data_ptr() + W.src_base
+            if ev:
+                ev[0].record(stream)
+            W.fused.launch(src_ptr, atom.data_ptr(), ring[i % 2].data_ptr(), self.status, stream)
+            if ev:
+                ev[1].record(stream)
+            W.conv.launch(True, src_ptr, atom.data_ptr(), self.status, stream)
+            if ev:
+                ev[2].record(stream)
             W.load.launch(False, atom.data_ptr(), ring[i % 2].data_ptr(), self.status, stream)
-            if events is not None:
-                events[i][2].record(stream)
+            if ev:
+                ev[3].record(stream)
 
     def check(self) -> None:
         """Raise the reference exception for any data-dependent failure seen
@@ -223,19 +255,28 @@ class ReshardPlan:
         first, _ = self.status.read()
         if first == (1 << 64) - 1:
             return
+        arena = self._bufs["src_arena"]
+        for W in self.windows:
+            self._locate(W, arena.data_ptr() + W.src_base)
+        raise RuntimeError("reshard reported a failure that did not reproduce")
+
+    def _locate(self, W: Window, src_ptr: int) -> None:
+        """Re-run the source-reading launches of one window with a fresh
+        status word and raise the reference exception if one fails."""
         from .engine import describe_failure
 
-        arena = self._bufs["src_arena"]
         atom = self.buf("atom", self.max_atom)
-        for W in self.windows:
+        tgt = self.buf("tgt0", self.max_tgt)
+        for prog in (W.fused, W.conv):
             self.status.reset()
-            W.conv.launch(True, arena.data_ptr() + W.src_base, atom.data_ptr(), self.status)
+            if prog is W.fused:
+                prog.launch(src_ptr, atom.data_ptr(), tgt.data_ptr(), self.status)
+            else:
+                prog.launch(True, src_ptr, atom.data_ptr(), self.status)
             torch.cuda.synchronize(self.device)
             f, _ = self.status.read()
             if f != (1 << 64) - 1:
-                raise describe_failure(W.conv, f >> 32, f & 0xFFFFFFFF,
-                                       arena.data_ptr() + W.src_base)
-        raise RuntimeError("reshard reported a failure that did not reproduce")
+                raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, src_ptr)
 
     # ------------------------------------------------------------------ host-streamed
 
@@ -281,6 +322,8 @@ class ReshardPlan:
             s_cmp.wait_event(ev_in[i])
             if i >= 2:
                 s_cmp.wait_event(ev_out[i - 2])
+            W.fused.launch(dsrc[slot].data_ptr(), atom.data_ptr(), dtgt[slot].data_ptr(),
+                           self.status, s_cmp)
             W.conv.launch(True, dsrc[slot].data_ptr(), atom.data_ptr(), self.status, s_cmp)
             W.load.launch(False, atom.data_ptr(), dtgt[slot].data_ptr(), self.status, s_cmp)
             ev_cmp[i].record(s_cmp)
@@ -318,21 +361,12 @@ class ReshardPlan:
         first, _ = self.status.read()
         if first == (1 << 64) - 1:
             return
-        from .engine import describe_failure
-
-        # locate the failing convert program by re-running windows one by one
         dsrc = self.buf("chk_src", self.max_src)
-        atom = self.buf("atom", self.max_atom)
         for W in self.windows:
             if host_src is None:
                 break
             dsrc[:W.src_bytes].copy_(host_src[W.src_base:W.src_base + W.src_bytes])
-            self.status.reset()
-            W.conv.launch(True, dsrc.data_ptr(), atom.data_ptr(), self.status)
-            torch.cuda.synchronize(self.device)
-            f, _ = self.status.read()
-            if f != (1 << 64) - 1:
-                raise describe_failure(W.conv, f >> 32, f & 0xFFFFFFFF, dsrc.data_ptr())
+            self._locate(W, dsrc.data_ptr())
         raise RuntimeError("reshard reported a failure that did not reproduce")
 
     # ------------------------------------------------------------------ verification
@@ -343,39 +377,45 @@ class ReshardPlan:
 
         1. convert(partition_src(X)) == X bit for bit, where X is the
            generator state (the reference's own round-trip identity,
-           SPEC acceptance 1);
+           SPEC acceptance 1); skipped for fused units that do not
+           materialise the atomic tensor;
         2. convert_tgt(load(atomic)) == X: the materialised target fragments
            are a valid checkpoint of the same state under the target layout
            (needs f32 targets; bf16/f16 weights are lossy by design).
 
-        Returns {"windows": n, "atomic_ok": bool, "target_ok": bool|None}."""
+        Returns {"windows": n, "atomic_ok": bool|None, "target_ok": bool|None}."""
+        from .engine import compare
+
         arena = self._bufs["src_arena"]
         atom = self.buf("atom", self.max_atom)
         ref = self.buf("atom_ref", self.max_atom)
         back = self.buf("atom_back", self.max_atom)
         tgt = self.buf("tgt0", self.max_tgt)
         mism = torch.zeros(1, dtype=torch.int64, device=self.device)
-        from .engine import compare
-
-        atomic_ok, target_ok = True, (self.dtype is DType.F32) or None
+        atomic_ok = True if (self.materialize or not self.fused_mode) else None
+        target_ok = True if self.dtype is DType.F32 else None
         for W in self.windows:
             self.status.reset()
-            W.conv.launch(True, arena.data_ptr() + W.src_base, atom.data_ptr(), self.status)
+            src_ptr = arena.data_ptr() + W.src_base
+            W.fused.launch(src_ptr, atom.data_ptr(), tgt.data_ptr(), self.status)
+            W.conv.launch(True, src_ptr, atom.data_ptr(), self.status)
+            W.load.launch(False, atom.data_ptr(), tgt.data_ptr(), self.status)
             self.gen_atomic(W, ref, seed)
-            compare(atom.data_ptr(), ref.data_ptr(), W.atom_bytes, mism)
             torch.cuda.synchronize(self.device)
             self.check()
-            if int(mism.item()) != -1:
-                atomic_ok = False
+            if atomic_ok:
+                compare(atom.data_ptr(), ref.data_ptr(), W.atom_bytes, mism)
+                torch.cuda.synchronize(self.device)
+                if int(mism.item()) != -1:
+                    atomic_ok = False
             if target_ok:
-                W.load.launch(False, atom.data_ptr(), tgt.data_ptr(), self.status)
-                rev = self._reverse(W)
-                rev.launch(True, tgt.data_ptr(), back.data_ptr(), self.status)
+                self._reverse(W).launch(True, tgt.data_ptr(), back.data_ptr(), self.status)
                 compare(back.data_ptr(), ref.data_ptr(), W.atom_bytes, mism)
                 torch.cuda.synchronize(self.device)
                 if int(mism.item()) != -1:
                     target_ok = False
-        return {"windows": len(self.windows), "atomic_ok": atomic_ok, "target_ok": target_ok}
+        return {"windows": len(self.windows), "atomic_ok": atomic_ok, "target_ok": target_ok,
+                "fused_units": self.n_fused_units, "units": self.n_units}
 
     def _reverse(self, W: Window) -> Program:
         rev = getattr(W, "_rev", None)

@@ -92,3 +92,45 @@ def execute(runs, aux, tiles, src: np.ndarray, dst: np.ndarray) -> list:
                 for b in range(esz):
                     dst[pos + b] = out[:, b]
     return fails
+
+
+def execute_fused(runs, aux, tiles, src: np.ndarray, atom: np.ndarray, dst: np.ndarray) -> list:
+    """Interpret ucp_xrun tables (ucp_reshard_fused)."""
+    from paper_2406_18820_b200.plan import NO_ATOM
+
+    fails = []
+    for t in tiles:
+        r = runs[int(t["run"])]
+        ns, nd = int(r["n_src"]), int(r["n_dst"])
+        a = int(r["aux"])
+        srcs = [int(r["src"])] + [int(x) for x in aux[a:a + ns - 1]]
+        dsts = ([int(r["dst"])] + [int(x) for x in aux[a + ns - 1:a + ns - 1 + nd - 1]]) if nd else []
+        if int(r["flags"]) & RUN_ROWSPLIT:
+            rows = [int(t["row0"])]
+            c0, c1 = int(t["col0"]), int(t["col0"]) + int(t["count"])
+        else:
+            rows = range(int(t["row0"]), int(t["row0"]) + int(t["count"]))
+            c0, c1 = 0, int(r["cols"])
+        cols = np.arange(c0, c1, dtype=np.int64)
+        dt = int(r["dtype"])
+        esz = 4 if dt == 0 else 2
+        for row in rows:
+            sidx = row * int(r["src_pitch"]) + cols
+            v = _f32_at(src, srcs[0] + 4 * sidx)
+            bad = np.zeros(len(cols), dtype=bool)
+            for s in srcs[1:]:
+                bad |= v.view(np.uint32) != _f32_at(src, s + 4 * sidx).view(np.uint32)
+            if bad.any():
+                fails.append((int(t["run"]), int(row * int(r["cols"]) + cols[np.argmax(bad)])))
+            if int(r["atom"]) != NO_ATOM:
+                pos = int(r["atom"]) + 4 * (row * int(r["atom_pitch"]) + cols)
+                for b in range(4):
+                    atom[pos + b] = v.view(np.uint8).reshape(-1, 4)[:, b]
+            out = (v.view(np.uint8).reshape(-1, 4) if dt == 0 else
+                   (O.bf16_bits(v) if dt == 2 else O.f16_bits(v)).view(np.uint8).reshape(-1, 2))
+            didx = row * int(r["dst_pitch"]) + cols
+            for d in dsts:
+                pos = d + esz * didx
+                for b in range(esz):
+                    dst[pos + b] = out[:, b]
+    return fails

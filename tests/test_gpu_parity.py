@@ -279,24 +279,26 @@ def test_resume_paths(tmp_path):
     assert O.world_digest(wd) == O.world_digest(want)
 
 
-def test_reshard_plan_host_round_trip(golden):
-    for name in ("gqa", "moe", "pad", "MoE.4"):
+@pytest.mark.parametrize("fused", [False, True])
+def test_reshard_plan_host_round_trip(golden, fused):
+    for name in ("gqa", "moe", "pad", "MoE.4", "DenseGPT.0", "GQA.5"):
         row = next(r for r in golden["pipelines"] if r["name"] == name)
         spec = cell_spec(golden, row)
         src_cfg, tgt_cfg = cell_cfgs(row)
         shards = O.partition_mem(spec, O.init_state(spec, 7), src_cfg)
         for dt in (DType.F32, DType.BF16):
-            plan = ReshardPlan(spec, src_cfg, tgt_cfg, dtype=dt, window_bytes=1 << 16)
+            plan = ReshardPlan(spec, src_cfg, tgt_cfg, dtype=dt, window_bytes=1 << 16, fused=fused)
             out = plan.run_host({g: [a for _, a in v] for g, v in shards.items()})
             recs = {g: U.enumerate_rank_records(spec, tgt_cfg, g) for g in out}
             wd = {g: list(zip(recs[g], out[g])) for g in out}
             assert O.world_digest(wd) == row[f"world_{dt.name}"], (name, dt)
 
 
-def test_reshard_plan_device_verify_llama_slice():
+@pytest.mark.parametrize("fused", [False, True])
+def test_reshard_plan_device_verify_llama_slice(fused):
     # LLaMA-2-7B geometry (2 layers + vocab 32000 embed/head), cfg2 layouts
     spec, src, tgt, _ = U.bench_config("cfg2", n_layers=2)
-    plan = ReshardPlan(spec, src, tgt)
+    plan = ReshardPlan(spec, src, tgt, fused=fused)
     plan.synthesize(7)
     torch.cuda.synchronize()
     res = plan.verify(7)
@@ -308,7 +310,9 @@ def test_reshard_plan_device_verify_llama_slice():
         p = spec.param(pname)
         atomic_full[pname] = {k: (np.abs(O.gen_values(7, pname, k, p.shape)) if k == "v"
                                   else O.gen_values(7, pname, k, p.shape)) for k in ("weight", "m", "v")}
-    sub = ReshardPlan(spec, src, tgt, params=list(atomic_full))
+    if fused:
+        assert plan.n_fused_units == plan.n_units
+    sub = ReshardPlan(spec, src, tgt, params=list(atomic_full), fused=fused)
     shards = {}
     for g in range(src.world_size):
         shards[g] = {i: O.extract(spec.param(m.param), src, m, atomic_full[m.param][m.kind])
@@ -320,3 +324,17 @@ def test_reshard_plan_device_verify_llama_slice():
         for m, a in zip(recs, out[g]):
             want = O.extract(spec.param(m.param), tgt, m, atomic_full[m.param][m.kind])
             assert np.array_equal(a.view(np.uint32), want.view(np.uint32)), (g, m.param, m.kind)
+
+
+def test_fused_replica_mismatch_detected():
+    spec = U.make_model("GQA", {"n_layers": 2, "hidden": 64, "q_heads": 8, "kv_heads": 2})
+    src_cfg, tgt_cfg = cfg(dp=2, tp=2, zero="z1"), cfg(dp=2, tp=4, zero="z1")
+    shards = O.partition_mem(spec, O.init_state(spec, 7), src_cfg)
+    host = {g: [a.copy() for _, a in v] for g, v in shards.items()}
+    recs = U.enumerate_rank_records(spec, src_cfg, 3)
+    i = next(k for k, m in enumerate(recs) if m.param == "layers.1.attn_qkv" and m.kind == "weight")
+    host[3][i].reshape(-1)[17] = np.float32(7.0)
+    plan = ReshardPlan(spec, src_cfg, tgt_cfg, fused=True)
+    with pytest.raises(U.ReplicateMismatchError) as ei:
+        plan.run_host(host)
+    assert "layers.1.attn_qkv.weight" in str(ei.value) and "dp" in str(ei.value)

@@ -253,3 +253,84 @@ def test_finish_classed_partitions_tiles():
     cls = run_classes(runs)[tiles["run"]]
     assert (np.diff(cls) >= 0).all()
     assert counts[CLASS_GENERAL] > 0  # noise + misaligned dp=3 pieces
+
+
+def _fused_world(spec, src_cfg, tgt_cfg, shards, dtype, tile_bytes=4096, materialize=True):
+    from descr_interp import execute_fused
+    from paper_2406_18820_b200.plan import XRunTable, compile_fused
+
+    srecs, trecs = all_rank_records(spec, src_cfg), all_rank_records(spec, tgt_cfg)
+    frags, blobs, at = {}, [], 0
+    for g in range(src_cfg.world_size):
+        for meta, (_, arr) in zip(srecs[g], shards[g]):
+            frags.setdefault((meta.param, meta.kind), []).append((meta, at, arr.size))
+            blobs.append((at, arr))
+            at += align_up(arr.nbytes)
+    src = np.zeros(max(at, 16), dtype=np.uint8)
+    for o, a in blobs:
+        src[o:o + a.nbytes] = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
+    by_unit, outs, tat = {}, [], 0
+    for g in range(tgt_cfg.world_size):
+        for m in trecs[g]:
+            p = spec.param(m.param)
+            odt = dtype if m.kind == "weight" else DType.F32
+            n = fragment_elems(p, tgt_cfg, m)
+            by_unit.setdefault((m.param, m.kind), []).append((m, tat))
+            outs.append((g, m, tat, n, odt))
+            tat += align_up(n * odt.itemsize)
+    fx, rc, rl = XRunTable(), RunTable(), RunTable()
+    aoff, aat, fused = {}, 0, 0
+    for p in spec.params:
+        for k in STATE_KINDS:
+            aoff[(p.name, k)] = aat
+            odt = dtype if k == "weight" else DType.F32
+            fused += compile_fused(fx, rc, rl, p, src_cfg, frags[(p.name, k)], aat, tgt_cfg,
+                                   by_unit.get((p.name, k), []), odt, True, materialize)
+            aat += align_up(4 * p.numel)
+    atom = np.zeros(max(aat, 16), dtype=np.uint8)
+    dst = np.full(max(tat, 16), 0xCD, dtype=np.uint8)
+    xr, xa, xt, _ = fx.finish_classed(tile_bytes)
+    assert execute_fused(xr, xa, xt, src, atom, dst) == []
+    r1, a1, t1 = rc.finish(tile_bytes)
+    assert execute(r1, a1, t1, src, atom) == []
+    r2, a2, t2 = rl.finish(tile_bytes)
+    assert execute(r2, a2, t2, atom, dst) == []
+    world = {}
+    for g, m, o, n, odt in outs:
+        shape = U.plan.fragment_shape(spec.param(m.param), tgt_cfg, m)
+        world.setdefault(g, []).append((m, dst[o:o + n * odt.itemsize].view(odt.storage).reshape(shape)))
+    atomics = {k: atom[o:o + 4 * spec.param(k[0]).numel].view(np.float32) for k, o in aoff.items()}
+    return world, atomics, fused, fx
+
+
+@pytest.mark.parametrize("name", CELLS)
+@pytest.mark.parametrize("dtype", ["F32", "BF16"])
+def test_fused_matches_golden(golden, name, dtype):
+    row = next(r for r in golden["pipelines"] if r["name"] == name)
+    spec = cell_spec(golden, row)
+    src_cfg, tgt_cfg = cell_cfgs(row)
+    state = O.init_state(spec, 7)
+    shards = O.partition_mem(spec, state, src_cfg)
+    world, atomics, fused, _ = _fused_world(spec, src_cfg, tgt_cfg, shards, DType[dtype])
+    assert O.world_digest(world) == row[f"world_{dtype}"]
+    for (pname, k), a in atomics.items():
+        assert np.array_equal(a.view(np.uint32), state[pname][k].reshape(-1).view(np.uint32))
+    assert fused > 0
+
+
+def test_fused_covers_llama_units():
+    # every LLaMA unit fuses (no Partial params, all pieces 16-B phase aligned)
+    spec = U.llama_spec("7b", n_layers=1)
+    _, src, tgt, _ = U.bench_config("cfg2", n_layers=1)
+    from paper_2406_18820_b200.plan import XRunTable, compile_fused
+
+    srecs, trecs = all_rank_records(spec, src), all_rank_records(spec, tgt)
+    n_f = 0
+    for p in spec.params:
+        for k in STATE_KINDS:
+            frags = [(m, 1 << 40, fragment_elems(p, src, m)) for g in range(src.world_size)
+                     for m in srecs[g] if (m.param, m.kind) == (p.name, k)]
+            tg = [(m, 1 << 41) for g in range(tgt.world_size) for m in trecs[g]
+                  if (m.param, m.kind) == (p.name, k)]
+            n_f += compile_fused(XRunTable(), RunTable(), RunTable(), p, src, frags, 0, tgt, tg)
+    assert n_f == 3 * len(spec.params)
