@@ -247,6 +247,32 @@ class ReshardPlan:
             if ev:
                 ev[3].record(stream)
 
+    def step_windowed(self, seed: int = 7, stream=None, events=None) -> None:
+        """Reshard of a state larger than HBM: each window's
+        source fragments are synthesised into a window-sized arena just
+        before its launches (outside the events), then resharded exactly as
+        in ``step_device``. events[i] brackets window i's reshard launches
+        only, so summing them gives device-resident kernel time per step."""
+        arena = self.buf("src_win", self.max_src)
+        atom = self.buf("atom", self.max_atom)
+        ring = [self.buf("tgt0", self.max_tgt), self.buf("tgt1", self.max_tgt)]
+        for i, W in enumerate(self.windows):
+            self.gen_atomic(W, atom, seed, stream)
+            W.synth.launch(False, atom.data_ptr(), arena.data_ptr(), self.status, stream)
+            ev = events[i] if events is not None else None
+            if ev:
+                ev[0].record(stream)
+            W.fused.launch(arena.data_ptr(), atom.data_ptr(), ring[i % 2].data_ptr(), self.status,
+                           stream)
+            if ev:
+                ev[1].record(stream)
+            W.conv.launch(True, arena.data_ptr(), atom.data_ptr(), self.status, stream)
+            if ev:
+                ev[2].record(stream)
+            W.load.launch(False, atom.data_ptr(), ring[i % 2].data_ptr(), self.status, stream)
+            if ev:
+                ev[3].record(stream)
+
     def check(self) -> None:
         """Raise the reference exception for any data-dependent failure seen
         since the last status reset (replica mismatch / nonzero pad). The

@@ -338,3 +338,11 @@ def test_fused_replica_mismatch_detected():
     with pytest.raises(U.ReplicateMismatchError) as ei:
         plan.run_host(host)
     assert "layers.1.attn_qkv.weight" in str(ei.value) and "dp" in str(ei.value)
+
+
+def test_shard_hy_union_gpu():
+    p = ParamSpec("g", (64, 96), 0, ParamKind.MATMUL2D, 0)
+    full = np.arange(64 * 96, dtype=np.float32).reshape(64, 96)
+    msgs = [U.FragmentMsg(RecordMeta(p.name, "m", "shard_hy", (0, r, c), blk.shape), blk)
+            for (r, c), blk in O.hy_blocks(full, 4, 3)]
+    assert np.array_equal(U.union(p, cfg(), msgs[::-1]), full)

@@ -334,3 +334,28 @@ def test_fused_covers_llama_units():
                   if (m.param, m.kind) == (p.name, k)]
             n_f += compile_fused(XRunTable(), RunTable(), RunTable(), p, src, frags, 0, tgt, tg)
     assert n_f == 3 * len(spec.params)
+
+
+def test_shard_hy_grid_union():
+    # _union_hy (ucp/convert.py:196-218): blocks placed at (0, row, col)
+    p = ParamSpec("g", (8, 6), 0, ParamKind.MATMUL2D, 0)
+    full = np.arange(48, dtype=np.float32).reshape(8, 6)
+    blocks = O.hy_blocks(full, 2, 3)
+    src = np.zeros(48 * 4 + 256 * 6, dtype=np.uint8)
+    frags = []
+    for i, ((r, c), blk) in enumerate(blocks[::-1]):
+        o = 256 * i
+        src[o:o + blk.nbytes] = blk.view(np.uint8).reshape(-1)
+        frags.append((RecordMeta(p.name, "weight", "shard_hy", (0, r, c), blk.shape), o, blk.size))
+    tab = RunTable()
+    compile_union(tab, p, ParallelConfig(), frags, 0, True)
+    runs, aux, tiles = tab.finish(64)
+    dst = np.zeros(48 * 4, dtype=np.uint8)
+    assert execute(runs, aux, tiles, src, dst) == []
+    assert np.array_equal(dst.view(np.float32).reshape(8, 6), full)
+    assert np.array_equal(O.union(p, ParallelConfig(), [(f[0], blk) for f, (_, blk) in
+                                                        zip(frags, blocks[::-1])]), full)
+    with pytest.raises(U.OverlappingRangeError):
+        compile_union(RunTable(), p, ParallelConfig(), frags + frags[:1], 0, True)
+    with pytest.raises(U.MissingFragmentError):
+        compile_union(RunTable(), p, ParallelConfig(), frags[1:], 0, True)
