@@ -91,3 +91,56 @@ def alltoallv(send_buf: torch.Tensor, send_counts: list, recv_counts: list, grou
     recv = torch.empty(sum(recv_counts), dtype=torch.uint8, device=send_buf.device)
     dist.all_to_all_single(recv, send_buf, recv_counts, send_counts, group=group)
     return recv
+
+
+@dataclass
+class ExchangePlan:
+    """Rank-homed load exchange for one rank (target rank g homed on GPU
+    g mod world). Per window index w: this rank sends ``send[w][h]`` =
+    (offset, nbytes) of its window-w target region to GPU h and receives
+    ``recv[w][s]`` bytes from GPU s; ``index[(g, i)]`` = (w, byte offset in
+    the window-w receive buffer) of every target record homed here."""
+
+    rank: int
+    world: int
+    n_windows: int
+    send: list
+    recv: list
+    index: dict
+
+    def recv_bytes(self, w: int) -> int:
+        return sum(self.recv[w])
+
+
+def build_exchange(spec: ModelSpec, src, tgt, world: int, rank: int, window_bytes: int,
+                   dtype) -> ExchangePlan:
+    """Deterministic on every rank: replays every rank's window layout
+    (``reshard.layout_windows`` with home ordering) without touching a
+    device."""
+    from .reshard import layout_windows, make_windows
+
+    home_of = [g % world for g in range(tgt.world_size)]
+    plan = plan_work(spec, world)
+    layouts = []
+    for s in range(world):
+        mine = set(plan.groups[s])
+        wins = make_windows([p for p in spec.params if p.name in mine], window_bytes)
+        layout_windows(spec, src, tgt, wins, dtype, home_of, world)
+        layouts.append(wins)
+    n_w = max(len(w) for w in layouts)
+    send, recv, index = [], [], {}
+    for w in range(n_w):
+        mine = layouts[rank][w] if w < len(layouts[rank]) else None
+        send.append([tuple(mine.tgt_chunks[h]) if mine else (0, 0) for h in range(world)])
+        row, at = [], 0
+        for s in range(world):
+            W = layouts[s][w] if w < len(layouts[s]) else None
+            off, nb = W.tgt_chunks[rank] if W else (0, 0)
+            row.append(nb)
+            if W:
+                for g, i, m, o, n, dt in W.tgt_frags:
+                    if home_of[g] == rank:
+                        index[(g, i)] = (w, at + (o - off))
+            at += nb
+        recv.append(row)
+    return ExchangePlan(rank, world, n_w, send, recv, index)

@@ -58,6 +58,74 @@ class Window:
     load: object = None
     synth: object = None
     fused: object = None  # XProgram (fused mode)
+    tgt_chunks: list = field(default_factory=list)  # per home GPU: (offset, nbytes)
+
+
+def make_windows(params: list, budget: int) -> list:
+    """Contiguous groups of params (spec order) under a state-byte budget."""
+    out, cur, acc = [], [], 0
+    for p in params:
+        s = 12 * p.numel
+        if cur and acc + s > budget:
+            out.append(Window(cur))
+            cur, acc = [], 0
+        cur.append(p)
+        acc += s
+    if cur:
+        out.append(Window(cur))
+    return out
+
+
+def layout_windows(spec, src, tgt, windows, dtype, home_of=None, n_homes: int = 1) -> tuple:
+    """Assign arena offsets (host only, no device): source fragments of every
+    source rank, atomic tensors and target fragments of every target rank,
+    grouped by window. With ``home_of`` (target rank -> home GPU) the target
+    fragments of a window are ordered by home GPU so each window's target
+    region is directly the send buffer of the all-to-all-v exchange
+    (``tgt_chunks`` = per-home (offset, nbytes)). Returns (src_total,
+    tgt_total)."""
+    src_recs = all_rank_records(spec, src)
+    tgt_recs = all_rank_records(spec, tgt)
+    win_of = {p.name: i for i, w in enumerate(windows) for p in w.params}
+    for g in range(src.world_size):
+        for i, m in enumerate(src_recs[g]):
+            w = win_of.get(m.param)
+            if w is None:
+                continue
+            W = windows[w]
+            n = fragment_elems(spec.param(m.param), src, m)
+            W.src_frags.append((g, i, m, W.src_bytes, n))
+            W.src_bytes += align_up(4 * n)
+    order = list(range(tgt.world_size))
+    if home_of is not None:
+        order.sort(key=lambda g: (home_of[g], g))
+    for W in windows:
+        W.tgt_chunks = [[0, 0] for _ in range(n_homes)]
+    for g in order:
+        for i, m in enumerate(tgt_recs[g]):
+            w = win_of.get(m.param)
+            if w is None:
+                continue
+            W = windows[w]
+            dt = dtype if m.kind == "weight" else DType.F32
+            n = fragment_elems(spec.param(m.param), tgt, m)
+            h = home_of[g] if home_of is not None else 0
+            ch = W.tgt_chunks[h]
+            if ch[1] == 0:
+                ch[0] = W.tgt_bytes
+            W.tgt_frags.append((g, i, m, W.tgt_bytes, n, dt))
+            W.tgt_bytes += align_up(dt.itemsize * n)
+            ch[1] = W.tgt_bytes - ch[0]
+    sb = tb = 0
+    for W in windows:
+        for p in W.params:
+            for k in STATE_KINDS:
+                W.atom[(p.name, k)] = W.atom_bytes
+                W.atom_bytes += align_up(4 * p.numel)
+        W.src_base, W.tgt_base = sb, tb
+        sb += W.src_bytes
+        tb += W.tgt_bytes
+    return sb, tb
 
 
 class ReshardPlan:
@@ -66,11 +134,12 @@ class ReshardPlan:
     def __init__(self, spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig,
                  dtype: DType = DType.F32, strict: bool = True, params=None, device=None,
                  window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17, fused: bool = False,
-                 materialize_atomic: bool = True):
+                 materialize_atomic: bool = True, home_of=None, n_homes: int = 1):
         validate_model_config(spec, src)
         validate_model_config(spec, tgt)
         self.spec, self.src, self.tgt, self.dtype, self.strict = spec, src, tgt, dtype, strict
         self.fused_mode, self.materialize = fused, materialize_atomic
+        self.home_of, self.n_homes = home_of, n_homes
         self.device = require_device(device)
         self.tile_bytes = tile_bytes
         names = None if params is None else set(params)
@@ -84,51 +153,12 @@ class ReshardPlan:
     # ------------------------------------------------------------------ planning
 
     def _make_windows(self, budget: int) -> list:
-        out, cur, acc = [], [], 0
-        for p in self.params:
-            s = 12 * p.numel
-            if cur and acc + s > budget:
-                out.append(Window(cur))
-                cur, acc = [], 0
-            cur.append(p)
-            acc += s
-        if cur:
-            out.append(Window(cur))
-        return out
+        return make_windows(self.params, budget)
 
     def _layout(self) -> None:
-        src_recs = all_rank_records(self.spec, self.src)
-        tgt_recs = all_rank_records(self.spec, self.tgt)
-        win_of = {p.name: i for i, w in enumerate(self.windows) for p in w.params}
-        for g in range(self.src.world_size):
-            for i, m in enumerate(src_recs[g]):
-                w = win_of.get(m.param)
-                if w is None:
-                    continue
-                W = self.windows[w]
-                n = fragment_elems(self.spec.param(m.param), self.src, m)
-                W.src_frags.append((g, i, m, W.src_bytes, n))
-                W.src_bytes += align_up(4 * n)
-        for g in range(self.tgt.world_size):
-            for i, m in enumerate(tgt_recs[g]):
-                w = win_of.get(m.param)
-                if w is None:
-                    continue
-                W = self.windows[w]
-                dt = self.dtype if m.kind == "weight" else DType.F32
-                n = fragment_elems(self.spec.param(m.param), self.tgt, m)
-                W.tgt_frags.append((g, i, m, W.tgt_bytes, n, dt))
-                W.tgt_bytes += align_up(dt.itemsize * n)
-        sb = tb = 0
-        for W in self.windows:
-            for p in W.params:
-                for k in STATE_KINDS:
-                    W.atom[(p.name, k)] = W.atom_bytes
-                    W.atom_bytes += align_up(4 * p.numel)
-            W.src_base, W.tgt_base = sb, tb
-            sb += W.src_bytes
-            tb += W.tgt_bytes
-        self.src_total, self.tgt_total = sb, tb
+        lay = layout_windows(self.spec, self.src, self.tgt, self.windows, self.dtype,
+                             self.home_of, self.n_homes)
+        self.src_total, self.tgt_total = lay
         self.max_src = max((W.src_bytes for W in self.windows), default=0)
         self.max_atom = max((W.atom_bytes for W in self.windows), default=0)
         self.max_tgt = max((W.tgt_bytes for W in self.windows), default=0)

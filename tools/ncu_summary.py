@@ -59,7 +59,7 @@ def details(tag: str) -> list:
 
 def main():
     tag = sys.argv[1]
-    ls = launches(tag)
+    ls = launches(tag) if os.path.exists(os.path.join(OUT, f"launches_{tag}.csv")) else []
     tot = sum(x["ms"] for x in ls)
     by = OrderedDict()
     for x in ls:
