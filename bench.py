@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--windowed", action="store_true",
                     help="synthesise each window's sources just before it (states > HBM); "
                          "times the per-window reshard launches only")
+    ap.add_argument("--home", default="param", choices=["param", "rank"],
+                    help="param: targets stay on the param-owner GPU (no collective); rank: "
+                         "target rank g is homed on GPU g mod N, one NCCL all-to-all-v per window")
     ap.add_argument("--unfused", action="store_true",
                     help="separate convert and load launches (atomic re-read from HBM)")
     ap.add_argument("--cpu-threads", type=int, default=os.cpu_count())
@@ -234,16 +237,24 @@ def run_ours(args):
     from paper_2406_18820_b200.dist import init_process_group, owned_params
     from paper_2406_18820_b200.reshard import ReshardPlan
 
-    rank, world, local = init_process_group("nccl")
+    rank, world, local = init_process_group("nccl", force=args.home == "rank")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import torch.distributed as dist
 
     spec, src, tgt, desc = bench_config(args.config, args.layers)
     mine = owned_params(spec, rank, world) if world > 1 else None
+    homed = args.home == "rank"
     plan = ReshardPlan(spec, src, tgt, params=mine, device=dev,
                        window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024,
-                       fused=not args.unfused)
+                       fused=not args.unfused,
+                       home_of=[g % world for g in range(tgt.world_size)] if homed else None,
+                       n_homes=world if homed else 1)
+    exch = None
+    if homed:
+        from paper_2406_18820_b200.dist import build_exchange
+
+        exch = build_exchange(spec, src, tgt, world, rank, int(args.window_gb * GB), plan.dtype)
     S_local = plan.state_bytes
     free, _ = torch.cuda.mem_get_info(dev)
     need = plan.src_total + plan.max_atom * 3 + plan.max_tgt * 2 + (2 << 30)
@@ -263,8 +274,15 @@ def run_ours(args):
 
     stream = torch.cuda.current_stream()
     plan.status.reset()
-    step = (lambda ev=None: plan.step_windowed(7, stream, ev)) if windowed else \
-        (lambda ev=None: plan.step_device(stream, ev))
+    if homed and windowed:
+        raise SystemExit("--home rank needs the source arena resident (use more GPUs)")
+    comm_stream = torch.cuda.Stream(dev) if homed else None
+    if homed:
+        step = lambda ev=None: plan.step_device_homed(exch, None, stream, comm_stream, ev)
+    elif windowed:
+        step = lambda ev=None: plan.step_windowed(7, stream, ev)
+    else:
+        step = lambda ev=None: plan.step_device(stream, ev)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -272,7 +290,8 @@ def run_ours(args):
         plan.check()
 
     nW = len(plan.windows)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nW)]
+    nEv = exch.n_windows if exch else nW
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nEv)]
            for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
@@ -435,7 +454,10 @@ def run_ours(args):
                          plan.bytes["R_c"] + plan.bytes["W_c"] + plan.fused_bytes["R"] + 2 * plan.fused_bytes["W_atom"]
                          + plan.bytes["R_l"] + plan.bytes["W_l"] + plan.fused_bytes["W_tgt"]),
                      "windows": nW,
-                     "parallelism": f"param-sharded x{world}", "l2": "inputs larger than L2 "
+                     "parallelism": f"param-sharded x{world}" + (
+                         ", rank-homed targets: one NCCL all-to-all-v per window "
+                         f"({sum(sum(nb for _, nb in exch.send[w]) - exch.send[w][rank][1] for w in range(exch.n_windows)) / GB:.2f} GB sent/step by rank 0)"
+                         if homed else ", param-homed targets (no collective)"), "l2": "inputs larger than L2 "
                      f"({plan.src_total / GB:.1f} GB source arena per rank)",
                      "residency": ("windowed: sources synthesised per window outside the timed "
                                    "events; value = S / sum of per-window reshard time")
@@ -443,7 +465,7 @@ def run_ours(args):
                      "strict_replicate": True},
           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
           "gpu_launches": gpu_launches, "parity": parity}, rank)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -57,11 +57,14 @@ def env_rank() -> tuple:
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def init_process_group(backend: str = "nccl"):
+def init_process_group(backend: str = "nccl", force: bool = False):
+    """Initialise torch.distributed from torchrun's environment when more
+    than one rank runs (or ``force``: a 1-rank group, e.g. to exercise the
+    collective path on one GPU)."""
     import torch.distributed as dist
 
     rank, world, local = env_rank()
-    if world > 1 and not dist.is_initialized():
+    if (world > 1 or force) and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
         if backend == "nccl":

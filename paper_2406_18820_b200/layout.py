@@ -43,7 +43,34 @@ def validate_model_config(spec: ModelSpec, cfg: ParallelConfig) -> None:
                 f"interleaved(v={cfg.pp_schedule.v}) needs n_layers divisible by pp*v = "
                 f"{chunks}, got {spec.n_layers}")
     for p in spec.params:
-        tp_mode(p, cfg.tp)
+        mode_of(p, cfg)
+
+
+def vocab_padded_rows(p: ParamSpec, cfg: ParallelConfig):
+    """Padded row count of an embedding / output layer under Megatron-style
+    vocab padding (extension): ceil(V / (m * tp)) * m * tp, or
+    None when cfg.vocab_multiple == 1 or the param is not vocab-sized."""
+    m = getattr(cfg, "vocab_multiple", 1)
+    if m <= 1 or p.kind not in _VOCAB or not p.shape:
+        return None
+    unit = m * cfg.tp
+    return -(-p.shape[0] // unit) * unit
+
+
+def mode_of(p: ParamSpec, cfg: ParallelConfig) -> str:
+    """tp_mode with the vocab-padding extension: a padded vocab param is
+    Shard-V over its padded rows (always divisible)."""
+    if vocab_padded_rows(p, cfg) is not None:
+        return "full" if cfg.tp == 1 else SHARD_V
+    return tp_mode(p, cfg.tp)
+
+
+def frag_shape(p: ParamSpec, mode: str, cfg: ParallelConfig) -> tuple:
+    """tp_fragment_shape with the vocab-padding extension."""
+    rows = vocab_padded_rows(p, cfg)
+    if rows is not None:
+        return (rows // cfg.tp,) + tuple(p.shape[1:])
+    return tp_fragment_shape(p, mode, cfg.tp)
 
 
 def pp_layer_map(n_layers: int, pp: int, schedule) -> list:
@@ -165,7 +192,7 @@ def _numel(shape) -> int:
 def _all_records(spec: ModelSpec, cfg: ParallelConfig) -> tuple:
     stages = pp_layer_map(spec.n_layers, cfg.pp, cfg.pp_schedule)
     last = max(spec.n_layers - 1, 0)
-    modes = [tp_mode(p, cfg.tp) for p in spec.params]
+    modes = [mode_of(p, cfg) for p in spec.params]
     out = []
     for g in range(cfg.world_size):
         pp_r, tp_r, dp_r = cfg.coords_of(g)
@@ -174,7 +201,7 @@ def _all_records(spec: ModelSpec, cfg: ParallelConfig) -> tuple:
         for p, mode in zip(spec.params, modes):
             if min(p.layer_index, last) not in mine:
                 continue
-            fshape = tp_fragment_shape(p, mode, cfg.tp)
+            fshape = frag_shape(p, mode, cfg)
             fnumel = _numel(fshape)
             segs = p.nc_segments if mode == SHARD_NC else None
             for kind in STATE_KINDS:

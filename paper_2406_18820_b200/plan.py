@@ -38,7 +38,18 @@ from ._errors import (
     PatternCoverageError,
     ShapeError,
 )
-from .layout import PARTIAL, REPLICATE, SHARD_H, SHARD_HY, SHARD_NC, SHARD_V, tp_fragment_shape, tp_mode
+from .layout import (
+    PARTIAL,
+    REPLICATE,
+    SHARD_H,
+    SHARD_HY,
+    SHARD_NC,
+    SHARD_V,
+    frag_shape,
+    mode_of,
+    tp_fragment_shape,
+    vocab_padded_rows,
+)
 from .spec import DType, ParallelConfig, ParamSpec, RecordMeta
 
 # --------------------------------------------------------------------------- ABI
@@ -254,14 +265,21 @@ def make_tiles(runs: np.ndarray, tile_bytes: int, extra_bpe=None) -> np.ndarray:
 # --------------------------------------------------------------------------- geometry
 
 
-def tp_correspondences(p: ParamSpec, mode: str, tp: int, t: int) -> list:
+def tp_correspondences(p: ParamSpec, mode: str, tp: int, t: int, vrows=None) -> list:
     """[(f0, x_off, x_pitch, rows, cols)]: TP fragment t's flat elements
     f0 + i*cols + j  <->  atomic element x_off + i*x_pitch + j.
-    The inverse of extract_fragment's slicing (ucp/parallel.py:383-399)."""
+    The inverse of extract_fragment's slicing (ucp/parallel.py:383-399).
+    ``vrows``: padded vocab rows (extension); fragment rows beyond the real
+    vocabulary have no atomic counterpart (stripped / zero-filled)."""
     shape = tuple(p.shape)
     n = _numel(shape)
     if n == 0:
         return []
+    if vrows is not None:
+        w = _numel(shape[1:])
+        r = vrows // tp
+        real = max(0, min(r, shape[0] - t * r))
+        return [(0, t * r * w, real * w, 1, real * w)] if real else []
     if mode in ("full", REPLICATE, PARTIAL):
         return [(0, 0, n, 1, n)]
     if mode == SHARD_V:
@@ -364,7 +382,7 @@ def _collapse(p, cfg, t, items, mode, strict, where):
         dups = [d for d, grp in seen.items() if len(grp) > 1]
         if dups:
             raise OverlappingRangeError(f"{ctx}: duplicate fragments from dp ranks {dups}")
-        fshape = _mode_shape(p, mode, cfg.tp)
+        fshape = _mode_shape(p, mode, cfg)
         fn = _numel(fshape)
         maps = []
         for d in range(cfg.dp if strict else 1):
@@ -389,7 +407,7 @@ def _collapse(p, cfg, t, items, mode, strict, where):
             raise PaddingError(f"{ctx}: pad recorded on a non-final flat shard")
         segs.append((lo, hi, off))
     pad = ranged[-1][0].pad_elems
-    fn = _numel(tp_fragment_shape(p, mode, cfg.tp))
+    fn = _numel(frag_shape(p, mode, cfg))
     if pad < 0 or fn + pad != pos:
         raise PaddingError(
             f"pad arithmetic mismatch: {pos} elements != {fn} + pad {pad}")
@@ -403,9 +421,9 @@ def _collapse(p, cfg, t, items, mode, strict, where):
     return [smap], pad_runs
 
 
-def _mode_shape(p, mode, tp):
+def _mode_shape(p, mode, cfg):
     if mode in ("full", REPLICATE, PARTIAL, SHARD_V, SHARD_H, SHARD_NC):
-        return tp_fragment_shape(p, mode, tp)
+        return frag_shape(p, mode, cfg)
     raise ManifestError(f"{p.name}: unknown pattern tag {mode!r}")
 
 
@@ -462,16 +480,18 @@ def compile_union(tab: RunTable, p: ParamSpec, cfg: ParallelConfig, frags: list,
         segs = frags[0][0].segments
         if segs is None or tuple(map(tuple, segs)) != tuple(map(tuple, p.nc_segments or ())):
             raise ManifestError(f"{where}: nc segments disagree with the model spec")
-    fshape = tp_fragment_shape(p, mode, cfg.tp)
-    _check_assembled(p, mode, fshape, cfg.tp, where)
+    fshape = frag_shape(p, mode, cfg)
+    vrows = vocab_padded_rows(p, cfg)
+    if vrows is None:
+        _check_assembled(p, mode, fshape, cfg.tp, where)
     fn = _numel(fshape)
 
     for off, n in pads:
         tab.add(srcs=[off], dsts=[], src_pitch=n, dst_pitch=n, rows=1, cols=n,
                 op=OP_CHECKZERO, tag=tag, labels=[("pad",)])
     if mode == "full":
-        _emit_group(tab, p, [per_tp[0]], tp_correspondences(p, "full", 1, 0), fn, dst_off,
-                    OP_COPY, tag, 1)
+        _emit_group(tab, p, [per_tp[0]], tp_correspondences(p, "full", 1, 0, vrows), fn,
+                    dst_off, OP_COPY, tag, 1)
     elif mode == REPLICATE:
         grp = [m for t in range(cfg.tp) for m in per_tp[t]] if strict else per_tp[0][:1]
         _emit_group(tab, p, [grp], tp_correspondences(p, mode, cfg.tp, 0), fn, dst_off,
@@ -482,7 +502,7 @@ def compile_union(tab: RunTable, p: ParamSpec, cfg: ParallelConfig, frags: list,
                     OP_MEAN, tag, cfg.tp)
     else:
         for t in range(cfg.tp):
-            _emit_group(tab, p, [per_tp[t]], tp_correspondences(p, mode, cfg.tp, t), fn,
+            _emit_group(tab, p, [per_tp[t]], tp_correspondences(p, mode, cfg.tp, t, vrows), fn,
                         dst_off, OP_COPY, tag, 1)
     return tag
 
@@ -552,8 +572,9 @@ def compile_extract(tab: RunTable, p: ParamSpec, cfg: ParallelConfig, targets: l
     if not targets:
         return -1
     tag = tab.unit(p.name, targets[0][0].kind)
-    mode = tp_mode(p, cfg.tp)
-    fshape = tp_fragment_shape(p, mode, cfg.tp)
+    mode = mode_of(p, cfg)
+    fshape = frag_shape(p, mode, cfg)
+    vrows = vocab_padded_rows(p, cfg)
     fn = _numel(fshape)
     esz = _ESZ[dtype]
     groups = defaultdict(list)
@@ -570,30 +591,36 @@ def compile_extract(tab: RunTable, p: ParamSpec, cfg: ParallelConfig, targets: l
     padded = -(-fn // cfg.dp) * cfg.dp if fn else 0
     for (key_t, fr), dsts in groups.items():
         t = max(key_t, 0)
-        corrs = tp_correspondences(p, mode if mode != PARTIAL else "full", cfg.tp, t)
+        corrs = tp_correspondences(p, mode if mode != PARTIAL else "full", cfg.tp, t, vrows)
         op = OP_NOISE if mode == PARTIAL and key_t >= 0 else OP_COPY
         if fr is None:
             lo, hi = 0, fn
         else:
             lo, hi = min(fr[0], padded), min(max(fr[1], fr[0]), padded)
-        real_hi = min(hi, fn)
+        covered = []
         for corr in corrs:
-            for fs, xs, xp, rows, cols in split_rows(corr, lo, real_hi):
+            for fs, xs, xp, rows, cols in split_rows(corr, lo, min(hi, fn)):
                 tab.add(srcs=[src_off + 4 * xs], dsts=[d + esz * (fs - lo) for d in dsts],
                         src_pitch=xp, dst_pitch=corr[4], rows=rows, cols=cols, op=op,
                         dtype=dtype, tp_rank=t, tp=cfg.tp, tag=tag)
-        if hi > max(lo, fn):
-            z0 = max(lo, fn)
-            tab.add(srcs=[], dsts=[d + esz * (z0 - lo) for d in dsts], src_pitch=hi - z0,
-                    dst_pitch=hi - z0, rows=1, cols=hi - z0, op=OP_ZERO, dtype=dtype, tag=tag)
+                covered.append((fs, fs + rows * cols))
+        # zero-fill whatever no correspondence covers: the ZeRO pad tail and
+        # (extension) padded vocabulary rows
+        at = lo
+        for a, b in sorted(covered) + [(hi, hi)]:
+            if a > at:
+                tab.add(srcs=[], dsts=[d + esz * (at - lo) for d in dsts], src_pitch=a - at,
+                        dst_pitch=a - at, rows=1, cols=a - at, op=OP_ZERO, dtype=dtype, tag=tag)
+            at = max(at, b)
     return tag
 
 
 def fragment_elems(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta) -> int:
     """Element count of the fragment extract_fragment returns for meta."""
+    fshape = frag_shape(p, mode_of(p, cfg), cfg)
     if meta.flat_range is None:
-        return _numel(tp_fragment_shape(p, tp_mode(p, cfg.tp), cfg.tp))
-    fn = _numel(tp_fragment_shape(p, tp_mode(p, cfg.tp), cfg.tp))
+        return _numel(fshape)
+    fn = _numel(fshape)
     padded = -(-fn // cfg.dp) * cfg.dp if fn else 0
     lo, hi = meta.flat_range
     lo, hi = min(lo, padded), min(max(hi, lo), padded)
@@ -602,7 +629,7 @@ def fragment_elems(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta) -> int:
 
 def fragment_shape(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta) -> tuple:
     if meta.flat_range is None:
-        return tuple(tp_fragment_shape(p, tp_mode(p, cfg.tp), cfg.tp))
+        return tuple(frag_shape(p, mode_of(p, cfg), cfg))
     return (fragment_elems(p, cfg, meta),)
 
 

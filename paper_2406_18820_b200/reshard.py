@@ -277,6 +277,54 @@ class ReshardPlan:
             if ev:
                 ev[3].record(stream)
 
+    def step_device_homed(self, exch, group=None, stream=None, comm_stream=None,
+                          events=None) -> None:
+        """Rank-homed variant of ``step_device`` (north_star item 3): after
+        window w's reshard launches, its target region (ordered by home GPU,
+        see ``layout_windows``) is exchanged with one all-to-all-v over NCCL
+        on ``comm_stream`` while window w+1 computes. Window w+2 reuses the
+        ring slot only after the exchange of w has drained it."""
+        import torch.distributed as dist
+
+        stream = stream or torch.cuda.current_stream(self.device)
+        comm_stream = comm_stream or torch.cuda.Stream(self.device)
+        arena = self._bufs["src_arena"]
+        atom = self.buf("atom", self.max_atom)
+        ring = [self.buf("tgt0", self.max_tgt), self.buf("tgt1", self.max_tgt)]
+        rmax = max((exch.recv_bytes(w) for w in range(exch.n_windows)), default=0)
+        recv = [self.buf("rcv0", rmax), self.buf("rcv1", rmax)]
+        done = [None, None]
+        for w in range(exch.n_windows):
+            slot = w % 2
+            if done[slot] is not None:
+                stream.wait_event(done[slot])
+            W = self.windows[w] if w < len(self.windows) else None
+            ev = events[w] if events is not None and w < len(events) else None
+            if ev:
+                ev[0].record(stream)
+            if W is not None:
+                src_ptr = arena.data_ptr() + W.src_base
+                W.fused.launch(src_ptr, atom.data_ptr(), ring[slot].data_ptr(), self.status, stream)
+                W.conv.launch(True, src_ptr, atom.data_ptr(), self.status, stream)
+                W.load.launch(False, atom.data_ptr(), ring[slot].data_ptr(), self.status, stream)
+            ready = torch.cuda.Event()
+            ready.record(stream)
+            if ev:
+                ev[1].record(stream)
+                ev[2].record(stream)
+                ev[3].record(stream)
+            sizes = [nb for _, nb in exch.send[w]]
+            with torch.cuda.stream(comm_stream):
+                comm_stream.wait_event(ready)
+                dist.all_to_all_single(recv[slot][:exch.recv_bytes(w)], ring[slot][:sum(sizes)],
+                                       exch.recv[w], sizes, group=group)
+                fin = torch.cuda.Event()
+                fin.record(comm_stream)
+            done[slot] = fin
+        for fin in done:
+            if fin is not None:
+                stream.wait_event(fin)
+
     def step_windowed(self, seed: int = 7, stream=None, events=None) -> None:
         """Reshard of a state larger than HBM: each window's
         source fragments are synthesised into a window-sized arena just

@@ -186,6 +186,10 @@ class ParallelConfig:
     sp: int = 1
     zero_stage: ZeroStage = ZeroStage.Z0
     pp_schedule: PPSchedule = field(default_factory=PPSchedule)
+    # extension: Megatron-style vocab padding of embedding /
+    # output-layer rows to a multiple of vocab_multiple * tp; 1 = none (the
+    # reference has no vocab padding)
+    vocab_multiple: int = 1
 
     @property
     def world_size(self) -> int:
@@ -208,6 +212,8 @@ class ParallelConfig:
             raise IncompatibleConfigError("interleaved schedule needs pp >= 2")
         if self.sp > 1 and self.dp % self.sp:
             raise IncompatibleConfigError("sp folds into dp and must divide it")
+        if self.vocab_multiple < 1:
+            raise IncompatibleConfigError("vocab_multiple must be >= 1")
 
 
 @dataclass(frozen=True)
@@ -269,16 +275,20 @@ def spec_from_dict(d: dict) -> ModelSpec:
 
 
 def config_to_dict(cfg: ParallelConfig) -> dict:
-    return {"dp": cfg.dp, "tp": cfg.tp, "pp": cfg.pp, "sp": cfg.sp,
-            "zero_stage": cfg.zero_stage.value, "pp_schedule": cfg.pp_schedule.kind,
-            "pp_interleave": cfg.pp_schedule.v}
+    d = {"dp": cfg.dp, "tp": cfg.tp, "pp": cfg.pp, "sp": cfg.sp,
+         "zero_stage": cfg.zero_stage.value, "pp_schedule": cfg.pp_schedule.kind,
+         "pp_interleave": cfg.pp_schedule.v}
+    if cfg.vocab_multiple != 1:
+        d["vocab_multiple"] = cfg.vocab_multiple  # extension key, absent by default
+    return d
 
 
 def config_from_dict(d: dict) -> ParallelConfig:
     try:
         cfg = ParallelConfig(dp=int(d["dp"]), tp=int(d["tp"]), pp=int(d["pp"]), sp=int(d["sp"]),
                              zero_stage=ZeroStage(d["zero_stage"]),
-                             pp_schedule=PPSchedule(d["pp_schedule"], int(d["pp_interleave"])))
+                             pp_schedule=PPSchedule(d["pp_schedule"], int(d["pp_interleave"])),
+                             vocab_multiple=int(d.get("vocab_multiple", 1)))
     except (KeyError, ValueError, TypeError) as e:
         raise IncompatibleConfigError(f"bad parallel config: {e}") from e
     cfg.validate()

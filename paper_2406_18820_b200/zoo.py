@@ -99,8 +99,9 @@ def llama_spec(size: str, n_layers: int | None = None) -> ModelSpec:
     return ModelSpec(f"LLaMA-2-{size}", L, (), tuple(ps))
 
 
-def _cfg(dp=1, tp=1, pp=1, sp=1, zero="z1") -> ParallelConfig:
-    return ParallelConfig(dp=dp, tp=tp, pp=pp, sp=sp, zero_stage=ZeroStage(zero))
+def _cfg(dp=1, tp=1, pp=1, sp=1, zero="z1", vocab_multiple=1) -> ParallelConfig:
+    return ParallelConfig(dp=dp, tp=tp, pp=pp, sp=sp, zero_stage=ZeroStage(zero),
+                          vocab_multiple=vocab_multiple)
 
 
 def bench_config(name: str, n_layers: int | None = None):
@@ -112,8 +113,11 @@ def bench_config(name: str, n_layers: int | None = None):
         return (llama_spec("7b", n_layers), _cfg(4, 2), _cfg(2, 4),
                 "LLaMA-2-7B ZeRO-1 TP2/DP4 -> TP4/DP2")
     if name == "cfg3":
-        return (llama_spec("13b", n_layers), _cfg(2, 2, 2), _cfg(2, 4),
-                "LLaMA-2-13B ZeRO-1 TP2/PP2/DP2 -> TP4/DP2")
+        # Megatron vocab padding (make-vocab-size-divisible-by 128): 32000 rows
+        # at TP2, 32256 at TP4 -- stripped by convert, zero re-padded by load
+        return (llama_spec("13b", n_layers), _cfg(2, 2, 2, vocab_multiple=128),
+                _cfg(2, 4, vocab_multiple=128),
+                "LLaMA-2-13B ZeRO-1 TP2/PP2/DP2 -> TP4/DP2, vocab padded to 128*tp")
     if name == "cfg4":
         spec = make_model("DenseGPT", {"n_layers": n_layers or 48, "hidden": 7168})
         return (spec, _cfg(8, zero="z3"), _cfg(4, 2, sp=2, zero="z2"),

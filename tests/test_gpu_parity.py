@@ -346,3 +346,26 @@ def test_shard_hy_union_gpu():
     msgs = [U.FragmentMsg(RecordMeta(p.name, "m", "shard_hy", (0, r, c), blk.shape), blk)
             for (r, c), blk in O.hy_blocks(full, 4, 3)]
     assert np.array_equal(U.union(p, cfg(), msgs[::-1]), full)
+
+
+def test_vocab_padding_file_pipeline(tmp_path):
+    spec = U.make_model("GQA", {"n_layers": 2, "hidden": 64, "q_heads": 8, "kv_heads": 2})
+    src_cfg = ParallelConfig(dp=2, tp=2, zero_stage=ZeroStage.Z1, vocab_multiple=100)
+    tgt_cfg = ParallelConfig(dp=3, tp=4, zero_stage=ZeroStage.Z1, vocab_multiple=36)
+    state = O.init_state(spec, 7)
+    src, shards = _src_tree(tmp_path, spec, src_cfg)
+    atom = str(tmp_path / "atomic")
+    U.convert(src, atom)
+    want = str(tmp_path / "want")
+    O.write_atomic(spec, state, want, fingerprint=O.config_fingerprint(src))
+    assert O.dir_digest(atom) == O.dir_digest(want)
+    for dt in (DType.F32, DType.BF16):
+        world = U.load(atom, tgt_cfg, dtype=dt)
+        wd = {g: [(s.meta, s.tensor.data) for s in world.shards[g]] for g in world.shards}
+        assert O.world_digest(wd) == O.world_digest(O.load_mem(spec, state, tgt_cfg, dt.name))
+    for fused in (False, True):
+        plan = ReshardPlan(spec, src_cfg, tgt_cfg, dtype=DType.BF16, fused=fused)
+        out = plan.run_host({g: [a for _, a in v] for g, v in shards.items()})
+        recs = {g: U.enumerate_rank_records(spec, tgt_cfg, g) for g in out}
+        assert O.world_digest({g: list(zip(recs[g], out[g])) for g in out}) == \
+            O.world_digest(O.load_mem(spec, state, tgt_cfg, "BF16"))
