@@ -43,6 +43,7 @@ from .api import (
     load,
     load_atomic,
     partition,
+    reshard,
     resident_bound_elements,
     resume,
     source_fingerprint,

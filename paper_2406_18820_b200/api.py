@@ -361,6 +361,81 @@ def _io_pool(n_workers: int) -> ThreadPoolExecutor:
     return ThreadPoolExecutor(max_workers=max(4, min(32, 2 * n_workers, os.cpu_count() or 4)))
 
 
+# --------------------------------------------------------------------------- pipeline
+
+
+def _write_atomic(out_dir: str, o, ov: memoryview) -> None:
+    p, kind, at = o
+    pdir = os.path.join(out_dir, p.name)
+    os.makedirs(pdir, exist_ok=True)
+    codec.write_raw(os.path.join(pdir, ATOMIC_FILES[kind]), DType.F32, p.shape,
+                    ov[at:at + 4 * p.numel])
+
+
+def _pipeline(wplans: list, dev, key: str, n_workers: int, gather: bool, emit) -> None:
+    """Windowed file pipeline, double-buffered so file reads of window w+1
+    and the output handling of window w-1 overlap the GPU work of window w:
+
+        read files (thread pool) -> pinned -> H2D -> kernel -> D2H -> pinned
+        -> emit(o, view) per output (thread pool)
+
+    wplans: [(Program, read jobs (path, header, offset), src bytes, outs,
+    dst bytes)]. Data-dependent failures raise after their window syncs, so
+    a failing window never reaches emit (torn output, ucp/convert.py:503)."""
+    if not wplans:
+        return
+    ms = max(w[2] for w in wplans)
+    md = max(w[4] for w in wplans)
+    h_src = [_STAGE.host_buf(f"{key}_src{i}", ms) for i in range(2)]
+    h_dst = [_STAGE.host_buf(f"{key}_dst{i}", md) for i in range(2)]
+    d_src = [_STAGE.dev_buf(f"{key}_src{i}", ms, dev) for i in range(2)]
+    d_dst = [_STAGE.dev_buf(f"{key}_dst{i}", md, dev) for i in range(2)]
+    st = _status(dev)
+    stream = torch.cuda.current_stream(dev)
+    nthreads = max(4, min(32, 2 * n_workers, os.cpu_count() or 4))
+    with ThreadPoolExecutor(nthreads) as rpool, ThreadPoolExecutor(nthreads) as wpool:
+
+        def reads(w):
+            hv = memoryview(h_src[w % 2].numpy())
+            return [rpool.submit(codec.read_payload_into, path, hdr, hv[at:at + hdr.nbytes])
+                    for path, hdr, at in wplans[w][1]]
+
+        pending = {0: reads(0)}
+        written: dict = {}
+        h2d_ev: dict = {}
+        try:
+            for w, (prog, _, s_at, outs, d_at) in enumerate(wplans):
+                slot = w % 2
+                for f in pending.pop(w):
+                    f.result()
+                d_src[slot][:s_at].copy_(h_src[slot][:s_at], non_blocking=True)
+                h2d_ev[w] = torch.cuda.Event()
+                h2d_ev[w].record(stream)
+                st.reset(stream)
+                prog.launch(gather, d_src[slot].data_ptr(), d_dst[slot].data_ptr(), st, stream)
+                for f in written.pop(w - 2, ()):  # h_dst[slot] is free again
+                    f.result()
+                h_dst[slot][:d_at].copy_(d_dst[slot][:d_at], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(stream)
+                if w + 1 < len(wplans):
+                    if w >= 1:
+                        h2d_ev.pop(w - 1).synchronize()  # h_src[(w+1)%2] drained
+                    pending[w + 1] = reads(w + 1)
+                done.synchronize()
+                st.raise_if_bad(prog, d_src[slot].data_ptr())
+                ov = memoryview(h_dst[slot].numpy())
+                written[w] = [wpool.submit(emit, o, ov) for o in outs]
+            for fs in written.values():
+                for f in fs:
+                    f.result()
+        except BaseException:
+            for fs in list(pending.values()) + list(written.values()):
+                for f in fs:
+                    f.cancel()
+            raise
+
+
 # --------------------------------------------------------------------------- convert
 
 
@@ -412,48 +487,26 @@ def convert(src: str, out_dir: str, n_workers: int = 1, inner: int = 1,
 
     windows = _windows(list(spec.params), lambda p: src_size(p) + 3 * align_up(4 * p.numel),
                        window_bytes)
-    st = _status(dev)
-    with _io_pool(n_workers) as pool:
-        for wparams in windows:
-            tab = RunTable()
-            jobs, s_at, a_at, outs = [], 0, 0, []
-            for p in wparams:
-                for kind in STATE_KINDS:
-                    items = units.get((p.name, kind))
-                    if not items:
-                        raise MissingFragmentError(f"{p.name}.{kind}: no fragments arrived")
-                    frags = []
-                    for meta, path, hdr in items:
-                        jobs.append((path, hdr, s_at))
-                        frags.append((meta, s_at, hdr.numel))
-                        s_at += align_up(hdr.nbytes)
-                    compile_union(tab, p, cfg, frags, a_at, strict_replicate)
-                    outs.append((p, kind, a_at))
-                    a_at += align_up(4 * p.numel)
-            h_src = _STAGE.host_buf("conv_src", s_at)
-            hv = memoryview(h_src.numpy())
-            list(pool.map(lambda j: codec.read_payload_into(j[0], j[1], hv[j[2]:j[2] + j[1].nbytes]),
-                          jobs))
-            d_src = _STAGE.dev_buf("conv_src", s_at, dev)
-            d_dst = _STAGE.dev_buf("conv_dst", a_at, dev)
-            d_src[:s_at].copy_(h_src[:s_at], non_blocking=True)
-            prog = Program(tab, dev)
-            st.reset()
-            prog.launch(True, d_src.data_ptr(), d_dst.data_ptr(), st)
-            h_dst = _STAGE.host_buf("conv_dst", a_at)
-            h_dst[:a_at].copy_(d_dst[:a_at], non_blocking=True)
-            torch.cuda.synchronize(dev)
-            st.raise_if_bad(prog, d_src.data_ptr())
-            ov = memoryview(h_dst.numpy())
-
-            def write(o):
-                p, kind, at = o
-                pdir = os.path.join(out_dir, p.name)
-                os.makedirs(pdir, exist_ok=True)
-                codec.write_raw(os.path.join(pdir, ATOMIC_FILES[kind]), DType.F32, p.shape,
-                                ov[at:at + 4 * p.numel])
-
-            list(pool.map(write, outs))
+    # compile every window first: all metadata validation precedes any IO
+    wplans = []
+    for wparams in windows:
+        tab = RunTable()
+        jobs, s_at, a_at, outs = [], 0, 0, []
+        for p in wparams:
+            for kind in STATE_KINDS:
+                items = units.get((p.name, kind))
+                if not items:
+                    raise MissingFragmentError(f"{p.name}.{kind}: no fragments arrived")
+                frags = []
+                for meta, path, hdr in items:
+                    jobs.append((path, hdr, s_at))
+                    frags.append((meta, s_at, hdr.numel))
+                    s_at += align_up(hdr.nbytes)
+                compile_union(tab, p, cfg, frags, a_at, strict_replicate)
+                outs.append((p, kind, a_at))
+                a_at += align_up(4 * p.numel)
+        wplans.append((Program(tab, dev), jobs, s_at, outs, a_at))
+    _pipeline(wplans, dev, "conv", n_workers, True, lambda o, ov: _write_atomic(out_dir, o, ov))
 
     with open(os.path.join(out_dir, codec.MODEL_JSON), "w") as f:
         f.write(spec_to_json(spec))
@@ -543,47 +596,44 @@ def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass
 
     params = [p for _, ps in _layer_groups(spec) for p in ps]
     windows = _windows(params, lambda p: 3 * align_up(4 * p.numel) + tgt_bytes(p), window_bytes)
-    filled: dict = {}
-    st = _status(dev)
-    with _io_pool(4) as pool:
-        for wparams in windows:
-            tab = RunTable()
-            jobs, s_at, t_at, outs = [], 0, 0, []
-            for p in wparams:
-                for kind in STATE_KINDS:
-                    path = atomic.param_file(p.name, kind)
-                    hdr = codec.read_header(path)
-                    if hdr.dtype is not DType.F32:
-                        raise CheckpointLayoutError(f"{path}: expected f32, got {hdr.dtype.name}")
-                    if tuple(hdr.shape) != tuple(p.shape):
-                        raise ShapeError(f"{p.name}: expected {p.shape}, got {hdr.shape}")
-                    jobs.append((path, hdr, s_at))
-                    targets = []
-                    odt = out_dtype(kind)
-                    for g, i, m in by_unit.get((p.name, kind), ()):
-                        n = fragment_elems(p, tgt, m)
-                        targets.append((m, t_at))
-                        outs.append((g, i, m, odt, t_at, n, fragment_shape(p, tgt, m)))
-                        t_at += align_up(n * odt.itemsize)
-                    compile_extract(tab, p, tgt, targets, s_at, odt)
-                    s_at += align_up(hdr.nbytes)
-            h_src = _STAGE.host_buf("load_src", s_at)
-            hv = memoryview(h_src.numpy())
-            list(pool.map(lambda j: codec.read_payload_into(j[0], j[1], hv[j[2]:j[2] + j[1].nbytes]),
-                          jobs))
-            d_src = _STAGE.dev_buf("load_src", s_at, dev)
-            d_dst = _STAGE.dev_buf("load_dst", t_at, dev)
-            d_src[:s_at].copy_(h_src[:s_at], non_blocking=True)
-            prog = Program(tab, dev)
-            st.reset()
-            prog.launch(False, d_src.data_ptr(), d_dst.data_ptr(), st)
-            host = np.empty(max(t_at, 1), dtype=np.uint8)
-            torch.from_numpy(host)[:t_at].copy_(d_dst[:t_at])
-            torch.cuda.synchronize(dev)
-            st.raise_if_bad(prog, d_src.data_ptr())
-            for g, i, m, odt, at, n, shape in outs:
-                arr = host[at:at + n * odt.itemsize].view(odt.storage).reshape(shape)
-                filled[(g, i)] = Tensor(odt, tuple(shape), arr)
+    wplans, outs_all, total = [], [], 0
+    for wparams in windows:
+        tab = RunTable()
+        jobs, s_at, t_at, outs = [], 0, 0, []
+        for p in wparams:
+            for kind in STATE_KINDS:
+                path = atomic.param_file(p.name, kind)
+                hdr = codec.read_header(path)
+                if hdr.dtype is not DType.F32:
+                    raise CheckpointLayoutError(f"{path}: expected f32, got {hdr.dtype.name}")
+                if tuple(hdr.shape) != tuple(p.shape):
+                    raise ShapeError(f"{p.name}: expected {p.shape}, got {hdr.shape}")
+                jobs.append((path, hdr, s_at))
+                targets = []
+                odt = out_dtype(kind)
+                for g, i, m in by_unit.get((p.name, kind), ()):
+                    n = fragment_elems(p, tgt, m)
+                    targets.append((m, t_at))
+                    o = (g, i, m, odt, t_at, n, fragment_shape(p, tgt, m), total)
+                    outs.append(o)
+                    outs_all.append(o)
+                    total += align_up(n * odt.itemsize, 16)
+                    t_at += align_up(n * odt.itemsize)
+                compile_extract(tab, p, tgt, targets, s_at, odt)
+                s_at += align_up(hdr.nbytes)
+        wplans.append((Program(tab, dev), jobs, s_at, outs, t_at))
+    host = np.empty(max(total, 1), dtype=np.uint8)
+
+    def emit(o, ov):
+        _, _, _, odt, at, n, _, g_at = o
+        host[g_at:g_at + n * odt.itemsize] = np.frombuffer(ov, dtype=np.uint8, count=n * odt.itemsize,
+                                                           offset=at)
+
+    _pipeline(wplans, dev, "load", 4, False, emit)
+    filled = {}
+    for g, i, m, odt, at, n, shape, g_at in outs_all:
+        arr = host[g_at:g_at + n * odt.itemsize].view(odt.storage).reshape(shape)
+        filled[(g, i)] = Tensor(odt, tuple(shape), arr)
     shards = {g: [WorldShard(m, filled[(g, i)]) for i, m in enumerate(info.records[g])]
               for g in range(tgt.world_size)}
     return LoadedWorld(tgt, spec, atomic.step, dict(atomic.metadata), shards, stats)
@@ -705,3 +755,21 @@ def partition(state: ModelState, cfg: ParallelConfig, out_dir: str, workers: int
         codec.write_json(os.path.join(out_dir, f"rank_{g}", codec.MANIFEST),
                          codec.manifest_dict(cfg, g, recs[g]))
     return codec.DistributedCheckpoint(out_dir, cfg, spec, state.step, dict(state.metadata))
+
+
+# --------------------------------------------------------------------------- in-memory reshard
+
+
+def reshard(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: dict,
+            dtype: DType = DType.F32, strict: bool = True, *, device=None,
+            fused: bool = True) -> dict:
+    """In-memory resume(): source fragments {g: [array per record of
+    enumerate_rank_records(spec, src, g)]} -> target fragments {g: [array
+    per record of enumerate_rank_records(spec, tgt, g)]} (weights cast to
+    dtype), through pinned host staging and the fused convert+load kernel.
+    Equivalent to convert() then load() without the file system
+    (ucp/load.py:276-281); raises the same exceptions."""
+    from .reshard import ReshardPlan
+
+    plan = ReshardPlan(spec, src, tgt, dtype=dtype, strict=strict, device=device, fused=fused)
+    return plan.run_host(shards)

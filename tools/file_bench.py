@@ -1,0 +1,69 @@
+#!/usr/bin/env python
+"""File pipeline throughput of the drop-in convert()/load() on tmpfs
+(SURVEY §8f row 1). Prints one JSON line.
+
+    python tools/file_bench.py [--config cfg1] [--root /dev/shm/ucpbench] [--workers 16]
+
+The source tree is written by the product's GPU partition() (outside the
+timed region). convert() reads every rank file, reshards on the GPU and
+writes the atomic tree; load() reads the atomic tree and materialises every
+target shard in host memory. GB/s = S / t with S = 12 B x numel.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--root", default="/dev/shm/ucpbench")
+    ap.add_argument("--workers", type=int, default=os.cpu_count())
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+
+    import paper_2406_18820_b200 as U
+
+    spec, src, tgt, desc = U.bench_config(args.config, args.layers)
+    S = 12 * spec.total_numel
+    shutil.rmtree(args.root, ignore_errors=True)
+    os.makedirs(args.root)
+    src_dir = os.path.join(args.root, "src")
+    t = time.perf_counter()
+    U.partition(U.init_state(spec, 7), src, src_dir)
+    t_part = time.perf_counter() - t
+    conv, load = [], []
+    for r in range(args.reps + 1):
+        out = os.path.join(args.root, f"atomic{r}")
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        U.convert(src_dir, out, n_workers=args.workers)
+        conv.append(time.perf_counter() - t)
+        t = time.perf_counter()
+        world = U.load(out, tgt)
+        load.append(time.perf_counter() - t)
+        del world
+        shutil.rmtree(out)
+    c, lo = min(conv[1:]), min(load[1:])
+    print(json.dumps({
+        "workload": desc, "config": args.config, "state_bytes": S, "root": args.root,
+        "workers": args.workers, "partition_s": t_part,
+        "convert_s": c, "convert_GBps": S / c / 1e9, "load_s": lo, "load_GBps": S / lo / 1e9,
+        "convert_plus_load_GBps": S / (c + lo) / 1e9, "reps": args.reps,
+        "all_convert_s": conv, "all_load_s": load}))
+    shutil.rmtree(args.root, ignore_errors=True)
+
+
+if __name__ == "__main__":
+    main()
