@@ -366,7 +366,7 @@ def run_ours(args):
         parity = parity or {"note": "windowed run: parity is covered by the resident runs and "
                             "tests (state exceeds HBM)"}
     if not args.no_e2e and not windowed:
-        budget = args.e2e_gb * GB
+        budget = args.e2e_gb * GB / world  # pinned host memory is shared by all ranks
         wins, acc = [], 0
         for W in plan.windows:
             if wins and acc + W.src_bytes + W.tgt_bytes > budget:

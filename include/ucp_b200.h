@@ -176,6 +176,25 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
 int ucp_compare(const void* a, const void* b, uint64_t nbytes, unsigned long long* mismatch,
                 void* stream);
 
+/*
+ * Peer memory for the rank-homed load (north_star item 3): target fragments
+ * whose home GPU is not the param owner are written by ucp_reshard_fused /
+ * ucp_load_scatter straight into the home GPU's receive buffer through a
+ * CUDA IPC mapping (NVLink / NVSwitch stores, overlapped with the HBM work
+ * tile by tile). Buffers are cudaMalloc'ed here so the IPC handle covers the
+ * allocation exactly.
+ */
+typedef struct ucp_ipc_handle {
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} ucp_ipc_handle;
+
+int ucp_dev_alloc(uint64_t nbytes, void** ptr);
+int ucp_dev_free(void* ptr);
+int ucp_ipc_export(const void* dev_ptr, ucp_ipc_handle* out);
+/* Map a peer's buffer into this process (peer access enabled lazily). */
+int ucp_ipc_open(const ucp_ipc_handle* handle, void** mapped);
+int ucp_ipc_close(void* mapped);
+
 /* Synchronous device->host copy of n bytes (error-path diagnostics: reading
  * the replicas behind a failing run to name them in the exception). */
 int ucp_peek(const void* device_src, void* host_dst, uint64_t nbytes);

@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 # exported symbols declared in include/ucp_b200.h
 EXPORTS = ("ucp_version", "ucp_status_reset", "ucp_convert_gather", "ucp_load_scatter",
-           "ucp_reshard_fused", "ucp_gen_state", "ucp_compare", "ucp_peek")
+           "ucp_reshard_fused", "ucp_gen_state", "ucp_compare", "ucp_peek",
+           "ucp_dev_alloc", "ucp_dev_free", "ucp_ipc_export", "ucp_ipc_open", "ucp_ipc_close")
 ABI_VERSION = 1
 
 _lib = None
@@ -34,6 +35,11 @@ _SIGS = {
     "ucp_gen_state": (_c.c_int, [_c.c_uint64, _c.c_uint64, _c.c_uint64, _c.c_int, _P, _P]),
     "ucp_compare": (_c.c_int, [_P, _P, _c.c_uint64, _P, _P]),
     "ucp_peek": (_c.c_int, [_P, _P, _c.c_uint64]),
+    "ucp_dev_alloc": (_c.c_int, [_c.c_uint64, _P]),
+    "ucp_dev_free": (_c.c_int, [_P]),
+    "ucp_ipc_export": (_c.c_int, [_P, _P]),
+    "ucp_ipc_open": (_c.c_int, [_P, _P]),
+    "ucp_ipc_close": (_c.c_int, [_P]),
 }
 
 

@@ -15,6 +15,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "ucp_b200.h"
 
@@ -846,6 +847,40 @@ int ucp_compare(const void* a, const void* b, uint64_t nbytes, unsigned long lon
   compare_kernel<<<grid_for(nbytes, 256 * 16 * 4), 256, 0, s>>>(
       static_cast<const unsigned char*>(a), static_cast<const unsigned char*>(b), nbytes, mismatch);
   return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
+}
+
+int ucp_dev_alloc(uint64_t nbytes, void** ptr) {
+  if (!ptr) return UCP_EINVAL;
+  *ptr = nullptr;
+  return cudaMalloc(ptr, nbytes ? nbytes : 256) == cudaSuccess ? UCP_OK : UCP_ECUDA;
+}
+
+int ucp_dev_free(void* ptr) {
+  if (!ptr) return UCP_OK;
+  return cudaFree(ptr) == cudaSuccess ? UCP_OK : UCP_ECUDA;
+}
+
+int ucp_ipc_export(const void* dev_ptr, ucp_ipc_handle* out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(ucp_ipc_handle), "ipc handle size");
+  if (!dev_ptr || !out) return UCP_EINVAL;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)) != cudaSuccess) return UCP_ECUDA;
+  memcpy(out->bytes, &h, sizeof(h));
+  return UCP_OK;
+}
+
+int ucp_ipc_open(const ucp_ipc_handle* handle, void** mapped) {
+  if (!handle || !mapped) return UCP_EINVAL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle->bytes, sizeof(h));
+  *mapped = nullptr;
+  return cudaIpcOpenMemHandle(mapped, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess
+             ? UCP_OK : UCP_ECUDA;
+}
+
+int ucp_ipc_close(void* mapped) {
+  if (!mapped) return UCP_OK;
+  return cudaIpcCloseMemHandle(mapped) == cudaSuccess ? UCP_OK : UCP_ECUDA;
 }
 
 int ucp_peek(const void* device_src, void* host_dst, uint64_t nbytes) {
