@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--home", default="param", choices=["param", "rank"],
                     help="param: targets stay on the param-owner GPU (no collective); rank: "
                          "target rank g is homed on GPU g mod N, one NCCL all-to-all-v per window")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="rank-homed transport: peer = the reshard kernel stores into the home "
+                         "GPU's CUDA-IPC-mapped buffer over NVLink; nccl = all-to-all-v per window")
     ap.add_argument("--unfused", action="store_true",
                     help="separate convert and load launches (atomic re-read from HBM)")
     ap.add_argument("--cpu-threads", type=int, default=os.cpu_count())
@@ -245,16 +248,20 @@ def run_ours(args):
     spec, src, tgt, desc = bench_config(args.config, args.layers)
     mine = owned_params(spec, rank, world) if world > 1 else None
     homed = args.home == "rank"
+    exch = peer = None
+    if homed:
+        from paper_2406_18820_b200.dist import PeerBuffers, build_exchange
+        from paper_2406_18820_b200.spec import DType as _DT
+
+        exch = build_exchange(spec, src, tgt, world, rank, int(args.window_gb * GB), _DT.F32)
+        if args.exchange == "peer":
+            peer = PeerBuffers(exch.max_recv, n_slots=2)
     plan = ReshardPlan(spec, src, tgt, params=mine, device=dev,
                        window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024,
                        fused=not args.unfused,
                        home_of=[g % world for g in range(tgt.world_size)] if homed else None,
-                       n_homes=world if homed else 1)
-    exch = None
-    if homed:
-        from paper_2406_18820_b200.dist import build_exchange
-
-        exch = build_exchange(spec, src, tgt, world, rank, int(args.window_gb * GB), plan.dtype)
+                       n_homes=world if homed else 1,
+                       peer=(exch, peer) if peer is not None else None)
     S_local = plan.state_bytes
     free, _ = torch.cuda.mem_get_info(dev)
     need = plan.src_total + plan.max_atom * 3 + plan.max_tgt * 2 + (2 << 30)
@@ -277,7 +284,7 @@ def run_ours(args):
     if homed and windowed:
         raise SystemExit("--home rank needs the source arena resident (use more GPUs)")
     comm_stream = torch.cuda.Stream(dev) if homed else None
-    if homed:
+    if homed and peer is None:
         step = lambda ev=None: plan.step_device_homed(exch, None, stream, comm_stream, ev)
     elif windowed:
         step = lambda ev=None: plan.step_windowed(7, stream, ev)
@@ -290,7 +297,7 @@ def run_ours(args):
         plan.check()
 
     nW = len(plan.windows)
-    nEv = exch.n_windows if exch else nW
+    nEv = exch.n_windows if (exch and peer is None) else nW
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nEv)]
            for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -365,7 +372,7 @@ def run_ours(args):
     if windowed:
         parity = parity or {"note": "windowed run: parity is covered by the resident runs and "
                             "tests (state exceeds HBM)"}
-    if not args.no_e2e and not windowed:
+    if not args.no_e2e and not windowed and peer is None:
         budget = args.e2e_gb * GB / world  # pinned host memory is shared by all ranks
         wins, acc = [], 0
         for W in plan.windows:
@@ -455,8 +462,10 @@ def run_ours(args):
                          + plan.bytes["R_l"] + plan.bytes["W_l"] + plan.fused_bytes["W_tgt"]),
                      "windows": nW,
                      "parallelism": f"param-sharded x{world}" + (
-                         ", rank-homed targets: one NCCL all-to-all-v per window "
-                         f"({sum(sum(nb for _, nb in exch.send[w]) - exch.send[w][rank][1] for w in range(exch.n_windows)) / GB:.2f} GB sent/step by rank 0)"
+                         (", rank-homed targets: kernel stores into peer GPUs' IPC-mapped buffers "
+                          if peer is not None else
+                          ", rank-homed targets: one NCCL all-to-all-v per window ") +
+                         f"({sum(sum(nb for _, nb in exch.send[w]) - exch.send[w][rank][1] for w in range(exch.n_windows)) / GB:.2f} GB crosses GPUs/step from rank 0)"
                          if homed else ", param-homed targets (no collective)"), "l2": "inputs larger than L2 "
                      f"({plan.src_total / GB:.1f} GB source arena per rank)",
                      "residency": ("windowed: sources synthesised per window outside the timed "
@@ -465,6 +474,10 @@ def run_ours(args):
                      "strict_replicate": True},
           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
           "gpu_launches": gpu_launches, "parity": parity}, rank)
+    if peer is not None:
+        if world > 1:
+            dist.barrier()
+        peer.close()
     if dist.is_initialized():
         dist.destroy_process_group()
 

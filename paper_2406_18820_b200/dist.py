@@ -110,9 +110,16 @@ class ExchangePlan:
     send: list
     recv: list
     index: dict
+    all_index: dict = None
+    max_recv: int = 0   # largest window receive buffer over all homes (same on every rank)
 
     def recv_bytes(self, w: int) -> int:
         return sum(self.recv[w])
+
+    def index_of(self, g: int, i: int) -> tuple:
+        """(window, offset in the home GPU's window receive buffer) of target
+        record i of rank g, for ANY home (not only this rank)."""
+        return self.all_index[(g, i)]
 
 
 def build_exchange(spec: ModelSpec, src, tgt, world: int, rank: int, window_bytes: int,
@@ -131,7 +138,23 @@ def build_exchange(spec: ModelSpec, src, tgt, world: int, rank: int, window_byte
         layout_windows(spec, src, tgt, wins, dtype, home_of, world)
         layouts.append(wins)
     n_w = max(len(w) for w in layouts)
-    send, recv, index = [], [], {}
+    send, recv, index, all_index = [], [], {}, {}
+    max_recv = 0
+    # receive-buffer offsets at every home: senders in rank order, each
+    # sender's chunk in its own layout order
+    for w in range(n_w):
+        for h in range(world):
+            at = 0
+            for s in range(world):
+                W = layouts[s][w] if w < len(layouts[s]) else None
+                if W is None:
+                    continue
+                off, nb = W.tgt_chunks[h]
+                for g, i, m, o, n, dt in W.tgt_frags:
+                    if home_of[g] == h:
+                        all_index[(g, i)] = (w, at + (o - off))
+                at += nb
+            max_recv = max(max_recv, at)
     for w in range(n_w):
         mine = layouts[rank][w] if w < len(layouts[rank]) else None
         send.append([tuple(mine.tgt_chunks[h]) if mine else (0, 0) for h in range(world)])
@@ -146,4 +169,81 @@ def build_exchange(spec: ModelSpec, src, tgt, world: int, rank: int, window_byte
                         index[(g, i)] = (w, at + (o - off))
             at += nb
         recv.append(row)
-    return ExchangePlan(rank, world, n_w, send, recv, index)
+    return ExchangePlan(rank, world, n_w, send, recv, index, all_index, max_recv)
+
+
+class PeerBuffers:
+    """Receive buffers of every rank, mapped into this process with CUDA IPC
+    so the reshard kernels store rank-homed target fragments straight into
+    the home GPU's memory (NVLink / NVSwitch peer stores; no separate
+    collective). ``n_slots`` ring slots of ``slot_bytes`` each; window w uses
+    slot w % n_slots. Handles are exchanged once with all_gather_object over
+    the default process group (gloo or NCCL)."""
+
+    def __init__(self, slot_bytes: int, n_slots: int = 2, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _native
+        from ._errors import from_status
+
+        lib = _native.lib()
+        self.slot_bytes = max(int(slot_bytes), 256)
+        self.n_slots = n_slots
+        ptr = ctypes.c_void_p()
+        rc = lib.ucp_dev_alloc(self.slot_bytes * n_slots, ctypes.byref(ptr))
+        if rc:
+            raise from_status(rc, "ucp_dev_alloc")
+        self.local = ptr.value
+        handle = (ctypes.c_ubyte * 64)()
+        rc = lib.ucp_ipc_export(ctypes.c_void_p(self.local), handle)
+        if rc:
+            raise from_status(rc, "ucp_ipc_export")
+        self.rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.bases, self._mapped = [], []
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                self.bases.append(self.local)
+                continue
+            m = ctypes.c_void_p()
+            h = (ctypes.c_ubyte * 64).from_buffer_copy(hb)
+            rc = lib.ucp_ipc_open(h, ctypes.byref(m))
+            if rc:
+                raise from_status(rc, f"ucp_ipc_open(rank {r})")
+            self.bases.append(m.value)
+            self._mapped.append(m.value)
+
+    def slot(self, home: int, w: int) -> int:
+        """Device address (valid in this process) of home GPU's slot for window w."""
+        return self.bases[home] + (w % self.n_slots) * self.slot_bytes
+
+    def read_local(self, w: int, offset: int, nbytes: int):
+        """Synchronous copy of this rank's received bytes (tests / checks)."""
+        import ctypes
+
+        import numpy as np
+
+        from . import _native
+
+        out = np.empty(nbytes, dtype=np.uint8)
+        if nbytes:
+            _native.lib().ucp_peek(ctypes.c_void_p(self.slot(self.rank, w) + offset),
+                                   out.ctypes.data, nbytes)
+        return out
+
+    def close(self) -> None:
+        import ctypes
+
+        from . import _native
+
+        lib = _native.lib()
+        for m in self._mapped:
+            lib.ucp_ipc_close(ctypes.c_void_p(m))
+        self._mapped = []
+        if self.local:
+            lib.ucp_dev_free(ctypes.c_void_p(self.local))
+            self.local = 0

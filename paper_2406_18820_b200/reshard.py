@@ -134,12 +134,16 @@ class ReshardPlan:
     def __init__(self, spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig,
                  dtype: DType = DType.F32, strict: bool = True, params=None, device=None,
                  window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17, fused: bool = False,
-                 materialize_atomic: bool = True, home_of=None, n_homes: int = 1):
+                 materialize_atomic: bool = True, home_of=None, n_homes: int = 1,
+                 peer=None):
         validate_model_config(spec, src)
         validate_model_config(spec, tgt)
         self.spec, self.src, self.tgt, self.dtype, self.strict = spec, src, tgt, dtype, strict
         self.fused_mode, self.materialize = fused, materialize_atomic
         self.home_of, self.n_homes = home_of, n_homes
+        # peer = (ExchangePlan, PeerBuffers): target fragments are written
+        # straight into their home GPU's receive slot (absolute addresses)
+        self.peer = peer
         self.device = require_device(device)
         self.tile_bytes = tile_bytes
         names = None if params is None else set(params)
@@ -174,6 +178,10 @@ class ReshardPlan:
             for g, i, m, off, n in W.src_frags:
                 src_by_unit.setdefault((m.param, m.kind), []).append((m, off, n))
             for g, i, m, off, n, dt in W.tgt_frags:
+                if self.peer is not None:
+                    exch, bufs = self.peer
+                    w_idx, roff = exch.index_of(g, i)
+                    off = bufs.slot(g % exch.world, w_idx) + roff
                 tgt_by_unit.setdefault((m.param, m.kind), []).append((m, off))
             for p in W.params:
                 for k in STATE_KINDS:
@@ -267,13 +275,14 @@ class ReshardPlan:
             src_ptr = arena.data_ptr() + W.src_base
             if ev:
                 ev[0].record(stream)
-            W.fused.launch(src_ptr, atom.data_ptr(), ring[i % 2].data_ptr(), self.status, stream)
+            tgt_ptr = 0 if self.peer is not None else ring[i % 2].data_ptr()
+            W.fused.launch(src_ptr, atom.data_ptr(), tgt_ptr, self.status, stream)
             if ev:
                 ev[1].record(stream)
             W.conv.launch(True, src_ptr, atom.data_ptr(), self.status, stream)
             if ev:
                 ev[2].record(stream)
-            W.load.launch(False, atom.data_ptr(), ring[i % 2].data_ptr(), self.status, stream)
+            W.load.launch(False, atom.data_ptr(), tgt_ptr, self.status, stream)
             if ev:
                 ev[3].record(stream)
 
@@ -497,13 +506,14 @@ class ReshardPlan:
         tgt = self.buf("tgt0", self.max_tgt)
         mism = torch.zeros(1, dtype=torch.int64, device=self.device)
         atomic_ok = True if (self.materialize or not self.fused_mode) else None
-        target_ok = True if self.dtype is DType.F32 else None
+        target_ok = True if self.dtype is DType.F32 and self.peer is None else None
         for W in self.windows:
             self.status.reset()
             src_ptr = arena.data_ptr() + W.src_base
-            W.fused.launch(src_ptr, atom.data_ptr(), tgt.data_ptr(), self.status)
+            tgt_ptr = 0 if self.peer is not None else tgt.data_ptr()
+            W.fused.launch(src_ptr, atom.data_ptr(), tgt_ptr, self.status)
             W.conv.launch(True, src_ptr, atom.data_ptr(), self.status)
-            W.load.launch(False, atom.data_ptr(), tgt.data_ptr(), self.status)
+            W.load.launch(False, atom.data_ptr(), tgt_ptr, self.status)
             self.gen_atomic(W, ref, seed)
             torch.cuda.synchronize(self.device)
             self.check()

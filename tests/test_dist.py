@@ -142,6 +142,8 @@ def _exchange_worker(rank, world, port, q):
             recv = alltoallv(sendt, send_sizes, ex.recv[w])
             got[w] = recv.numpy()
         ok = 0
+        assert all(ex.all_index[k] == v for k, v in ex.index.items())
+        assert ex.max_recv >= max(ex.recv_bytes(w) for w in range(ex.n_windows))
         for (g, i), (w, off) in ex.index.items():
             m = recs[g][i]
             a = O.extract(spec.param(m.param), tgt, m, state[m.param][m.kind])
