@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--tile-kb", type=int, default=128)
     ap.add_argument("--e2e-gb", type=float, default=24.0, help="pinned host budget of the e2e sample")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-window-gb", type=float, default=0.4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -158,15 +159,19 @@ def cpu_reshard(spec, src, tgt, frags: dict, threads: int) -> float:
 
 
 def sample_params(spec, budget_state_bytes: float) -> list:
-    """First transformer layer(s) of the spec as the bounded CPU sample."""
-    names, acc = [], 0
+    """Whole transformer layers from layer 0 while they fit the budget (at
+    least one layer): the bounded CPU sample."""
+    by_layer = {}
     for p in spec.params:
         if p.name.startswith("layers."):
-            layer = int(p.name.split(".")[1])
-            if acc and (layer > 0 and acc + 12 * p.numel > budget_state_bytes):
-                break
-            names.append(p.name)
-            acc += 12 * p.numel
+            by_layer.setdefault(int(p.name.split(".")[1]), []).append(p)
+    names, acc = [], 0
+    for layer in sorted(by_layer):
+        size = sum(12 * p.numel for p in by_layer[layer])
+        if names and acc + size > budget_state_bytes:
+            break
+        names += [p.name for p in by_layer[layer]]
+        acc += size
     return names
 
 
@@ -380,47 +385,53 @@ def run_ours(args):
                 break
             wins.append(W)
             acc += W.src_bytes + W.tgt_bytes
+        names = [p.name for W in wins for p in W.params]
+        # the e2e path gets its own plan with small windows so PCIe in, HBM
+        # work and PCIe out overlap with little pipeline fill / drain
+        eplan = ReshardPlan(spec, src, tgt, params=names, device=dev,
+                            window_bytes=int(args.e2e_window_gb * GB),
+                            tile_bytes=args.tile_kb * 1024, fused=not args.unfused)
         arena = plan._bufs["src_arena"]
-        s_lo, s_hi = wins[0].src_base, wins[-1].src_base + wins[-1].src_bytes
-        t_lo, t_hi = wins[0].tgt_base, wins[-1].tgt_base + wins[-1].tgt_bytes
-        host_src = torch.empty(s_hi - s_lo, dtype=torch.uint8, pin_memory=True)
-        host_tgt = torch.empty(t_hi - t_lo, dtype=torch.uint8, pin_memory=True)
-        host_src.copy_(arena[s_lo:s_hi])
+        where = {(g, i): W.src_base + off for W in wins for g, i, m, off, n in W.src_frags}
+        host_src = torch.empty(max(eplan.src_total, 256), dtype=torch.uint8, pin_memory=True)
+        host_tgt = torch.empty(max(eplan.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
+        for W in eplan.windows:
+            for g, i, m, off, n in W.src_frags:
+                a = where[(g, i)]
+                host_src[W.src_base + off:W.src_base + off + 4 * n].copy_(arena[a:a + 4 * n])
         if rank == 0 and world == 1 and not args.no_cpu:
             cpu_names = [p.name for p in wins[-1].params]
             hv = host_src.numpy()
             host_cpu_frags = {}
-            for g, i, m, off, n in wins[-1].src_frags:
-                at = wins[-1].src_base - s_lo + off
-                a = hv[at:at + 4 * n].view("<f4").copy().reshape(m.shape)
-                host_cpu_frags.setdefault((m.param, m.kind), []).append((m, a))
+            for W in eplan.windows:
+                for g, i, m, off, n in W.src_frags:
+                    if m.param in cpu_names:
+                        at = W.src_base + off
+                        a = hv[at:at + 4 * n].view("<f4").copy().reshape(m.shape)
+                        host_cpu_frags.setdefault((m.param, m.kind), []).append((m, a))
         for key in ("src_arena", "tgt0", "tgt1"):
             plan._bufs.pop(key, None)
         torch.cuda.empty_cache()
-        # stream_host indexes the host arenas by window base; shift views
-        import types
-
-        shifted = [types.SimpleNamespace(**{**W.__dict__, "src_base": W.src_base - s_lo,
-                                            "tgt_base": W.tgt_base - t_lo}) for W in wins]
         streams = tuple(torch.cuda.Stream(dev) for _ in range(3))
-        plan.status.reset()
-        plan.stream_host(host_src, host_tgt, shifted, streams)
+        eplan.status.reset()
+        eplan.stream_host(host_src, host_tgt, None, streams)
         torch.cuda.synchronize()
+        eplan._check_windows(host_src)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        for s in streams:
-            s.wait_stream(stream)
+        for s_ in streams:
+            s_.wait_stream(stream)
         for _ in range(args.e2e_steps):
-            plan.stream_host(host_src, host_tgt, shifted, streams)
-        for s in streams:
-            stream.wait_stream(s)
+            eplan.stream_host(host_src, host_tgt, None, streams)
+        for s_ in streams:
+            stream.wait_stream(s_)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-        S_e2e = sum(12 * p.numel for W in wins for p in W.params)
+        S_e2e = eplan.state_bytes
         if world > 1:
             t = torch.tensor([e2e_ms, float(S_e2e)], device=dev, dtype=torch.float64)
             mx = t.clone()
@@ -428,10 +439,13 @@ def run_ours(args):
             dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
             e2e_ms, S_e2e = float(mx[0]), float(t[1])
         e2e = {"value": S_e2e / (e2e_ms / 1e3) / GB, "unit": "GB/s",
-               "h2d_bytes_per_step": int(s_hi - s_lo), "d2h_bytes_per_step": int(t_hi - t_lo),
+               "h2d_bytes_per_step": int(eplan.src_total), "d2h_bytes_per_step": int(eplan.tgt_total),
                "ms_per_step": e2e_ms, "state_bytes_per_step": int(S_e2e),
-               "sample": f"windows 0..{len(wins) - 1} of {nW} ({S_e2e / GB:.2f} GB state/rank) "
-                         "from pinned host memory, H2D + convert + load + D2H, double-buffered"}
+               "sample": f"{len(names)} params ({names[0]} .. {names[-1]}; "
+                         f"{S_e2e / GB:.2f} GB state/rank) from pinned host memory: H2D + fused "
+                         f"reshard + D2H in {len(eplan.windows)} double-buffered windows on "
+                         "3 streams"}
+        del eplan
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

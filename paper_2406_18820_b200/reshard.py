@@ -421,6 +421,11 @@ class ReshardPlan:
         dsrc = [self.buf("ssrc0", self.max_src), self.buf("ssrc1", self.max_src)]
         dtgt = [self.buf("stgt0", self.max_tgt), self.buf("stgt1", self.max_tgt)]
         atom = self.buf("atom", self.max_atom)
+        # buffers are reused across calls: the first H2D must not overwrite a
+        # source slot still being read, the first kernel must not overwrite a
+        # target slot still being copied out
+        s_in.wait_stream(s_cmp)
+        s_cmp.wait_stream(s_out)
         ev_in = [torch.cuda.Event() for _ in wins]
         ev_cmp = [torch.cuda.Event() for _ in wins]
         ev_out = [torch.cuda.Event() for _ in wins]

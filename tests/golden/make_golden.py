@@ -208,6 +208,29 @@ def main() -> None:
             open(os.path.join(root, "rank_0", "shards.json"), "rb").read()).hexdigest()
     out["pipelines"] = pipes
 
+    # --- the reference's own verification grid (ucp/verify.py:301-357): 117
+    # identity cells (39 configs x 3 stock models) + 21 cross-config cells
+    from ucp.verify import resume_pairs, roundtrip_configs, stock_models
+
+    grid = []
+    with tempfile.TemporaryDirectory() as tmp:
+        cells = [(fam, c, c) for fam, _ in stock_models() for c in roundtrip_configs()]
+        cells += [(fam, a, b) for fam, _ in stock_models() for a, b in resume_pairs()]
+        for k, (fam, a, b) in enumerate(cells):
+            spec = specs[fam]
+            state = ucp.init_state(spec, 11)
+            src = os.path.join(tmp, f"s{k}")
+            atom = os.path.join(tmp, f"a{k}")
+            ucp.partition(state, a, src)
+            ucp.convert(src, atom)
+            row = {"model": fam, "src": cfg_key(a), "tgt": cfg_key(b),
+                   "src_digest": dir_digest(src), "atomic_digest": dir_digest(atom)}
+            for dt in (DType.F32, DType.BF16):
+                row[f"world_{dt.name}"] = world_digest(ucp.load(atom, b, dtype=dt))
+            grid.append(row)
+    out["grid"] = grid
+    print("grid cells", len(grid))
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
         f.write("\n")

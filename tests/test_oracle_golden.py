@@ -159,3 +159,34 @@ def test_union_unit_cases():
         O.union(p, cfg, [(rec(p, "shard_v", (0, 0, 1), (2,), (2, 4), 1), np.float32([3, -0.0])),
                          (rec(p, "shard_v", (0, 0, 0), (2,), (0, 2)), np.float32([1, 2]))])
     assert ei.value.name == "PaddingError"
+
+
+def _grid_cells(golden):
+    from helpers import SCALES
+    from paper_2406_18820_b200.zoo import make_model
+
+    specs = {f: make_model(f, sc) for f, sc in SCALES.items()}
+    for row in golden["grid"]:
+        yield row, specs[row["model"]], parse_config_string(row["src"]), parse_config_string(row["tgt"])
+
+
+@pytest.mark.parametrize("chunk", range(6))
+def test_reference_verify_grid(golden, tmp_path, chunk):
+    # the reference's own acceptance grid (ucp/verify.py:301-357): 117 identity
+    # cells + 21 cross-config cells, seed 11
+    cells = list(_grid_cells(golden))
+    assert len(cells) == 138
+    for k, (row, spec, a, b) in enumerate(cells):
+        if k % 6 != chunk:
+            continue
+        state = O.init_state(spec, 11)
+        shards = O.partition_mem(spec, state, a)
+        src = str(tmp_path / f"s{k}")
+        O.write_tree(spec, a, shards, src)
+        assert O.dir_digest(src) == row["src_digest"], (row["model"], row["src"])
+        atomic = O.convert_mem(spec, a, shards)
+        for p in spec.params:
+            for kind in ("weight", "m", "v"):
+                assert np.array_equal(atomic[p.name][kind], state[p.name][kind])
+        for dt in ("F32", "BF16"):
+            assert O.world_digest(O.load_mem(spec, atomic, b, dt)) == row[f"world_{dt}"]
