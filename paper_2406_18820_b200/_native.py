@@ -14,7 +14,8 @@ import os
 from ._errors import NativeUnavailableError
 
 LIB_NAME = "libucp_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("UCP_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)  # env override: kernel A/B experiments
 
 # exported symbols declared in include/ucp_b200.h
 EXPORTS = ("ucp_version", "ucp_status_reset", "ucp_convert_gather", "ucp_load_scatter",

@@ -33,11 +33,25 @@ constexpr int kMaxAux = 256;             // host splits runs beyond this
 
 // ---------------------------------------------------------------- memory ops
 
+#ifndef UCP_L2_PREFETCH
+#define UCP_L2_PREFETCH 0  // 0, 128 or 256: L2 sector prefetch hint on streaming loads
+#endif
+
 __device__ __forceinline__ float4 ld_stream4(const void* p) {
   float4 r;
+#if UCP_L2_PREFETCH == 256
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p));
+#elif UCP_L2_PREFETCH == 128
+  asm("ld.global.nc.L1::no_allocate.L2::128B.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p));
+#else
   asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
       : "l"(p));
+#endif
   return r;
 }
 
