@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="rank-homed transport: peer = the reshard kernel stores into the home "
                          "GPU's CUDA-IPC-mapped buffer over NVLink; nccl = all-to-all-v per window")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to smoke-test the multi-rank logic with >1 rank per GPU")
     ap.add_argument("--unfused", action="store_true",
                     help="separate convert and load launches (atomic re-read from HBM)")
     ap.add_argument("--cpu-threads", type=int, default=os.cpu_count())
@@ -245,9 +247,11 @@ def run_ours(args):
     from paper_2406_18820_b200.dist import init_process_group, owned_params
     from paper_2406_18820_b200.reshard import ReshardPlan
 
-    rank, world, local = init_process_group("nccl", force=args.home == "rank")
+    rank, world, local = init_process_group(args.dist_backend, force=args.home == "rank")
+    local = local % torch.cuda.device_count()  # >1 rank per GPU only for gloo smoke tests
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
     import torch.distributed as dist
 
     spec, src, tgt, desc = bench_config(args.config, args.layers)
@@ -332,7 +336,7 @@ def run_ours(args):
     conv_bytes = plan.bytes["R_c"] + plan.bytes["W_c"]
     load_bytes = plan.bytes["R_l"] + plan.bytes["W_l"]
     if world > 1:
-        t = torch.tensor([ms_local, float(S_local)], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms_local, float(S_local)], device=red_dev, dtype=torch.float64)
         mx = t.clone()
         dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
@@ -433,7 +437,7 @@ def run_ours(args):
         e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
         S_e2e = eplan.state_bytes
         if world > 1:
-            t = torch.tensor([e2e_ms, float(S_e2e)], device=dev, dtype=torch.float64)
+            t = torch.tensor([e2e_ms, float(S_e2e)], device=red_dev, dtype=torch.float64)
             mx = t.clone()
             dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
             dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
