@@ -435,7 +435,7 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-        S_e2e = eplan.state_bytes
+        S_e2e = S_e2e_local = eplan.state_bytes
         if world > 1:
             t = torch.tensor([e2e_ms, float(S_e2e)], device=red_dev, dtype=torch.float64)
             mx = t.clone()
@@ -446,7 +446,7 @@ def run_ours(args):
                "h2d_bytes_per_step": int(eplan.src_total), "d2h_bytes_per_step": int(eplan.tgt_total),
                "ms_per_step": e2e_ms, "state_bytes_per_step": int(S_e2e),
                "sample": f"{len(names)} params ({names[0]} .. {names[-1]}; "
-                         f"{S_e2e / GB:.2f} GB state/rank) from pinned host memory: H2D + fused "
+                         f"{S_e2e_local / GB:.2f} GB state/rank) from pinned host memory: H2D + fused "
                          f"reshard + D2H in {len(eplan.windows)} double-buffered windows on "
                          "3 streams"}
         del eplan
