@@ -60,9 +60,11 @@ def parse():
     ap.add_argument("--home", default="param", choices=["param", "rank"],
                     help="param: targets stay on the param-owner GPU (no collective); rank: "
                          "target rank g is homed on GPU g mod N, one NCCL all-to-all-v per window")
-    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl", "torch"],
                     help="rank-homed transport: peer = the reshard kernel stores into the home "
-                         "GPU's CUDA-IPC-mapped buffer over NVLink; nccl = all-to-all-v per window")
+                         "GPU's CUDA-IPC-mapped buffer over NVLink; nccl = all-to-all-v per "
+                         "window through libucp_b200_comm.so; torch = the same through "
+                         "torch.distributed")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to smoke-test the multi-rank logic with >1 rank per GPU")
     ap.add_argument("--unfused", action="store_true",
@@ -293,8 +295,13 @@ def run_ours(args):
     if homed and windowed:
         raise SystemExit("--home rank needs the source arena resident (use more GPUs)")
     comm_stream = torch.cuda.Stream(dev) if homed else None
+    ncomm = None
+    if homed and args.exchange == "nccl":
+        from paper_2406_18820_b200.dist import NcclComm
+
+        ncomm = NcclComm()
     if homed and peer is None:
-        step = lambda ev=None: plan.step_device_homed(exch, None, stream, comm_stream, ev)
+        step = lambda ev=None: plan.step_device_homed(exch, None, stream, comm_stream, ev, ncomm)
     elif windowed:
         step = lambda ev=None: plan.step_windowed(7, stream, ev)
     else:
@@ -482,7 +489,7 @@ def run_ours(args):
                      "parallelism": f"param-sharded x{world}" + (
                          (", rank-homed targets: kernel stores into peer GPUs' IPC-mapped buffers "
                           if peer is not None else
-                          ", rank-homed targets: one NCCL all-to-all-v per window ") +
+                          f", rank-homed targets: one NCCL all-to-all-v per window ({args.exchange}) ") +
                          f"({sum(sum(nb for _, nb in exch.send[w]) - exch.send[w][rank][1] for w in range(exch.n_windows)) / GB:.2f} GB crosses GPUs/step from rank 0)"
                          if homed else ", param-homed targets (no collective)"), "l2": "inputs larger than L2 "
                      f"({plan.src_total / GB:.1f} GB source arena per rank)",
@@ -496,6 +503,8 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         peer.close()
+    if ncomm is not None:
+        ncomm.close()
     if dist.is_initialized():
         dist.destroy_process_group()
 

@@ -171,6 +171,20 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
                       const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
                       void* atom_base, void* dst_base, ucp_status* status, void* stream);
 
+/*
+ * One bias-corrected Adam step of the reference's toy trainer, in place,
+ * bit-exact with ucp/models.py:265-293 (f64 elementwise, fixed operation
+ * order, RNE to f32): g = hash_unit(grad_base, start + i) (ucp/models.py:247-253),
+ *   m' = b1*m + (1-b1)*g ; v' = b2*v + ((1-b2)*g)*g
+ *   w' = w - (lr*(m'/bc1)) / (sqrt(v'/bc2) + eps)
+ * bc1/bc2 and 1-b1/1-b2 are computed by the caller exactly as the
+ * reference does (plain repeated multiplication, _pow_seq).
+ */
+int ucp_adam_step(float* w, float* m, float* v, uint64_t count, uint64_t grad_base,
+                  uint64_t start, double b1, double one_minus_b1, double b2,
+                  double one_minus_b2, double bc1, double bc2, double lr, double eps,
+                  void* stream);
+
 /* Byte-compare two device buffers; *mismatch (device) receives the first
  * differing byte index or ~0. Used by the checker paths of the bench. */
 int ucp_compare(const void* a, const void* b, uint64_t nbytes, unsigned long long* mismatch,

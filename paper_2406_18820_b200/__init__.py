@@ -75,6 +75,7 @@ from .spec import (
     spec_from_dict,
     spec_to_dict,
 )
+from .trainer import TrainerConfig, first_diff, states_equal, train_steps
 from .zoo import FAMILIES, bench_config, llama_spec, make_model
 
 __version__ = "0.1.0"

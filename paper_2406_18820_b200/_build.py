@@ -17,6 +17,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "ucp_b200.cu")
 OUT = os.path.join(HERE, "libucp_b200.so")
+COMM_SRC = os.path.join(HERE, "csrc", "ucp_comm.cpp")
+COMM_OUT = os.path.join(HERE, "libucp_b200_comm.so")
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC,-O2", "-ftz=false",
               "-prec-div=true", "-prec-sqrt=true", "-fmad=false"]
@@ -29,10 +32,33 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def _fresh(out: str, srcs: list) -> bool:
+    return os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(s) for s in srcs)
+
+
+def build_comm(verbose: bool = False) -> str:
+    """libucp_b200_comm.so: host-only NCCL wrapper (links libnccl.so.2 by
+    soname, so a process that already loaded torch's NCCL reuses it)."""
+    srcs = [COMM_SRC, os.path.join(ROOT, "include", "ucp_b200_comm.h")]
+    if _fresh(COMM_OUT, srcs):
+        return COMM_OUT
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", os.path.join(ROOT, "include"),
+           "-I", os.path.join(CUDA_HOME, "include"), COMM_SRC, "-o", COMM_OUT + ".tmp",
+           "-L", os.path.join(CUDA_HOME, "lib64"), "-lnccl", "-lcudart"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or res.returncode:
+        sys.stderr.write(res.stdout + res.stderr)
+    if res.returncode:
+        raise RuntimeError(f"g++ failed ({res.returncode}): {' '.join(cmd)}")
+    os.replace(COMM_OUT + ".tmp", COMM_OUT)
+    return COMM_OUT
+
+
 def build(verbose: bool = False) -> str:
-    """Compile if the .so is missing or older than its sources."""
+    """Compile if a .so is missing or older than its sources."""
+    build_comm(verbose)
     srcs = [SRC, os.path.join(ROOT, "include", "ucp_b200.h")]
-    if os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(s) for s in srcs):
+    if _fresh(OUT, srcs):
         return OUT
     cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), SRC, "-o", OUT + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("UCP_B200_LIB") or os.path.join(
 
 # exported symbols declared in include/ucp_b200.h
 EXPORTS = ("ucp_version", "ucp_status_reset", "ucp_convert_gather", "ucp_load_scatter",
-           "ucp_reshard_fused", "ucp_gen_state", "ucp_compare", "ucp_peek",
+           "ucp_reshard_fused", "ucp_gen_state", "ucp_adam_step", "ucp_compare", "ucp_peek",
            "ucp_dev_alloc", "ucp_dev_free", "ucp_ipc_export", "ucp_ipc_open", "ucp_ipc_close")
 ABI_VERSION = 1
 
@@ -33,6 +33,8 @@ _SIGS = {
     "ucp_convert_gather": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "ucp_load_scatter": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "ucp_reshard_fused": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ucp_adam_step": (_c.c_int, [_P, _P, _P, _c.c_uint64, _c.c_uint64, _c.c_uint64] +
+                      [_c.c_double] * 8 + [_P]),
     "ucp_gen_state": (_c.c_int, [_c.c_uint64, _c.c_uint64, _c.c_uint64, _c.c_int, _P, _P]),
     "ucp_compare": (_c.c_int, [_P, _P, _c.c_uint64, _P, _P]),
     "ucp_peek": (_c.c_int, [_P, _P, _c.c_uint64]),
@@ -66,3 +68,33 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
 
 def lib() -> ctypes.CDLL:
     return load_library()
+
+
+# --------------------------------------------------------------------------- comm library
+
+COMM_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libucp_b200_comm.so")
+COMM_EXPORTS = ("ucp_comm_version", "ucp_comm_unique_id", "ucp_comm_init", "ucp_alltoallv",
+                "ucp_comm_destroy")
+_comm = None
+_COMM_SIGS = {
+    "ucp_comm_version": (_c.c_int, []),
+    "ucp_comm_unique_id": (_c.c_int, [_P]),
+    "ucp_comm_init": (_c.c_int, [_c.c_int, _c.c_int, _P, _P]),
+    "ucp_alltoallv": (_c.c_int, [_P, _P, _P, _P, _P, _P]),
+    "ucp_comm_destroy": (_c.c_int, [_P]),
+}
+
+
+def comm_lib() -> ctypes.CDLL:
+    """libucp_b200_comm.so (NCCL all-to-all-v of the rank-homed exchange)."""
+    global _comm
+    if _comm is None:
+        if not os.path.exists(COMM_PATH):
+            raise NativeUnavailableError(f"{COMM_PATH} is missing; run __graft_entry__.build()")
+        lib = ctypes.CDLL(COMM_PATH)
+        for name, (res, args) in _COMM_SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _comm = lib
+    return _comm

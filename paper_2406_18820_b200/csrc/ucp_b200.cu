@@ -716,6 +716,28 @@ gen_state_kernel(uint64_t base, uint64_t start, uint64_t count, int abs_flag, fl
   }
 }
 
+struct AdamArgs {
+  double b1, omb1, b2, omb2, bc1, bc2, lr, eps;
+};
+
+__global__ void __launch_bounds__(256)
+adam_step_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
+                 uint64_t count, uint64_t base, uint64_t start, AdamArgs a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const double g = (double)gen1(base + start + i);
+    const double m64 = __dadd_rn(__dmul_rn(a.b1, (double)m[i]), __dmul_rn(a.omb1, g));
+    const double v64 = __dadd_rn(__dmul_rn(a.b2, (double)v[i]), __dmul_rn(__dmul_rn(a.omb2, g), g));
+    const double mhat = __ddiv_rn(m64, a.bc1);
+    const double vhat = __ddiv_rn(v64, a.bc2);
+    const double upd = __ddiv_rn(__dmul_rn(a.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps));
+    const double w64 = __dadd_rn((double)w[i], -upd);
+    w[i] = __double2float_rn(w64);
+    m[i] = __double2float_rn(m64);
+    v[i] = __double2float_rn(v64);
+  }
+}
+
 __global__ void __launch_bounds__(256)
 compare_kernel(const unsigned char* a, const unsigned char* b, uint64_t n,
                unsigned long long* mismatch) {
@@ -848,6 +870,18 @@ int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, f
   if (!out) return UCP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   gen_state_kernel<<<grid_for(count, 256 * 4 * 4), 256, 0, s>>>(base, start, count, abs_flag, out);
+  return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
+}
+
+int ucp_adam_step(float* w, float* m, float* v, uint64_t count, uint64_t grad_base,
+                  uint64_t start, double b1, double one_minus_b1, double b2,
+                  double one_minus_b2, double bc1, double bc2, double lr, double eps,
+                  void* stream) {
+  if (count == 0) return UCP_OK;
+  if (!w || !m || !v) return UCP_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const AdamArgs a{b1, one_minus_b1, b2, one_minus_b2, bc1, bc2, lr, eps};
+  adam_step_kernel<<<grid_for(count, 256 * 8), 256, 0, s>>>(w, m, v, count, grad_base, start, a);
   return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
 }
 

@@ -247,3 +247,54 @@ class PeerBuffers:
         if self.local:
             lib.ucp_dev_free(ctypes.c_void_p(self.local))
             self.local = 0
+
+
+class NcclComm:
+    """libucp_b200_comm.so communicator (one per process / GPU). Rank 0's
+    unique id is distributed over the default torch.distributed group."""
+
+    def __init__(self, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _native
+        from ._errors import NativeUnavailableError
+
+        lib = _native.comm_lib()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (ctypes.c_char * 128)()
+        if rank == 0 and lib.ucp_comm_unique_id(uid):
+            raise NativeUnavailableError("ucp_comm_unique_id failed")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = (ctypes.c_char * 128).from_buffer_copy(box[0])
+        comm = ctypes.c_void_p()
+        if lib.ucp_comm_init(world, rank, uid, ctypes.byref(comm)):
+            raise NativeUnavailableError("ucp_comm_init failed")
+        self.comm, self.world, self.rank = comm.value, world, rank
+
+    def alltoallv(self, send_ptr: int, send_counts: list, recv_ptr: int, recv_counts: list,
+                  stream_ptr: int) -> None:
+        import ctypes
+
+        import numpy as np
+
+        from . import _native
+        from ._errors import NativeUnavailableError
+
+        sc = np.ascontiguousarray(send_counts, dtype=np.uint64)
+        rc = np.ascontiguousarray(recv_counts, dtype=np.uint64)
+        if _native.comm_lib().ucp_alltoallv(ctypes.c_void_p(self.comm), ctypes.c_void_p(send_ptr),
+                                            sc.ctypes.data, ctypes.c_void_p(recv_ptr),
+                                            rc.ctypes.data, ctypes.c_void_p(stream_ptr)):
+            raise NativeUnavailableError("ucp_alltoallv failed")
+
+    def close(self) -> None:
+        import ctypes
+
+        from . import _native
+
+        if self.comm:
+            _native.comm_lib().ucp_comm_destroy(ctypes.c_void_p(self.comm))
+            self.comm = None

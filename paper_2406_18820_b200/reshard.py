@@ -287,7 +287,7 @@ class ReshardPlan:
                 ev[3].record(stream)
 
     def step_device_homed(self, exch, group=None, stream=None, comm_stream=None,
-                          events=None) -> None:
+                          events=None, comm=None) -> None:
         """Rank-homed variant of ``step_device`` (north_star item 3): after
         window w's reshard launches, its target region (ordered by home GPU,
         see ``layout_windows``) is exchanged with one all-to-all-v over NCCL
@@ -325,8 +325,13 @@ class ReshardPlan:
             sizes = [nb for _, nb in exch.send[w]]
             with torch.cuda.stream(comm_stream):
                 comm_stream.wait_event(ready)
-                dist.all_to_all_single(recv[slot][:exch.recv_bytes(w)], ring[slot][:sum(sizes)],
-                                       exch.recv[w], sizes, group=group)
+                if comm is not None:  # libucp_b200_comm.so: grouped ncclSend/ncclRecv
+                    comm.alltoallv(ring[slot].data_ptr(), sizes, recv[slot].data_ptr(),
+                                   exch.recv[w], comm_stream.cuda_stream)
+                else:
+                    dist.all_to_all_single(recv[slot][:exch.recv_bytes(w)],
+                                           ring[slot][:sum(sizes)], exch.recv[w], sizes,
+                                           group=group)
                 fin = torch.cuda.Event()
                 fin.record(comm_stream)
             done[slot] = fin

@@ -231,6 +231,30 @@ def main() -> None:
     out["grid"] = grid
     print("grid cells", len(grid))
 
+    # --- toy trainer (ucp/models.py:247-328): trained-state digests
+    from ucp.models import TrainerConfig, train_steps
+
+    def state_digest(st) -> str:
+        h = hashlib.sha256()
+        for p in st.spec.params:
+            for kind in ("weight", "m", "v"):
+                h.update(f"{p.name}|{kind}|".encode())
+                h.update(np.ascontiguousarray(getattr(st.params[p.name], kind).data).tobytes())
+        h.update(f"step={st.step}".encode())
+        return h.hexdigest()
+
+    trained = []
+    for fam in SCALES:
+        for n in (1, 3):
+            st = train_steps(ucp.init_state(specs[fam], 7), TrainerConfig(), 0, n)
+            trained.append({"model": fam, "steps": n, "digest": state_digest(st),
+                            "iteration": st.metadata["iteration"]})
+    st = train_steps(ucp.init_state(specs["GQA"], 7), TrainerConfig(lr=3e-2, beta1=0.8, grad_seed=5),
+                     0, 4)
+    trained.append({"model": "GQA", "steps": 4, "cfg": {"lr": 3e-2, "beta1": 0.8, "grad_seed": 5},
+                    "digest": state_digest(st), "iteration": 4})
+    out["trained"] = trained
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
         f.write("\n")

@@ -55,3 +55,14 @@ def test_argument_errors_without_device():
     assert lib.ucp_load_scatter(None, 0, None, None, zero.ctypes.data, None, None, None, None) == 0
     assert lib.ucp_gen_state(0, 0, 0, 0, None, None) == 0
     assert lib.ucp_status_reset(None, None) == -10
+
+
+def test_comm_library_exports():
+    hdr = HDR.replace("ucp_b200.h", "ucp_b200_comm.h")
+    names = sorted(set(re.findall(r"^int\s+(ucp_\w+)\s*\(", open(hdr).read(), flags=re.M)))
+    assert names == sorted(_native.COMM_EXPORTS)
+    lib = _native.comm_lib()
+    for n in names:
+        assert hasattr(lib, n)
+    assert lib.ucp_comm_version() == 1
+    assert lib.ucp_comm_init(0, 0, None, None) == -10

@@ -190,3 +190,15 @@ def test_reference_verify_grid(golden, tmp_path, chunk):
                 assert np.array_equal(atomic[p.name][kind], state[p.name][kind])
         for dt in ("F32", "BF16"):
             assert O.world_digest(O.load_mem(spec, atomic, b, dt)) == row[f"world_{dt}"]
+
+
+def test_trainer_matches_reference(golden):
+    from helpers import SCALES
+    from paper_2406_18820_b200.zoo import make_model
+
+    for row in golden["trained"]:
+        spec = make_model(row["model"], SCALES[row["model"]])
+        kw = row.get("cfg", {})
+        kw = {"lr": kw.get("lr", 1e-3), "b1": kw.get("beta1", 0.9), "grad_seed": kw.get("grad_seed", 2024)}
+        st = O.train_mem(spec, O.init_state(spec, 7), 0, row["steps"], **kw)
+        assert O.state_digest(spec, st, row["steps"]) == row["digest"], row
