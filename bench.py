@@ -67,6 +67,11 @@ def parse():
                          "torch.distributed")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to smoke-test the multi-rank logic with >1 rank per GPU")
+    ap.add_argument("--no-atomic", action="store_true",
+                    help="fused path without materialising the atomic tensors (pure in-memory "
+                         "resume; not the default: convert's output is the atomic checkpoint)")
+    ap.add_argument("--non-strict", action="store_true",
+                    help="strict_replicate=False: read one replica per replication group")
     ap.add_argument("--unfused", action="store_true",
                     help="separate convert and load launches (atomic re-read from HBM)")
     ap.add_argument("--cpu-threads", type=int, default=os.cpu_count())
@@ -269,7 +274,8 @@ def run_ours(args):
             peer = PeerBuffers(exch.max_recv, n_slots=2)
     plan = ReshardPlan(spec, src, tgt, params=mine, device=dev,
                        window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024,
-                       fused=not args.unfused,
+                       fused=not args.unfused, strict=not args.non_strict,
+                       materialize_atomic=not args.no_atomic,
                        home_of=[g % world for g in range(tgt.world_size)] if homed else None,
                        n_homes=world if homed else 1,
                        peer=(exch, peer) if peer is not None else None)
@@ -496,7 +502,8 @@ def run_ours(args):
                      "residency": ("windowed: sources synthesised per window outside the timed "
                                    "events; value = S / sum of per-window reshard time")
                      if windowed else "whole source arena resident in HBM",
-                     "strict_replicate": True},
+                     "strict_replicate": not args.non_strict,
+                     "atomic_materialised": not args.no_atomic},
           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
           "gpu_launches": gpu_launches, "parity": parity}, rank)
     if peer is not None:
