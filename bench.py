@@ -293,7 +293,7 @@ def run_ours(args):
         for k in ("atom_ref", "atom_back"):
             plan._bufs.pop(k, None)
         torch.cuda.empty_cache()
-        if not (parity["atomic_ok"] and parity["target_ok"] in (True, None)):
+        if parity["atomic_ok"] is False or parity["target_ok"] is False:
             raise SystemExit(f"parity failure: {parity}")
 
     stream = torch.cuda.current_stream()

@@ -396,3 +396,48 @@ def test_reference_verify_grid_gpu(golden, tmp_path, chunk):
             world = U.load(atom, b, dtype=dt)
             wd = {g: [(s.meta, s.tensor.data) for s in world.shards[g]] for g in world.shards}
             assert O.world_digest(wd) == row[f"world_{dt.name}"], (row["model"], row["tgt"], dt)
+
+
+def test_fused_pad_error_and_bypass_counters(tmp_path):
+    # nonzero ZeRO pad through the fused engine (CHECKZERO rides in the
+    # unfused remainder of a fused window)
+    spec = U.make_model("DenseGPT", {"n_layers": 0, "hidden": 1024})
+    src_cfg, tgt_cfg = cfg(dp=3, zero="z3"), cfg(dp=2, tp=2, zero="z1")
+    shards = O.partition_mem(spec, O.init_state(spec, 7), src_cfg)
+    host = {g: [a.copy() for _, a in v] for g, v in shards.items()}
+    recs = U.enumerate_rank_records(spec, src_cfg, 2)
+    i = next(k for k, m in enumerate(recs) if m.param == "pos.alibi" and m.kind == "m")
+    assert recs[i].pad_elems == 2
+    host[2][i][-1] = np.float32(1.0)
+    with pytest.raises(U.PaddingError):
+        ReshardPlan(spec, src_cfg, tgt_cfg, fused=True).run_host(host)
+    # read amplification (SPEC criterion 5): bypass=False reads every file dp times
+    src, _ = _src_tree(tmp_path, U.make_model("GQA", {"n_layers": 4, "hidden": 64, "q_heads": 8,
+                                                      "kv_heads": 2}), cfg(dp=2, tp=1, pp=4, zero="z1"))
+    atom = str(tmp_path / "atomic")
+    U.convert(src, atom)
+    tgt = cfg(dp=4)
+    st_on, st_off = U.load(atom, tgt).stats, U.load(atom, tgt, bypass=False).stats
+    assert st_on.group_files_read == st_on.group_files_needed
+    assert st_off.group_files_read == {k: v * tgt.dp for k, v in st_off.group_files_needed.items()}
+    assert st_off.bytes_read == tgt.dp * st_on.bytes_read
+
+
+def test_zero2_alias_pipeline(tmp_path):
+    # extension G1: cfg4-shaped ZeRO-3 DP8 -> "ZeRO-2" TP2/SP2/DP4 on a small GPT
+    spec = U.make_model("DenseGPT", {"n_layers": 4, "hidden": 64})
+    src_cfg = cfg(dp=8, zero="z3")
+    tgt_cfg = ParallelConfig(dp=4, tp=2, sp=2, zero_stage=ZeroStage.Z2)
+    state = O.init_state(spec, 7)
+    src, shards = _src_tree(tmp_path, spec, src_cfg)
+    atom = str(tmp_path / "atomic")
+    U.convert(src, atom)
+    want = str(tmp_path / "want")
+    O.write_atomic(spec, state, want, fingerprint=O.config_fingerprint(src))
+    assert O.dir_digest(atom) == O.dir_digest(want)
+    world = U.load(atom, tgt_cfg, dtype=DType.BF16)
+    wd = {g: [(s.meta, s.tensor.data) for s in world.shards[g]] for g in world.shards}
+    assert O.world_digest(wd) == O.world_digest(O.load_mem(spec, state, tgt_cfg, "BF16"))
+    # identical bytes to the Z1 layout
+    z1 = ParallelConfig(dp=4, tp=2, sp=2, zero_stage=ZeroStage.Z1)
+    assert O.world_digest(wd) == O.world_digest(O.load_mem(spec, state, z1, "BF16"))
