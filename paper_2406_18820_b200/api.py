@@ -16,6 +16,7 @@ from __future__ import annotations
 import hashlib
 import json
 import os
+import threading
 from collections import defaultdict
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -31,14 +32,8 @@ from ._errors import (
     ShapeError,
     UnsupportedCastError,
 )
-from .engine import Arena, Program, Status, align_up, gen_state, require_device
-from .layout import (
-    all_rank_records,
-    enumerate_rank_records,
-    layer_of,
-    pp_layer_map,
-    validate_model_config,
-)
+from .engine import Program, Status, align_up, gen_state, require_device
+from .layout import all_rank_records, layer_of, pp_layer_map, validate_model_config
 from .plan import RunTable, compile_extract, compile_union, fragment_elems, fragment_shape
 from .spec import (
     FORMAT_VERSION,
@@ -204,15 +199,38 @@ class _Staging:
         return b
 
 
-_STAGE = _Staging()
-_STATUS: dict = {}
+class _PerThread(threading.local):
+    """Staging buffers and status words are per thread: the reference runs
+    union()/write_union() concurrently from reducer threads
+    (ucp/convert.py:512-522), and every call here is reentrant."""
+
+    def __init__(self):
+        self.stage = _Staging()
+        self.status: dict = {}
+
+
+_LOCAL = _PerThread()
+
+
+class _StageProxy:
+    def __getattr__(self, name):
+        return getattr(_LOCAL.stage, name)
+
+
+_STAGE = _StageProxy()
 
 
 def _status(dev) -> Status:
-    s = _STATUS.get(str(dev))
+    s = _LOCAL.status.get(str(dev))
     if s is None:
-        s = _STATUS[str(dev)] = Status(dev)
+        s = _LOCAL.status[str(dev)] = Status(dev)
     return s
+
+
+def release_staging() -> None:
+    """Drop this thread's pinned / device staging buffers (they are
+    grow-only and reused across calls otherwise)."""
+    _LOCAL.stage = _Staging()
 
 
 def _run(prog: Program, gather: bool, src_base: int, dst_base: int, dev) -> None:

@@ -777,28 +777,27 @@ def compile_fused(fx: XRunTable, rest_conv: RunTable, rest_load: RunTable, p: Pa
         _absorb(rest_conv, conv)
         _absorb(rest_load, load)
         return False
+    cmap, lmap = {}, {}
     tag = fx.unit(p.name, frags[0][0].kind)
     for srcs, atom, dsts, sp, dp, rows, cols, ci in cells:
         fx.add(srcs=srcs, atom=atom if materialize else NO_ATOM, dsts=dsts, src_pitch=sp,
                atom_pitch=W, dst_pitch=dp, rows=rows, cols=cols, dtype=dtype, tag=tag,
                labels=conv.units[0].labels.get(ci) if conv.units else None)
     for i in extra_conv:
-        _absorb_row(rest_conv, conv, i)
+        _absorb_row(rest_conv, conv, i, cmap)
     for i in extra_load:
-        _absorb_row(rest_load, load, i)
+        _absorb_row(rest_load, load, i, lmap)
     return True
 
 
-def _absorb_row(dst: RunTable, src: RunTable, i: int) -> None:
+def _absorb_row(dst: RunTable, src: RunTable, i: int, tags: dict) -> None:
+    """Copy run i of src into dst; ``tags`` maps src unit ids to dst unit
+    ids for this (src, dst) pair."""
     (s0, d0, sp, dp, rows, cols, aux, ns, nd, groups, op, dt, tpr, tp, tag, flags) = src._rows[i]
     unit = src.units[tag]
-    key = (id(src), tag)
-    new_tag = dst._adopted.get(key) if hasattr(dst, "_adopted") else None
+    new_tag = tags.get(tag)
     if new_tag is None:
-        if not hasattr(dst, "_adopted"):
-            dst._adopted = {}
-        new_tag = dst.unit(unit.param, unit.kind)
-        dst._adopted[key] = new_tag
+        new_tag = tags[tag] = dst.unit(unit.param, unit.kind)
     nsx = max(ns - 1, 0)
     srcs = ([s0] + src._aux[aux:aux + nsx]) if ns else []
     dsts = ([d0] + src._aux[aux + nsx:aux + nsx + nd - 1]) if nd else []
@@ -808,5 +807,6 @@ def _absorb_row(dst: RunTable, src: RunTable, i: int) -> None:
 
 
 def _absorb(dst: RunTable, src: RunTable) -> None:
+    tags: dict = {}
     for i in range(len(src._rows)):
-        _absorb_row(dst, src, i)
+        _absorb_row(dst, src, i, tags)

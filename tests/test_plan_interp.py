@@ -359,3 +359,32 @@ def test_shard_hy_grid_union():
         compile_union(RunTable(), p, ParallelConfig(), frags + frags[:1], 0, True)
     with pytest.raises(U.MissingFragmentError):
         compile_union(RunTable(), p, ParallelConfig(), frags[1:], 0, True)
+
+
+def test_fused_remainder_keeps_unit_provenance():
+    # units that cannot fuse (Partial mean/noise) are re-homed into the
+    # unfused tables; their runs must keep pointing at the right (param, kind)
+    from paper_2406_18820_b200.plan import XRunTable, compile_fused
+
+    spec = U.make_model("DenseGPT", {"n_layers": 2, "hidden": 32})
+    src_cfg, tgt_cfg = ParallelConfig(dp=3, tp=2, zero_stage=ZeroStage.Z1), ParallelConfig(tp=4)
+    srecs, trecs = all_rank_records(spec, src_cfg), all_rank_records(spec, tgt_cfg)
+    fx, rc, rl = XRunTable(), RunTable(), RunTable()
+    aoff, at = {}, 0
+    for p in spec.params:
+        for k in STATE_KINDS:
+            aoff[(p.name, k)] = (at, at + 4 * p.numel)
+            frags = [(m, 1 << 40, fragment_elems(p, src_cfg, m)) for g in range(src_cfg.world_size)
+                     for m in srecs[g] if (m.param, m.kind) == (p.name, k)]
+            tg = [(m, 1 << 41) for g in range(tgt_cfg.world_size) for m in trecs[g]
+                  if (m.param, m.kind) == (p.name, k)]
+            compile_fused(fx, rc, rl, p, src_cfg, frags, at, tgt_cfg, tg)
+            at += align_up(4 * p.numel)
+    assert len(rc) and len(rl)
+    for table, field in ((rc, 1), (rl, 0)):
+        for row in table._rows:
+            if row[10] in (3, 4):  # ZERO / CHECKZERO do not touch the atomic
+                continue
+            unit = table.units[row[14]]
+            lo, hi = aoff[(unit.param, unit.kind)]
+            assert lo <= row[field] < hi, (unit.param, unit.kind)
