@@ -394,7 +394,7 @@ def run_ours(args):
     if windowed:
         parity = parity or {"note": "windowed run: parity is covered by the resident runs and "
                             "tests (state exceeds HBM)"}
-    if not args.no_e2e and not windowed and peer is None:
+    if not args.no_e2e and peer is None:
         budget = args.e2e_gb * GB / world  # pinned host memory is shared by all ranks
         wins, acc = [], 0
         for W in plan.windows:
@@ -408,14 +408,17 @@ def run_ours(args):
         eplan = ReshardPlan(spec, src, tgt, params=names, device=dev,
                             window_bytes=int(args.e2e_window_gb * GB),
                             tile_bytes=args.tile_kb * 1024, fused=not args.unfused)
-        arena = plan._bufs["src_arena"]
-        where = {(g, i): W.src_base + off for W in wins for g, i, m, off, n in W.src_frags}
+        # inputs of the sample: synthesised by the GPU generator into the
+        # e2e plan's own arena, then copied to pinned host memory (untimed)
+        for key in ("src_arena", "tgt0", "tgt1", "src_win"):
+            plan._bufs.pop(key, None)
+        torch.cuda.empty_cache()
+        eplan.synthesize(7)
         host_src = torch.empty(max(eplan.src_total, 256), dtype=torch.uint8, pin_memory=True)
         host_tgt = torch.empty(max(eplan.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
-        for W in eplan.windows:
-            for g, i, m, off, n in W.src_frags:
-                a = where[(g, i)]
-                host_src[W.src_base + off:W.src_base + off + 4 * n].copy_(arena[a:a + 4 * n])
+        host_src[:eplan.src_total].copy_(eplan._bufs["src_arena"][:eplan.src_total])
+        eplan._bufs.pop("src_arena", None)
+        torch.cuda.empty_cache()
         if rank == 0 and world == 1 and not args.no_cpu:
             cpu_names = [p.name for p in wins[-1].params]
             hv = host_src.numpy()
@@ -426,9 +429,6 @@ def run_ours(args):
                         at = W.src_base + off
                         a = hv[at:at + 4 * n].view("<f4").copy().reshape(m.shape)
                         host_cpu_frags.setdefault((m.param, m.kind), []).append((m, a))
-        for key in ("src_arena", "tgt0", "tgt1"):
-            plan._bufs.pop(key, None)
-        torch.cuda.empty_cache()
         streams = tuple(torch.cuda.Stream(dev) for _ in range(3))
         eplan.status.reset()
         eplan.stream_host(host_src, host_tgt, None, streams)
