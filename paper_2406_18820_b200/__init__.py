@@ -36,6 +36,7 @@ from .api import (
     UcpInfo,
     WorldShard,
     cast,
+    consolidate_world,
     conversions_invoked,
     convert,
     extract_fragment,

@@ -791,3 +791,29 @@ def reshard(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: d
 
     plan = ReshardPlan(spec, src, tgt, dtype=dtype, strict=strict, device=device, fused=fused)
     return plan.run_host(shards)
+
+
+def consolidate_world(world: LoadedWorld) -> ModelState:
+    """Rebuild the consolidated ModelState of a loaded world on the GPU: the
+    union of every (param, kind) over the target layout (the role of
+    ucp/oracle.py:213-226; here it is the convert kernel applied to
+    in-memory shards). Weights must be f32 (bf16/f16 casts are lossy)."""
+    spec, tgt = world.spec, world.cfg
+    by_unit = defaultdict(list)
+    for g in sorted(world.shards):
+        for s in world.shards[g]:
+            if s.tensor.dtype is not DType.F32:
+                raise ShapeError(f"{s.meta.param}.{s.meta.kind}: consolidate needs f32 shards")
+            by_unit[(s.meta.param, s.meta.kind)].append(FragmentMsg(s.meta, s.tensor.data))
+    params = {}
+    for p in spec.params:
+        lead = spec.tied_leader(p.name)
+        if lead != p.name and lead in params:
+            params[p.name] = params[lead]
+            continue
+        ts = []
+        for kind in STATE_KINDS:
+            arr = union(p, tgt, by_unit.get((p.name, kind), []), strict=True)
+            ts.append(Tensor(DType.F32, tuple(p.shape), np.ascontiguousarray(arr)))
+        params[p.name] = ParamState(*ts)
+    return ModelState(spec, params, world.step, dict(world.metadata))

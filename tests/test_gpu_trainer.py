@@ -59,6 +59,9 @@ def test_resume_equivalence(tmp_path, pair):
     back = _model_state(spec, O.consolidate_world(spec, b, wd), 3)
     resumed = U.train_steps(back, tc, 3, 3)
     assert U.first_diff(resumed, straight) is None
+    # the product's own consolidation (GPU union over the world) agrees
+    mine = U.consolidate_world(world)
+    assert U.first_diff(mine, back) is None
 
 
 def test_native_nccl_alltoallv_single_rank():
