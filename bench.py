@@ -388,7 +388,8 @@ def run_ours(args):
     gpu_launches = args.steps * plan.n_launches
 
     # ---- live copy reference in the same process (context for roofline.peak):
-    # torch copy_ of 1 Gi bf16 elements, best of 5, read + write bytes
+    # torch copy_ of 1 Gi bf16 elements (MEASURED_PEAKS.json's method), best
+    # of 20, read + write bytes
     plan.free()  # the timed plan's buffers are not needed any more
     torch.cuda.empty_cache()
     live = None
@@ -396,7 +397,7 @@ def run_ours(args):
         a_ = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
         b_ = torch.empty_like(a_)
         best = 1e9
-        for _ in range(6):
+        for _ in range(20):
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(stream)
             b_.copy_(a_)

@@ -25,9 +25,18 @@ static_assert(sizeof(ucp_xrun) == 64, "ucp_xrun must be 64 bytes");
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef UCP_THREADS
+#define UCP_THREADS 256
+#endif
+#ifndef UCP_MINB
+#define UCP_MINB 4  // CTAs per SM the vector kernels are register-limited to
+#endif
+#ifndef UCP_VEC
+#define UCP_VEC 4
+#endif
+constexpr int kThreads = UCP_THREADS;
 constexpr int kWarps = kThreads / 32;
-constexpr int kVec = 4;                  // 16-B vectors per lane per segment
+constexpr int kVec = UCP_VEC;            // 16-B vectors per lane per segment
 constexpr uint32_t kSeg = 32 * 4 * kVec;  // elements per warp segment (512)
 constexpr int kMaxAux = 256;             // host splits runs beyond this
 
@@ -647,13 +656,13 @@ __device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
       const ucp_tile *__restrict__ tiles, const char *__restrict__ sb, char *__restrict__ ab, \
       char *__restrict__ db, ucp_status *st
 
-__global__ void __launch_bounds__(kThreads, 4) reshard_fused_f32(UCP_FUSED_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f32(UCP_FUSED_ARGS) {
   fused_body<UCP_DT_F32>(runs, aux, tiles, sb, ab, db, st);
 }
-__global__ void __launch_bounds__(kThreads, 4) reshard_fused_bf16(UCP_FUSED_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_bf16(UCP_FUSED_ARGS) {
   fused_body<UCP_DT_BF16>(runs, aux, tiles, sb, ab, db, st);
 }
-__global__ void __launch_bounds__(kThreads, 4) reshard_fused_f16(UCP_FUSED_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f16(UCP_FUSED_ARGS) {
   fused_body<UCP_DT_F16>(runs, aux, tiles, sb, ab, db, st);
 }
 
@@ -667,16 +676,16 @@ __global__ void __launch_bounds__(kThreads, 4) reshard_fused_f16(UCP_FUSED_ARGS)
       const ucp_tile *__restrict__ tiles, const char *__restrict__ sb, char *__restrict__ db, \
       ucp_status *st
 
-__global__ void __launch_bounds__(kThreads, 4) convert_gather_f32(UCP_MOVE_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_MINB) convert_gather_f32(UCP_MOVE_ARGS) {
   vec_body<UCP_DT_F32>(runs, aux, tiles, sb, db, st);
 }
-__global__ void __launch_bounds__(kThreads, 4) load_scatter_f32(UCP_MOVE_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_f32(UCP_MOVE_ARGS) {
   vec_body<UCP_DT_F32>(runs, aux, tiles, sb, db, st);
 }
-__global__ void __launch_bounds__(kThreads, 4) load_scatter_bf16(UCP_MOVE_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_bf16(UCP_MOVE_ARGS) {
   vec_body<UCP_DT_BF16>(runs, aux, tiles, sb, db, st);
 }
-__global__ void __launch_bounds__(kThreads, 4) load_scatter_f16(UCP_MOVE_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_f16(UCP_MOVE_ARGS) {
   vec_body<UCP_DT_F16>(runs, aux, tiles, sb, db, st);
 }
 __global__ void __launch_bounds__(kThreads) convert_gather_general(UCP_MOVE_ARGS) {
