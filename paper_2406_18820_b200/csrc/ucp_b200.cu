@@ -34,6 +34,9 @@ namespace {
 #ifndef UCP_VEC
 #define UCP_VEC 4
 #endif
+#ifndef UCP_PERSISTENT
+#define UCP_PERSISTENT 0  // 1: fused kernel runs 148*UCP_MINB persistent CTAs over the tiles
+#endif
 constexpr int kThreads = UCP_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kVec = UCP_VEC;            // 16-B vectors per lane per segment
@@ -554,15 +557,13 @@ __device__ __forceinline__ void general_body(const ucp_run* __restrict__ runs,
 // HBM traffic R_c + W_c + W_l instead of R_c + 2 S + W_l.
 
 template <int DT>
-__device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
+__device__ __forceinline__ void fused_tile(const ucp_xrun* __restrict__ runs,
                                            const uint64_t* __restrict__ aux,
-                                           const ucp_tile* __restrict__ tiles,
+                                           const ucp_tile& tile, ucp_xrun& s_run,
+                                           uint64_t* s_aux,
                                            const char* __restrict__ sb, char* __restrict__ ab,
                                            char* __restrict__ db, ucp_status* st) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  __shared__ ucp_xrun s_run;
-  __shared__ uint64_t s_aux[kMaxAux];
-  const ucp_tile tile = tiles[blockIdx.x];
   if (threadIdx.x < 4) {
     reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
         reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
@@ -651,19 +652,41 @@ __device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
   }
 }
 
+template <int DT>
+__device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
+                                           const uint64_t* __restrict__ aux,
+                                           const ucp_tile* __restrict__ tiles, uint32_t n_tiles,
+                                           const char* __restrict__ sb, char* __restrict__ ab,
+                                           char* __restrict__ db, ucp_status* st) {
+  __shared__ ucp_xrun s_run;
+  __shared__ uint64_t s_aux[kMaxAux];
+#if UCP_PERSISTENT
+  // persistent CTAs walk the tile list; the barrier protects s_run / s_aux
+  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+    const ucp_tile tile = tiles[ti];
+    fused_tile<DT>(runs, aux, tile, s_run, s_aux, sb, ab, db, st);
+    __syncthreads();
+  }
+#else
+  (void)n_tiles;
+  const ucp_tile tile = tiles[blockIdx.x];
+  fused_tile<DT>(runs, aux, tile, s_run, s_aux, sb, ab, db, st);
+#endif
+}
+
 #define UCP_FUSED_ARGS                                                                     \
   const ucp_xrun *__restrict__ runs, const uint64_t *__restrict__ aux,                      \
-      const ucp_tile *__restrict__ tiles, const char *__restrict__ sb, char *__restrict__ ab, \
-      char *__restrict__ db, ucp_status *st
+      const ucp_tile *__restrict__ tiles, uint32_t n_tiles, const char *__restrict__ sb,     \
+      char *__restrict__ ab, char *__restrict__ db, ucp_status *st
 
 __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f32(UCP_FUSED_ARGS) {
-  fused_body<UCP_DT_F32>(runs, aux, tiles, sb, ab, db, st);
+  fused_body<UCP_DT_F32>(runs, aux, tiles, n_tiles, sb, ab, db, st);
 }
 __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_bf16(UCP_FUSED_ARGS) {
-  fused_body<UCP_DT_BF16>(runs, aux, tiles, sb, ab, db, st);
+  fused_body<UCP_DT_BF16>(runs, aux, tiles, n_tiles, sb, ab, db, st);
 }
 __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f16(UCP_FUSED_ARGS) {
-  fused_body<UCP_DT_F16>(runs, aux, tiles, sb, ab, db, st);
+  fused_body<UCP_DT_F16>(runs, aux, tiles, n_tiles, sb, ab, db, st);
 }
 
 // ---------------------------------------------------------------- entry kernels
@@ -863,11 +886,17 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
   for (int c = 0; c < UCP_CLASS_GENERAL; ++c) {
     const int64_t n = class_counts[c];
     if (n == 0) continue;
-    const dim3 grid((unsigned)n), block(kThreads);
+#if UCP_PERSISTENT
+    const unsigned g = (unsigned)(n < (int64_t)148 * UCP_MINB ? n : (int64_t)148 * UCP_MINB);
+#else
+    const unsigned g = (unsigned)n;
+#endif
+    const dim3 grid(g), block(kThreads);
     const ucp_tile* t = tiles + at;
-    if (c == UCP_CLASS_VEC_F32) reshard_fused_f32<<<grid, block, 0, s>>>(runs, aux, t, sb, ab, db, status);
-    else if (c == UCP_CLASS_VEC_BF16) reshard_fused_bf16<<<grid, block, 0, s>>>(runs, aux, t, sb, ab, db, status);
-    else reshard_fused_f16<<<grid, block, 0, s>>>(runs, aux, t, sb, ab, db, status);
+    const uint32_t nt = (uint32_t)n;
+    if (c == UCP_CLASS_VEC_F32) reshard_fused_f32<<<grid, block, 0, s>>>(runs, aux, t, nt, sb, ab, db, status);
+    else if (c == UCP_CLASS_VEC_BF16) reshard_fused_bf16<<<grid, block, 0, s>>>(runs, aux, t, nt, sb, ab, db, status);
+    else reshard_fused_f16<<<grid, block, 0, s>>>(runs, aux, t, nt, sb, ab, db, status);
     at += n;
   }
   return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
