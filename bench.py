@@ -494,7 +494,9 @@ def run_ours(args):
             host_cpu_frags = oracle_frags(spec, src, cpu_names, args.cpu_threads)
         S_cpu = sum(12 * spec.param(n).numel for n in cpu_names)
         t_cpu = cpu_reshard(spec, src, tgt, host_cpu_frags, args.cpu_threads)
+        t_cpu1 = cpu_reshard(spec, src, tgt, host_cpu_frags, 1)
         cpu = {"value": S_cpu / t_cpu / GB, "unit": "GB/s", "cores": args.cpu_threads,
+               "value_1_thread": S_cpu / t_cpu1 / GB,
                "kind": "port",
                "sample": f"{len(cpu_names)} params ({cpu_names[0]} .. {cpu_names[-1]}), "
                          f"{S_cpu / GB:.2f} GB state: oracle union + extract_fragment "

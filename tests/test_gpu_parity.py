@@ -441,3 +441,25 @@ def test_zero2_alias_pipeline(tmp_path):
     # identical bytes to the Z1 layout
     z1 = ParallelConfig(dp=4, tp=2, sp=2, zero_stage=ZeroStage.Z1)
     assert O.world_digest(wd) == O.world_digest(O.load_mem(spec, state, z1, "BF16"))
+
+
+def test_union_is_reentrant_across_threads():
+    # the reference calls union() from reducer threads (ucp/convert.py:512-522)
+    from concurrent.futures import ThreadPoolExecutor
+
+    spec = U.make_model("GQA", {"n_layers": 2, "hidden": 64, "q_heads": 8, "kv_heads": 2})
+    c = cfg(dp=2, tp=2, pp=1, zero="z1")
+    state = O.init_state(spec, 7)
+    shards = O.partition_mem(spec, state, c)
+    recs = {g: U.enumerate_rank_records(spec, c, g) for g in shards}
+    units = {}
+    for g, items in shards.items():
+        for m, (_, a) in zip(recs[g], items):
+            units.setdefault((m.param, m.kind), []).append(U.FragmentMsg(m, a))
+
+    def one(key):
+        out = U.union(spec.param(key[0]), c, units[key])
+        return np.array_equal(out.view(np.uint32), state[key[0]][key[1]].view(np.uint32))
+
+    with ThreadPoolExecutor(8) as pool:
+        assert all(pool.map(one, list(units) * 3))
