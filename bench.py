@@ -288,8 +288,8 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     parity = None
-    if not args.no_verify and not windowed:
-        parity = plan.verify(7)
+    if not args.no_verify:
+        parity = plan.verify(7, windowed=windowed)
         for k in ("atom_ref", "atom_back"):
             plan._bufs.pop(k, None)
         torch.cuda.empty_cache()
@@ -417,9 +417,6 @@ def run_ours(args):
     e2e = None
     host_cpu_frags = None
     cpu_names = None
-    if windowed:
-        parity = parity or {"note": "windowed run: parity is covered by the resident runs and "
-                            "tests (state exceeds HBM)"}
     if not args.no_e2e and peer is None:
         budget = args.e2e_gb * GB / world  # pinned host memory is shared by all ranks
         wins, acc = [], 0

@@ -494,7 +494,7 @@ class ReshardPlan:
 
     # ------------------------------------------------------------------ verification
 
-    def verify(self, seed: int = 7) -> dict:
+    def verify(self, seed: int = 7, windowed: bool = False) -> dict:
         """Full-size, size-independent parity check on the device (outside
         any timed region), for states synthesised with ``synthesize(seed)``:
 
@@ -506,10 +506,13 @@ class ReshardPlan:
            are a valid checkpoint of the same state under the target layout
            (needs f32 targets; bf16/f16 weights are lossy by design).
 
+        ``windowed``: for states larger than HBM, each window's sources are
+        synthesised into a window-sized arena first (as ``step_windowed``).
+
         Returns {"windows": n, "atomic_ok": bool|None, "target_ok": bool|None}."""
         from .engine import compare
 
-        arena = self._bufs["src_arena"]
+        arena = self.buf("src_win", self.max_src) if windowed else self._bufs["src_arena"]
         atom = self.buf("atom", self.max_atom)
         ref = self.buf("atom_ref", self.max_atom)
         back = self.buf("atom_back", self.max_atom)
@@ -519,14 +522,20 @@ class ReshardPlan:
         target_ok = True if self.dtype is DType.F32 and self.peer is None else None
         for W in self.windows:
             self.status.reset()
-            src_ptr = arena.data_ptr() + W.src_base
+            src_ptr = arena.data_ptr() + (0 if windowed else W.src_base)
+            if windowed:
+                self.gen_atomic(W, ref, seed)
+                W.synth.launch(False, ref.data_ptr(), src_ptr, self.status)
             tgt_ptr = 0 if self.peer is not None else tgt.data_ptr()
             W.fused.launch(src_ptr, atom.data_ptr(), tgt_ptr, self.status)
             W.conv.launch(True, src_ptr, atom.data_ptr(), self.status)
             W.load.launch(False, atom.data_ptr(), tgt_ptr, self.status)
-            self.gen_atomic(W, ref, seed)
+            if not windowed:
+                self.gen_atomic(W, ref, seed)
             torch.cuda.synchronize(self.device)
-            self.check()
+            first, _ = self.status.read()
+            if first != (1 << 64) - 1:
+                self._locate(W, src_ptr)
             if atomic_ok:
                 compare(atom.data_ptr(), ref.data_ptr(), W.atom_bytes, mism)
                 torch.cuda.synchronize(self.device)
