@@ -31,6 +31,18 @@ _FUSED = {ParamKind.FUSED_QKV, ParamKind.FUSED_EXPERT}
 _VOCAB = {ParamKind.EMBEDDING, ParamKind.TIED_EMBEDDING}
 
 
+def kind_of(p) -> ParamKind:
+    """The param's kind as this package's enum (duck-types the reference's
+    ParamSpec objects, whose enum class differs but whose values match)."""
+    k = p.kind
+    return k if isinstance(k, ParamKind) else ParamKind(getattr(k, "value", k))
+
+
+def zero_of(cfg) -> ZeroStage:
+    z = cfg.zero_stage
+    return z if isinstance(z, ZeroStage) else ZeroStage(getattr(z, "value", z))
+
+
 def validate_model_config(spec: ModelSpec, cfg: ParallelConfig) -> None:
     cfg.validate()
     if cfg.pp > max(spec.n_layers, 1):
@@ -51,7 +63,7 @@ def vocab_padded_rows(p: ParamSpec, cfg: ParallelConfig):
     vocab padding (extension): ceil(V / (m * tp)) * m * tp, or
     None when cfg.vocab_multiple == 1 or the param is not vocab-sized."""
     m = getattr(cfg, "vocab_multiple", 1)
-    if m <= 1 or p.kind not in _VOCAB or not p.shape:
+    if m <= 1 or kind_of(p) not in _VOCAB or not p.shape:
         return None
     unit = m * cfg.tp
     return -(-p.shape[0] // unit) * unit
@@ -121,7 +133,7 @@ def _divisible(p: ParamSpec, axis: int, tp: int) -> None:
 def tp_mode(p: ParamSpec, tp: int) -> str:
     if tp == 1:
         return "full"
-    k = p.kind
+    k = kind_of(p)
     if k in _REPLICATED:
         return REPLICATE
     if k is ParamKind.ASYNC_PARTIAL:
@@ -153,6 +165,7 @@ def tp_mode(p: ParamSpec, tp: int) -> str:
 
 
 def zero_flattens(kind: str, zero: ZeroStage) -> bool:
+    zero = ZeroStage(getattr(zero, "value", zero))
     if zero is ZeroStage.Z0:
         return False
     if zero in (ZeroStage.Z1, ZeroStage.Z2):
@@ -205,7 +218,7 @@ def _all_records(spec: ModelSpec, cfg: ParallelConfig) -> tuple:
             fnumel = _numel(fshape)
             segs = p.nc_segments if mode == SHARD_NC else None
             for kind in STATE_KINDS:
-                if zero_flattens(kind, cfg.zero_stage):
+                if zero_flattens(kind, zero_of(cfg)):
                     _, pad, ranges = zero_flatten_meta(fnumel, cfg.dp)
                     lo, hi = ranges[dp_r]
                     recs.append(RecordMeta(p.name, kind, pattern_tag(mode, True, cfg.dp),
