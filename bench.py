@@ -418,74 +418,96 @@ def run_ours(args):
     host_cpu_frags = None
     cpu_names = None
     if not args.no_e2e and peer is None:
-        budget = args.e2e_gb * GB / world  # pinned host memory is shared by all ranks
-        wins, acc = [], 0
-        for W in plan.windows:
-            if wins and acc + W.src_bytes + W.tgt_bytes > budget:
-                break
-            wins.append(W)
-            acc += W.src_bytes + W.tgt_bytes
-        names = [p.name for W in wins for p in W.params]
-        # the e2e path gets its own plan with small windows so PCIe in, HBM
-        # work and PCIe out overlap with little pipeline fill / drain
-        eplan = ReshardPlan(spec, src, tgt, params=names, device=dev,
-                            window_bytes=int(args.e2e_window_gb * GB),
-                            tile_bytes=args.tile_kb * 1024, fused=not args.unfused)
-        # inputs of the sample: synthesised by the GPU generator into the
-        # e2e plan's own arena, then copied to pinned host memory (untimed)
-        eplan.synthesize(7)
-        host_src = torch.empty(max(eplan.src_total, 256), dtype=torch.uint8, pin_memory=True)
-        host_tgt = torch.empty(max(eplan.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
-        host_src[:eplan.src_total].copy_(eplan._bufs["src_arena"][:eplan.src_total])
-        eplan._bufs.pop("src_arena", None)
-        torch.cuda.empty_cache()
-        if rank == 0 and world == 1 and not args.no_cpu:
-            cpu_names = [p.name for p in wins[-1].params]
-            hv = host_src.numpy()
-            host_cpu_frags = {}
-            for W in eplan.windows:
-                for g, i, m, off, n in W.src_frags:
-                    if m.param in cpu_names:
-                        at = W.src_base + off
-                        a = hv[at:at + 4 * n].view("<f4").copy().reshape(m.shape)
-                        host_cpu_frags.setdefault((m.param, m.kind), []).append((m, a))
-        streams = tuple(torch.cuda.Stream(dev) for _ in range(3))
-        eplan.status.reset()
-        eplan.stream_host(host_src, host_tgt, None, streams)
-        torch.cuda.synchronize()
-        eplan._check_windows(host_src)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for s_ in streams:
-            s_.wait_stream(stream)
-        for _ in range(args.e2e_steps):
+        e2e_ms, S_e2e_local, e2e_err, e2e_meta = float("inf"), 0, None, {}
+        try:
+            budget = args.e2e_gb * GB / world  # pinned host memory is shared by all ranks
+            wins, acc = [], 0
+            for W in plan.windows:
+                if wins and acc + W.src_bytes + W.tgt_bytes > budget:
+                    break
+                wins.append(W)
+                acc += W.src_bytes + W.tgt_bytes
+            names = [p.name for W in wins for p in W.params]
+            # the e2e path gets its own plan with small windows so PCIe in, HBM
+            # work and PCIe out overlap with little pipeline fill / drain
+            eplan = ReshardPlan(spec, src, tgt, params=names, device=dev,
+                                window_bytes=int(args.e2e_window_gb * GB),
+                                tile_bytes=args.tile_kb * 1024, fused=not args.unfused)
+            # inputs of the sample: synthesised by the GPU generator into the
+            # e2e plan's own arena, then copied to pinned host memory (untimed)
+            eplan.synthesize(7)
+            host_src = torch.empty(max(eplan.src_total, 256), dtype=torch.uint8, pin_memory=True)
+            host_tgt = torch.empty(max(eplan.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
+            host_src[:eplan.src_total].copy_(eplan._bufs["src_arena"][:eplan.src_total])
+            eplan._bufs.pop("src_arena", None)
+            torch.cuda.empty_cache()
+            if rank == 0 and world == 1 and not args.no_cpu:
+                cpu_names = [p.name for p in wins[-1].params]
+                hv = host_src.numpy()
+                host_cpu_frags = {}
+                for W in eplan.windows:
+                    for g, i, m, off, n in W.src_frags:
+                        if m.param in cpu_names:
+                            at = W.src_base + off
+                            a = hv[at:at + 4 * n].view("<f4").copy().reshape(m.shape)
+                            host_cpu_frags.setdefault((m.param, m.kind), []).append((m, a))
+            streams = tuple(torch.cuda.Stream(dev) for _ in range(3))
+            eplan.status.reset()
             eplan.stream_host(host_src, host_tgt, None, streams)
-        for s_ in streams:
-            stream.wait_stream(s_)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-        S_e2e = S_e2e_local = eplan.state_bytes
-        if world > 1:
-            t = torch.tensor([e2e_ms, float(S_e2e)], device=red_dev, dtype=torch.float64)
-            mx = t.clone()
+            torch.cuda.synchronize()
+            eplan._check_windows(host_src)
+        except Exception as exc:  # the main line must survive a host-memory failure
+            e2e_err = f"{type(exc).__name__}: {exc}"[:300]
+        if world > 1:  # every rank reaches this barrier, prepared or not
+            ready = torch.tensor([float(e2e_err is None)], device=red_dev, dtype=torch.float64)
+            dist.all_reduce(ready, op=dist.ReduceOp.MIN)
+            if ready.item() < 1 and e2e_err is None:
+                e2e_err = "e2e preparation failed on another rank"
+        try:
+            if e2e_err is not None:
+                raise RuntimeError(e2e_err)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for s_ in streams:
+                s_.wait_stream(stream)
+            for _ in range(args.e2e_steps):
+                eplan.stream_host(host_src, host_tgt, None, streams)
+            for s_ in streams:
+                stream.wait_stream(s_)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+            S_e2e_local = eplan.state_bytes
+            e2e_meta = {"h2d": int(eplan.src_total), "d2h": int(eplan.tgt_total),
+                        "windows": len(eplan.windows), "names": names}
+            del eplan
+        except Exception as exc:  # the main line must survive a host-memory failure
+            e2e_err = f"{type(exc).__name__}: {exc}"[:300]
+        S_e2e, ok = S_e2e_local, float(e2e_err is None)
+        if world > 1:  # collectives stay outside the try so no rank can skip them
+            t = torch.tensor([e2e_ms, float(S_e2e), ok], device=red_dev, dtype=torch.float64)
+            mx, mn = t.clone(), t.clone()
             dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-            e2e_ms, S_e2e = float(mx[0]), float(t[1])
-        e2e = {"value": S_e2e / (e2e_ms / 1e3) / GB, "unit": "GB/s",
-               "h2d_bytes_per_step": int(eplan.src_total), "d2h_bytes_per_step": int(eplan.tgt_total),
-               "ms_per_step": e2e_ms, "state_bytes_per_step": int(S_e2e),
-               "sample": f"{len(names)} params ({names[0]} .. {names[-1]}; "
-                         f"{S_e2e_local / GB:.2f} GB state/rank) from pinned host memory: H2D + fused "
-                         f"reshard + D2H in {len(eplan.windows)} double-buffered windows on "
-                         "3 streams"}
-        del eplan
+            dist.all_reduce(t[1:2], op=dist.ReduceOp.SUM)
+            dist.all_reduce(mn[2:], op=dist.ReduceOp.MIN)
+            e2e_ms, S_e2e, ok = float(mx[0]), float(t[1]), float(mn[2])
+        if ok and e2e_meta:
+            names = e2e_meta["names"]
+            e2e = {"value": S_e2e / (e2e_ms / 1e3) / GB, "unit": "GB/s",
+                   "h2d_bytes_per_step": e2e_meta["h2d"], "d2h_bytes_per_step": e2e_meta["d2h"],
+                   "ms_per_step": e2e_ms, "state_bytes_per_step": int(S_e2e),
+                   "sample": f"{len(names)} params ({names[0]} .. {names[-1]}; "
+                             f"{S_e2e_local / GB:.2f} GB state/rank) from pinned host memory: "
+                             f"H2D + fused reshard + D2H in {e2e_meta['windows']} double-buffered "
+                             "windows on 3 streams"}
+        else:
+            e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0, "error": e2e_err or "failed on another rank"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+      try:
         if host_cpu_frags is None:
             cpu_names = sample_params(spec, 3e9)
             host_cpu_frags = oracle_frags(spec, src, cpu_names, args.cpu_threads)
@@ -498,6 +520,8 @@ def run_ours(args):
                "sample": f"{len(cpu_names)} params ({cpu_names[0]} .. {cpu_names[-1]}), "
                          f"{S_cpu / GB:.2f} GB state: oracle union + extract_fragment "
                          f"(materialised), {args.cpu_threads} threads, one pass"}
+      except Exception as exc:  # rank 0 only: no collective to skip
+        cpu = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:300]}
 
     emit({"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
