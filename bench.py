@@ -410,8 +410,9 @@ def run_ours(args):
     except RuntimeError:
         live = None
     roofline["live_copy_GBps_same_run"] = live
-    if live:
-        roofline["frac_of_live_copy"] = achieved / live
+    roofline["live_copy_note"] = ("torch copy_ of 2 x 2 GiB in this process right after the timed "
+                                  "region (same clocks / power state); context only, the roofline "
+                                  "denominator is MEASURED_PEAKS.json")
 
     # ---- e2e: host-streamed sample, H2D + kernels + D2H in the timed region
     e2e = None
