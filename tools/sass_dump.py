@@ -13,13 +13,15 @@ funcs = re.split(r"\n\s*Function : ", txt)
 out = []
 for f in funcs[1:]:
     name = f.split("\n", 1)[0].strip()
-    m = re.search(r"(convert_gather_\w+?|load_scatter_\w+?|gen_state_kernel|compare_kernel)E", name)
+    m = re.search(r"(convert_gather_\w+?|load_scatter_\w+?|reshard_fused_\w+?|adam_step_kernel|"
+                  r"gen_state_kernel|compare_kernel)E", name)
     short = m.group(1) if m else name
     body = f
     mix = {k: len(re.findall(k, body)) for k in (r"LDG\.E\.NA\.128", r"LDG\.E\.128", r"STG\.E\.128",
                                                  r"STG\.E\.64", r"\bSTL\b", r"\bLDL\b", r"DADD", r"DMUL")}
     out.append((short, mix))
-    if any(k in name for k in ("convert_gather_f32", "load_scatter_bf16")):
+    if any(k in name for k in ("convert_gather_f32", "load_scatter_bf16", "reshard_fused_f32",
+                               "reshard_fused_bf16")):
         with open(f"profiles/sass_{short}_{tag}.txt", "w") as fh:
             fh.write("Function : " + f)
 for n, m in out:
