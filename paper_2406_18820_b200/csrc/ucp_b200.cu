@@ -562,16 +562,19 @@ __device__ __forceinline__ void fused_tile(const ucp_xrun* __restrict__ runs,
                                            const ucp_tile& tile, ucp_xrun& s_run,
                                            uint64_t* s_aux,
                                            const char* __restrict__ sb, char* __restrict__ ab,
-                                           char* __restrict__ db, ucp_status* st) {
+                                           char* __restrict__ db, ucp_status* st,
+                                           bool preloaded = false) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  if (threadIdx.x < 4) {
-    reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
-        reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
+  if (!preloaded) {
+    if (threadIdx.x < 4) {
+      reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
+          reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int ns = s_run.n_src, nd = s_run.n_dst;
   const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
-  if (n_aux > 0) {
+  if (n_aux > 0 && !preloaded) {
     for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
     __syncthreads();
   }
@@ -652,6 +655,124 @@ __device__ __forceinline__ void fused_tile(const ucp_xrun* __restrict__ runs,
   }
 }
 
+
+#ifndef UCP_FUSED_TMA
+#define UCP_FUSED_TMA 0  // 1: f32 fused tiles move through shared memory with TMA bulk copies
+#endif
+
+#if UCP_FUSED_TMA
+// ------------------------------------------------------------- TMA bulk path
+// Experiment: aligned f32 fused tiles go global -> smem with
+// cp.async.bulk (mbarrier complete_tx), replicas are compared from smem, and
+// smem -> global with cp.async.bulk stores to the atomic and every target.
+constexpr int kTmaCh = 2048;   // floats per chunk (8 KB)
+constexpr int kTmaMaxK = 4;    // replicas staged per chunk
+constexpr int kTmaSmem = 2 * kTmaMaxK * kTmaCh * 4 + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+               "r"(smem_u32(smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// returns false when the tile is not eligible (caller falls back to LDG)
+__device__ __forceinline__ bool fused_tile_tma(const ucp_xrun& r, const uint64_t* s_aux,
+                                               const ucp_tile& tile, const char* __restrict__ sb,
+                                               char* __restrict__ ab, char* __restrict__ db,
+                                               ucp_status* st, float* buf, uint64_t* bars,
+                                               uint32_t& uses) {
+  const int ns = r.n_src, nd = r.n_dst;
+  if (ns < 1 || ns > kTmaMaxK || r.dtype != UCP_DT_F32) return false;
+  const bool atom_on = r.atom != ~0ull;
+  uint64_t orr = r.src | r.dst | (atom_on ? r.atom : 0);
+  for (int i = 0; i < ns - 1 + (nd > 0 ? nd - 1 : 0); ++i) orr |= s_aux[i];
+  const bool rowsplit = r.flags & UCP_RUN_ROWSPLIT;
+  const uint32_t nr = rowsplit ? 1 : tile.count, nc = rowsplit ? tile.count : r.cols;
+  if ((orr & 15) || (nc & 3) || (tile.col0 & 3) ||
+      (nr > 1 && ((r.src_pitch | r.dst_pitch | r.atom_pitch) & 3)))
+    return false;
+  const uint32_t cpr = (nc + kTmaCh - 1) / kTmaCh, n_chunks = nr * cpr;
+  const int tid = threadIdx.x;
+  auto span = [&](uint32_t c, uint32_t& row, uint32_t& col, uint32_t& n) {
+    const uint32_t rr = c / cpr;
+    row = tile.row0 + rr;
+    col = tile.col0 + (c - rr * cpr) * kTmaCh;
+    n = min((uint32_t)kTmaCh, tile.col0 + nc - col);
+  };
+  auto stage = [&](uint32_t s, int k) { return buf + ((size_t)s * kTmaMaxK + k) * kTmaCh; };
+  auto issue = [&](uint32_t c) {
+    uint32_t row, col, n;
+    span(c, row, col, n);
+    const uint32_t s = (uses + c) & 1;
+    mbar_expect_tx(&bars[s], (uint32_t)ns * n * 4);
+    for (int k = 0; k < ns; ++k) {
+      const char* src = sb + (k == 0 ? r.src : s_aux[k - 1]) + 4ull * ((uint64_t)row * r.src_pitch + col);
+      bulk_load(stage(s, k), src, n * 4, &bars[s]);
+    }
+  };
+  if (tid == 0 && n_chunks) issue(0);
+  for (uint32_t c = 0; c < n_chunks; ++c) {
+    const uint32_t g = uses + c, s = g & 1;
+    if (tid == 0 && c + 1 < n_chunks) {
+      bulk_wait_read0();  // stores of the previous chunk no longer read stage (g+1)&1
+      issue(c + 1);
+    }
+    mbar_wait(&bars[s], (g >> 1) & 1);
+    uint32_t row, col, n;
+    span(c, row, col, n);
+    bool bad = false;
+    uint32_t bad_e = 0xffffffffu;
+    if (ns > 1) {
+      const float4* p0 = reinterpret_cast<const float4*>(stage(s, 0));
+      for (uint32_t v = tid; v < n / 4; v += kThreads) {
+        const float4 x = p0[v];
+        for (int k = 1; k < ns; ++k) {
+          const int d = diff4(x, reinterpret_cast<const float4*>(stage(s, k))[v]);
+          if (d < 4) { bad = true; bad_e = min(bad_e, 4 * v + d); }
+        }
+      }
+    }
+    report(bad, row * r.cols + col + bad_e, tile.run, st);
+    __syncthreads();  // every thread is done reading stage s before it is refilled
+    if (tid == 0) {
+      if (atom_on) bulk_store(ab + r.atom + 4ull * ((uint64_t)row * r.atom_pitch + col), stage(s, 0), n * 4);
+      for (int d = 0; d < nd; ++d)
+        bulk_store(db + (d == 0 ? r.dst : s_aux[ns - 1 + d - 1]) +
+                       4ull * ((uint64_t)row * r.dst_pitch + col), stage(s, 0), n * 4);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_read0();
+  uses += n_chunks;
+  __syncthreads();
+  return true;
+}
+#endif
+
 template <int DT>
 __device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
                                            const uint64_t* __restrict__ aux,
@@ -667,6 +788,28 @@ __device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
     fused_tile<DT>(runs, aux, tile, s_run, s_aux, sb, ab, db, st);
     __syncthreads();
   }
+#elif UCP_FUSED_TMA
+  (void)n_tiles;
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  float* buf = reinterpret_cast<float*>(dyn_smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dyn_smem + 2 * kTmaMaxK * kTmaCh * 4);
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const ucp_tile tile = tiles[blockIdx.x];
+  if (threadIdx.x < 4) {
+    reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
+        reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
+  }
+  __syncthreads();
+  const int n_aux = (s_run.n_src > 0 ? s_run.n_src - 1 : 0) + (s_run.n_dst > 0 ? s_run.n_dst - 1 : 0);
+  for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
+  __syncthreads();
+  uint32_t uses = 0;
+  if (DT != UCP_DT_F32 || !fused_tile_tma(s_run, s_aux, tile, sb, ab, db, st, buf, bars, uses))
+    fused_tile<DT>(runs, aux, tile, s_run, s_aux, sb, ab, db, st, true);
 #else
   (void)n_tiles;
   const ucp_tile tile = tiles[blockIdx.x];
@@ -894,9 +1037,21 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
     const dim3 grid(g), block(kThreads);
     const ucp_tile* t = tiles + at;
     const uint32_t nt = (uint32_t)n;
-    if (c == UCP_CLASS_VEC_F32) reshard_fused_f32<<<grid, block, 0, s>>>(runs, aux, t, nt, sb, ab, db, status);
-    else if (c == UCP_CLASS_VEC_BF16) reshard_fused_bf16<<<grid, block, 0, s>>>(runs, aux, t, nt, sb, ab, db, status);
-    else reshard_fused_f16<<<grid, block, 0, s>>>(runs, aux, t, nt, sb, ab, db, status);
+#if UCP_FUSED_TMA
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(reshard_fused_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      cudaFuncSetAttribute(reshard_fused_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      cudaFuncSetAttribute(reshard_fused_f16, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      attr_set = true;
+    }
+    const size_t dsm = kTmaSmem;
+#else
+    const size_t dsm = 0;
+#endif
+    if (c == UCP_CLASS_VEC_F32) reshard_fused_f32<<<grid, block, dsm, s>>>(runs, aux, t, nt, sb, ab, db, status);
+    else if (c == UCP_CLASS_VEC_BF16) reshard_fused_bf16<<<grid, block, dsm, s>>>(runs, aux, t, nt, sb, ab, db, status);
+    else reshard_fused_f16<<<grid, block, dsm, s>>>(runs, aux, t, nt, sb, ab, db, status);
     at += n;
   }
   return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
