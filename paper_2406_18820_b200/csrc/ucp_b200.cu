@@ -665,9 +665,16 @@ __device__ __forceinline__ void fused_tile(const ucp_xrun* __restrict__ runs,
 // Experiment: aligned f32 fused tiles go global -> smem with
 // cp.async.bulk (mbarrier complete_tx), replicas are compared from smem, and
 // smem -> global with cp.async.bulk stores to the atomic and every target.
-constexpr int kTmaCh = 2048;   // floats per chunk (8 KB)
-constexpr int kTmaMaxK = 4;    // replicas staged per chunk
-constexpr int kTmaSmem = 2 * kTmaMaxK * kTmaCh * 4 + 64;
+#ifndef UCP_TMA_STAGES
+#define UCP_TMA_STAGES 2
+#endif
+#ifndef UCP_TMA_CH
+#define UCP_TMA_CH 2048
+#endif
+constexpr int kTmaCh = UCP_TMA_CH;        // floats per chunk
+constexpr int kTmaMaxK = 4;               // replicas staged per chunk
+constexpr int kTmaStages = UCP_TMA_STAGES;
+constexpr int kTmaSmem = kTmaStages * kTmaMaxK * kTmaCh * 4 + 8 * kTmaStages;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -727,21 +734,22 @@ __device__ __forceinline__ bool fused_tile_tma(const ucp_xrun& r, const uint64_t
   auto issue = [&](uint32_t c) {
     uint32_t row, col, n;
     span(c, row, col, n);
-    const uint32_t s = (uses + c) & 1;
+    const uint32_t s = (uses + c) % kTmaStages;
     mbar_expect_tx(&bars[s], (uint32_t)ns * n * 4);
     for (int k = 0; k < ns; ++k) {
       const char* src = sb + (k == 0 ? r.src : s_aux[k - 1]) + 4ull * ((uint64_t)row * r.src_pitch + col);
       bulk_load(stage(s, k), src, n * 4, &bars[s]);
     }
   };
-  if (tid == 0 && n_chunks) issue(0);
+  if (tid == 0)
+    for (uint32_t c = 0; c + 1 < (uint32_t)kTmaStages && c < n_chunks; ++c) issue(c);
   for (uint32_t c = 0; c < n_chunks; ++c) {
-    const uint32_t g = uses + c, s = g & 1;
-    if (tid == 0 && c + 1 < n_chunks) {
-      bulk_wait_read0();  // stores of the previous chunk no longer read stage (g+1)&1
-      issue(c + 1);
+    const uint32_t g = uses + c, s = g % kTmaStages;
+    if (tid == 0 && c + kTmaStages - 1 < n_chunks) {
+      bulk_wait_read0();  // stores of chunk c-1 no longer read the stage being refilled
+      issue(c + kTmaStages - 1);
     }
-    mbar_wait(&bars[s], (g >> 1) & 1);
+    mbar_wait(&bars[s], (g / kTmaStages) & 1);
     uint32_t row, col, n;
     span(c, row, col, n);
     bool bad = false;
@@ -792,10 +800,9 @@ __device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
   (void)n_tiles;
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   float* buf = reinterpret_cast<float*>(dyn_smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dyn_smem + 2 * kTmaMaxK * kTmaCh * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dyn_smem + kTmaStages * kTmaMaxK * kTmaCh * 4);
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < kTmaStages; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const ucp_tile tile = tiles[blockIdx.x];
