@@ -457,23 +457,9 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, gather: bool, emit) -
 # --------------------------------------------------------------------------- convert
 
 
-def convert(src: str, out_dir: str, n_workers: int = 1, inner: int = 1,
-            strict_replicate: bool = True, *, device=None,
-            window_bytes: int = DEFAULT_WINDOW_BYTES) -> AtomicCheckpoint:
-    """Distributed checkpoint -> atomic checkpoint (ucp/convert.py:422-563).
-    Output bytes do not depend on n_workers/inner (they only size the file
-    I/O thread pool)."""
-    global INVOCATIONS
-    INVOCATIONS += 1
-    if n_workers < 1 or inner < 1:
-        raise ValueError("n_workers and inner must be >= 1")
-    ckpt = codec.load_checkpoint(src)
-    spec, cfg = ckpt.spec, ckpt.cfg
-    fingerprint = source_fingerprint(src)
-    dev = require_device(device)
-    codec.ensure_empty_dir(out_dir)
-
-    # mapper phase: manifests, stray/missing files, headers (ucp/convert.py:86-107)
+def _mapper_phase(ckpt, spec: ModelSpec, cfg: ParallelConfig) -> dict:
+    """Manifests, stray/missing files and headers of every rank dir
+    (ucp/convert.py:86-107): {(param, kind): [(meta, path, header)]}."""
     units = defaultdict(list)
     names = {p.name for p in spec.params}
     for g in range(cfg.world_size):
@@ -499,6 +485,27 @@ def convert(src: str, out_dir: str, n_workers: int = 1, inner: int = 1,
     missing = [p.name for p in spec.params if not any((p.name, k) in units for k in STATE_KINDS)]
     if missing:
         raise MissingFragmentError(f"no fragments at all for params {missing[:3]}")
+
+    return units
+
+
+def convert(src: str, out_dir: str, n_workers: int = 1, inner: int = 1,
+            strict_replicate: bool = True, *, device=None,
+            window_bytes: int = DEFAULT_WINDOW_BYTES) -> AtomicCheckpoint:
+    """Distributed checkpoint -> atomic checkpoint (ucp/convert.py:422-563).
+    Output bytes do not depend on n_workers/inner (they only size the file
+    I/O thread pool)."""
+    global INVOCATIONS
+    INVOCATIONS += 1
+    if n_workers < 1 or inner < 1:
+        raise ValueError("n_workers and inner must be >= 1")
+    ckpt = codec.load_checkpoint(src)
+    spec, cfg = ckpt.spec, ckpt.cfg
+    fingerprint = source_fingerprint(src)
+    dev = require_device(device)
+    codec.ensure_empty_dir(out_dir)
+
+    units = _mapper_phase(ckpt, spec, cfg)
 
     def src_size(p):
         return sum(align_up(h.nbytes) for k in STATE_KINDS for _, _, h in units.get((p.name, k), ()))
@@ -661,9 +668,17 @@ def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass
 
 
 def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1, inner: int = 1,
-           dtype: DType = DType.F32, bypass: bool = True) -> LoadedWorld:
+           dtype: DType = DType.F32, bypass: bool = True, *, device=None,
+           fused: bool = True, window_bytes: int = DEFAULT_WINDOW_BYTES) -> LoadedWorld:
     """Reload a distributed checkpoint under tgt (ucp/load.py:231-281): lazy
-    direct read when the layouts match, else convert into scratch + load."""
+    direct read when the layouts match, else convert into scratch + load.
+
+    With ``fused`` (default) the convert + load pair runs as one pass over
+    the source files: the fused kernel writes the atomic
+    tensors (saved to ``scratch/atomic`` exactly as convert() would) and the
+    target shards from the same registers, so the atomic tree is never read
+    back. Observable results (world, stats, scratch tree, conversion count)
+    equal the two-pass path."""
     src = codec.load_checkpoint(src_root)
     validate_model_config(src.spec, tgt)
     before = INVOCATIONS
@@ -692,10 +707,136 @@ def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1,
         return LoadedWorld(tgt, src.spec, src.step, dict(src.metadata), shards, stats)
     os.makedirs(scratch, exist_ok=True)
     atomic_dir = os.path.join(scratch, "atomic")
-    convert(src_root, atomic_dir, n_workers=n_workers, inner=inner)
-    world = load(atomic_dir, tgt, dtype=dtype, bypass=bypass)
+    if fused:
+        world = _resume_fused(src_root, atomic_dir, tgt, dtype, bypass, n_workers, device,
+                              window_bytes)
+    else:
+        convert(src_root, atomic_dir, n_workers=n_workers, inner=inner, device=device,
+                window_bytes=window_bytes)
+        world = load(atomic_dir, tgt, dtype=dtype, bypass=bypass, device=device,
+                     window_bytes=window_bytes)
     world.stats.conversions_invoked = INVOCATIONS - before
     return world
+
+
+def _resume_fused(src_root: str, atomic_dir: str, tgt: ParallelConfig, dtype: DType,
+                  bypass: bool, n_workers: int, device, window_bytes: int) -> LoadedWorld:
+    """convert(src_root, atomic_dir) + load(atomic_dir, tgt) in one pass."""
+    from .engine import XProgram, describe_failure
+    from .plan import XRunTable, compile_fused
+
+    global INVOCATIONS
+    INVOCATIONS += 1  # this is a conversion (ucp/convert.py:435-436)
+    ckpt = codec.load_checkpoint(src_root)
+    spec, cfg = ckpt.spec, ckpt.cfg
+    fingerprint = source_fingerprint(src_root)
+    dev = require_device(device)
+    codec.ensure_empty_dir(atomic_dir)
+    units = _mapper_phase(ckpt, spec, cfg)
+    validate_model_config(spec, tgt)
+    info = ucp_info(spec, tgt)
+    tgt_units = defaultdict(list)
+    for g in range(tgt.world_size):
+        for i, m in enumerate(info.records[g]):
+            tgt_units[(m.param, m.kind)].append((g, i, m))
+
+    def out_dtype(kind):
+        return dtype if kind == "weight" else DType.F32
+
+    def size(p):
+        b = 0
+        for k in STATE_KINDS:
+            b += sum(align_up(h.nbytes) for _, _, h in units.get((p.name, k), ()))
+            b += 2 * align_up(4 * p.numel)
+            b += sum(align_up(fragment_elems(p, tgt, m) * out_dtype(k).itemsize)
+                     for _, _, m in tgt_units.get((p.name, k), ()))
+        return b
+
+    wins, outs_all, total = [], [], 0
+    for wparams in _windows(list(spec.params), size, window_bytes):
+        fx, rc, rl = XRunTable(), RunTable(), RunTable()
+        jobs, s_at, a_at, t_at, atoms, outs = [], 0, 0, 0, [], []
+        for p in wparams:
+            for kind in STATE_KINDS:
+                items = units.get((p.name, kind))
+                if not items:
+                    raise MissingFragmentError(f"{p.name}.{kind}: no fragments arrived")
+                frags = []
+                for meta, path, hdr in items:
+                    jobs.append((path, hdr, s_at))
+                    frags.append((meta, s_at, hdr.numel))
+                    s_at += align_up(hdr.nbytes)
+                odt = out_dtype(kind)
+                targets = []
+                for g, i, m in tgt_units.get((p.name, kind), ()):
+                    n = fragment_elems(p, tgt, m)
+                    targets.append((m, t_at))
+                    o = (g, i, m, odt, t_at, n, fragment_shape(p, tgt, m), total)
+                    outs.append(o)
+                    outs_all.append(o)
+                    total += align_up(n * odt.itemsize, 16)
+                    t_at += align_up(n * odt.itemsize)
+                compile_fused(fx, rc, rl, p, cfg, frags, a_at, tgt, targets, odt, True)
+                atoms.append((p, kind, a_at))
+                a_at += align_up(4 * p.numel)
+        wins.append((XProgram(fx, dev), Program(rc, dev), Program(rl, dev), jobs, s_at, a_at,
+                     t_at, atoms, outs))
+    host = np.empty(max(total, 1), dtype=np.uint8)
+    ms = max((w[4] for w in wins), default=0)
+    ma = max((w[5] for w in wins), default=0)
+    mt = max((w[6] for w in wins), default=0)
+    h_src = _STAGE.host_buf("res_src", ms)
+    h_atom = _STAGE.host_buf("res_atom", ma)
+    h_tgt = _STAGE.host_buf("res_tgt", mt)
+    d_src = _STAGE.dev_buf("res_src", ms, dev)
+    d_atom = _STAGE.dev_buf("res_atom", ma, dev)
+    d_tgt = _STAGE.dev_buf("res_tgt", mt, dev)
+    st = _status(dev)
+    nthreads = max(4, min(32, 2 * n_workers, os.cpu_count() or 4))
+    with ThreadPoolExecutor(nthreads) as pool:
+        for fprog, cprog, lprog, jobs, s_at, a_at, t_at, atoms, outs in wins:
+            hv = memoryview(h_src.numpy())
+            list(pool.map(lambda j: codec.read_payload_into(j[0], j[1], hv[j[2]:j[2] + j[1].nbytes]),
+                          jobs))
+            d_src[:s_at].copy_(h_src[:s_at], non_blocking=True)
+            st.reset()
+            fprog.launch(d_src.data_ptr(), d_atom.data_ptr(), d_tgt.data_ptr(), st)
+            cprog.launch(True, d_src.data_ptr(), d_atom.data_ptr(), st)
+            lprog.launch(False, d_atom.data_ptr(), d_tgt.data_ptr(), st)
+            h_atom[:a_at].copy_(d_atom[:a_at], non_blocking=True)
+            h_tgt[:t_at].copy_(d_tgt[:t_at], non_blocking=True)
+            torch.cuda.synchronize(dev)
+            first, _ = st.read()
+            if first != (1 << 64) - 1:  # localise: re-run the source-reading launches
+                for prog in (fprog, cprog):
+                    st.reset()
+                    if prog is fprog:
+                        prog.launch(d_src.data_ptr(), d_atom.data_ptr(), d_tgt.data_ptr(), st)
+                    else:
+                        prog.launch(True, d_src.data_ptr(), d_atom.data_ptr(), st)
+                    torch.cuda.synchronize(dev)
+                    f, _ = st.read()
+                    if f != (1 << 64) - 1:
+                        raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, d_src.data_ptr())
+                raise RuntimeError("fused resume reported a failure that did not reproduce")
+            av, tv = memoryview(h_atom.numpy()), h_tgt.numpy()
+            list(pool.map(lambda o: _write_atomic(atomic_dir, o, av), atoms))
+            for g, i, m, odt, at, n, shape, g_at in outs:
+                host[g_at:g_at + n * odt.itemsize] = tv[at:at + n * odt.itemsize]
+    with open(os.path.join(atomic_dir, codec.MODEL_JSON), "w") as f:
+        f.write(spec_to_json(spec))
+    codec.write_json(os.path.join(atomic_dir, UCP_META_JSON), {
+        "format_version": FORMAT_VERSION, "step": ckpt.step, "metadata": ckpt.metadata,
+        "source_config_sha256": fingerprint})
+    atomic = load_atomic(atomic_dir)
+    stats = _load_stats(atomic, spec, tgt, bypass)
+    filled = {}
+    for g, i, m, odt, at, n, shape, g_at in outs_all:
+        filled[(g, i)] = Tensor(odt, tuple(shape),
+                                host[g_at:g_at + n * odt.itemsize].view(odt.storage).reshape(shape))
+    shards = {g: [WorldShard(m, filled[(g, i)]) for i, m in enumerate(info.records[g])]
+              for g in range(tgt.world_size)}
+    return LoadedWorld(tgt, spec, atomic.step, dict(atomic.metadata), shards, stats)
 
 
 # --------------------------------------------------------------------------- save side

@@ -463,3 +463,39 @@ def test_union_is_reentrant_across_threads():
 
     with ThreadPoolExecutor(8) as pool:
         assert all(pool.map(one, list(units) * 3))
+
+
+@pytest.mark.parametrize("name", ["gqa", "moe", "pad", "DenseGPT.1", "MoE.3", "GQA.4"])
+def test_fused_resume_equals_two_pass(golden, tmp_path, name):
+    row = next(r for r in golden["pipelines"] if r["name"] == name)
+    spec = cell_spec(golden, row)
+    src_cfg, tgt_cfg = cell_cfgs(row)
+    src, _ = _src_tree(tmp_path, spec, src_cfg)
+    for dt in (DType.F32, DType.BF16):
+        worlds = []
+        for fused in (True, False):
+            scratch = str(tmp_path / f"scratch_{fused}_{dt.name}")
+            before = U.conversions_invoked()
+            w = U.resume(src, tgt_cfg, scratch, dtype=dt, fused=fused, window_bytes=1 << 16)
+            assert U.conversions_invoked() == before + 1 and w.stats.conversions_invoked == 1
+            assert O.dir_digest(scratch + "/atomic") == row["atomic_digest"]
+            worlds.append(w)
+        for w in worlds:
+            wd = {g: [(s.meta, s.tensor.data) for s in w.shards[g]] for g in w.shards}
+            assert O.world_digest(wd) == row[f"world_{dt.name}"], (name, dt)
+        assert worlds[0].stats.to_dict() == worlds[1].stats.to_dict()
+
+
+def test_fused_resume_replica_fault_is_torn(tmp_path):
+    spec = U.make_model("GQA", {"n_layers": 4, "hidden": 64, "q_heads": 8, "kv_heads": 2})
+    src, _ = _src_tree(tmp_path, spec, cfg(dp=2, zero="z1"))
+    victim = os.path.join(src, "rank_1", "layers.2.attn_qkv.weight.ucpt")
+    t = codec.read_tensor(victim)
+    bad = t.data.copy()
+    bad.reshape(-1)[100] = np.float32(5.0)
+    codec.write_tensor(victim, U.Tensor(t.dtype, t.shape, bad))
+    scratch = str(tmp_path / "scratch")
+    with pytest.raises(U.ReplicateMismatchError) as ei:
+        U.resume(src, cfg(tp=2, dp=2, zero="z1"), scratch)
+    assert "layers.2.attn_qkv.weight" in str(ei.value)
+    assert not os.path.exists(os.path.join(scratch, "atomic", "ucp_meta.json"))
