@@ -55,12 +55,24 @@ def main():
         load.append(time.perf_counter() - t)
         del world
         shutil.rmtree(out)
+    res = {True: [], False: []}
+    for r in range(args.reps + 1):
+        for fused in (True, False):
+            scratch = os.path.join(args.root, f"scratch{r}{int(fused)}")
+            t = time.perf_counter()
+            world = U.resume(src_dir, tgt, scratch, n_workers=args.workers, fused=fused)
+            res[fused].append(time.perf_counter() - t)
+            del world
+            shutil.rmtree(scratch)
     c, lo = min(conv[1:]), min(load[1:])
+    rf, ru = min(res[True][1:]), min(res[False][1:])
     print(json.dumps({
         "workload": desc, "config": args.config, "state_bytes": S, "root": args.root,
         "workers": args.workers, "partition_s": t_part,
         "convert_s": c, "convert_GBps": S / c / 1e9, "load_s": lo, "load_GBps": S / lo / 1e9,
         "convert_plus_load_GBps": S / (c + lo) / 1e9, "reps": args.reps,
+        "resume_fused_s": rf, "resume_fused_GBps": S / rf / 1e9,
+        "resume_two_pass_s": ru, "resume_two_pass_GBps": S / ru / 1e9,
         "all_convert_s": conv, "all_load_s": load}))
     shutil.rmtree(args.root, ignore_errors=True)
 
