@@ -390,16 +390,66 @@ def _write_atomic(out_dir: str, o, ov: memoryview) -> None:
                     ov[at:at + 4 * p.numel])
 
 
-def _pipeline(wplans: list, dev, key: str, n_workers: int, gather: bool, emit) -> None:
+class _Step:
+    """One window's device work in ``_pipeline``: a single convert_gather or
+    load_scatter launch over (src arena, dst arena)."""
+
+    def __init__(self, prog: Program, gather: bool):
+        self.prog, self.gather = prog, gather
+
+    def launch(self, src: int, dst: int, st, stream) -> None:
+        self.prog.launch(self.gather, src, dst, st, stream)
+
+    def check(self, st, src: int, dst: int, stream) -> None:
+        st.raise_if_bad(self.prog, src)
+
+
+class _FusedStep:
+    """One fused-resume window: the ucp_reshard_fused launch plus the rest
+    tables (units compile_fused could not overlay), over one dst arena that
+    holds the atomic tensors at [0, atom_at) and the target shards from
+    atom_at on, so a single D2H drains both."""
+
+    def __init__(self, fprog, cprog: Program, lprog: Program, atom_at: int):
+        self.fprog, self.cprog, self.lprog, self.atom_at = fprog, cprog, lprog, atom_at
+
+    def launch(self, src: int, dst: int, st, stream) -> None:
+        self.fprog.launch(src, dst, dst + self.atom_at, st, stream)
+        self.cprog.launch(True, src, dst, st, stream)
+        self.lprog.launch(False, dst, dst + self.atom_at, st, stream)
+
+    def check(self, st, src: int, dst: int, stream) -> None:
+        from .engine import describe_failure
+
+        first, _ = st.read()
+        if first == (1 << 64) - 1:
+            return
+        # localise: re-run the source-reading launches one at a time (the load
+        # of atomic tensors cannot fail, it only reads what the others wrote)
+        for prog in (self.fprog, self.cprog):
+            st.reset(stream)
+            if prog is self.fprog:
+                prog.launch(src, dst, dst + self.atom_at, st, stream)
+            else:
+                prog.launch(True, src, dst, st, stream)
+            stream.synchronize()
+            f, _ = st.read()
+            if f != (1 << 64) - 1:
+                raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, src)
+        raise RuntimeError("fused resume reported a failure that did not reproduce")
+
+
+def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
     """Windowed file pipeline, double-buffered so file reads of window w+1
     and the output handling of window w-1 overlap the GPU work of window w:
 
-        read files (thread pool) -> pinned -> H2D -> kernel -> D2H -> pinned
+        read files (thread pool) -> pinned -> H2D -> kernel(s) -> D2H -> pinned
         -> emit(o, view) per output (thread pool)
 
-    wplans: [(Program, read jobs (path, header, offset), src bytes, outs,
-    dst bytes)]. Data-dependent failures raise after their window syncs, so
-    a failing window never reaches emit (torn output, ucp/convert.py:503)."""
+    wplans: [(step, read jobs (path, header, offset), src bytes, outs, dst
+    bytes)] with step a _Step/_FusedStep. Data-dependent failures raise after
+    their window syncs, so a failing window never reaches emit (torn output,
+    ucp/convert.py:503)."""
     if not wplans:
         return
     ms = max(w[2] for w in wplans)
@@ -422,7 +472,7 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, gather: bool, emit) -
         written: dict = {}
         h2d_ev: dict = {}
         try:
-            for w, (prog, _, s_at, outs, d_at) in enumerate(wplans):
+            for w, (step, _, s_at, outs, d_at) in enumerate(wplans):
                 slot = w % 2
                 for f in pending.pop(w):
                     f.result()
@@ -430,7 +480,7 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, gather: bool, emit) -
                 h2d_ev[w] = torch.cuda.Event()
                 h2d_ev[w].record(stream)
                 st.reset(stream)
-                prog.launch(gather, d_src[slot].data_ptr(), d_dst[slot].data_ptr(), st, stream)
+                step.launch(d_src[slot].data_ptr(), d_dst[slot].data_ptr(), st, stream)
                 for f in written.pop(w - 2, ()):  # h_dst[slot] is free again
                     f.result()
                 h_dst[slot][:d_at].copy_(d_dst[slot][:d_at], non_blocking=True)
@@ -441,7 +491,7 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, gather: bool, emit) -
                         h2d_ev.pop(w - 1).synchronize()  # h_src[(w+1)%2] drained
                     pending[w + 1] = reads(w + 1)
                 done.synchronize()
-                st.raise_if_bad(prog, d_src[slot].data_ptr())
+                step.check(st, d_src[slot].data_ptr(), d_dst[slot].data_ptr(), stream)
                 ov = memoryview(h_dst[slot].numpy())
                 written[w] = [wpool.submit(emit, o, ov) for o in outs]
             for fs in written.values():
@@ -530,8 +580,8 @@ def convert(src: str, out_dir: str, n_workers: int = 1, inner: int = 1,
                 compile_union(tab, p, cfg, frags, a_at, strict_replicate)
                 outs.append((p, kind, a_at))
                 a_at += align_up(4 * p.numel)
-        wplans.append((Program(tab, dev), jobs, s_at, outs, a_at))
-    _pipeline(wplans, dev, "conv", n_workers, True, lambda o, ov: _write_atomic(out_dir, o, ov))
+        wplans.append((_Step(Program(tab, dev), True), jobs, s_at, outs, a_at))
+    _pipeline(wplans, dev, "conv", n_workers, lambda o, ov: _write_atomic(out_dir, o, ov))
 
     with open(os.path.join(out_dir, codec.MODEL_JSON), "w") as f:
         f.write(spec_to_json(spec))
@@ -646,7 +696,7 @@ def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass
                     t_at += align_up(n * odt.itemsize)
                 compile_extract(tab, p, tgt, targets, s_at, odt)
                 s_at += align_up(hdr.nbytes)
-        wplans.append((Program(tab, dev), jobs, s_at, outs, t_at))
+        wplans.append((_Step(Program(tab, dev), False), jobs, s_at, outs, t_at))
     host = np.empty(max(total, 1), dtype=np.uint8)
 
     def emit(o, ov):
@@ -654,7 +704,7 @@ def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass
         host[g_at:g_at + n * odt.itemsize] = np.frombuffer(ov, dtype=np.uint8, count=n * odt.itemsize,
                                                            offset=at)
 
-    _pipeline(wplans, dev, "load", 4, False, emit)
+    _pipeline(wplans, dev, "load", 4, emit)
     filled = {}
     for g, i, m, odt, at, n, shape, g_at in outs_all:
         arr = host[g_at:g_at + n * odt.itemsize].view(odt.storage).reshape(shape)
@@ -722,7 +772,7 @@ def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1,
 def _resume_fused(src_root: str, atomic_dir: str, tgt: ParallelConfig, dtype: DType,
                   bypass: bool, n_workers: int, device, window_bytes: int) -> LoadedWorld:
     """convert(src_root, atomic_dir) + load(atomic_dir, tgt) in one pass."""
-    from .engine import XProgram, describe_failure
+    from .engine import XProgram
     from .plan import XRunTable, compile_fused
 
     global INVOCATIONS
@@ -747,7 +797,7 @@ def _resume_fused(src_root: str, atomic_dir: str, tgt: ParallelConfig, dtype: DT
         b = 0
         for k in STATE_KINDS:
             b += sum(align_up(h.nbytes) for _, _, h in units.get((p.name, k), ()))
-            b += 2 * align_up(4 * p.numel)
+            b += align_up(4 * p.numel)
             b += sum(align_up(fragment_elems(p, tgt, m) * out_dtype(k).itemsize)
                      for _, _, m in tgt_units.get((p.name, k), ()))
         return b
@@ -779,50 +829,21 @@ def _resume_fused(src_root: str, atomic_dir: str, tgt: ParallelConfig, dtype: DT
                 compile_fused(fx, rc, rl, p, cfg, frags, a_at, tgt, targets, odt, True)
                 atoms.append((p, kind, a_at))
                 a_at += align_up(4 * p.numel)
-        wins.append((XProgram(fx, dev), Program(rc, dev), Program(rl, dev), jobs, s_at, a_at,
-                     t_at, atoms, outs))
+        wouts = [("a", o) for o in atoms] + [("t", o[:7] + (a_at + o[4],) + o[7:]) for o in outs]
+        wins.append((_FusedStep(XProgram(fx, dev), Program(rc, dev), Program(rl, dev), a_at),
+                     jobs, s_at, wouts, a_at + t_at))
     host = np.empty(max(total, 1), dtype=np.uint8)
-    ms = max((w[4] for w in wins), default=0)
-    ma = max((w[5] for w in wins), default=0)
-    mt = max((w[6] for w in wins), default=0)
-    h_src = _STAGE.host_buf("res_src", ms)
-    h_atom = _STAGE.host_buf("res_atom", ma)
-    h_tgt = _STAGE.host_buf("res_tgt", mt)
-    d_src = _STAGE.dev_buf("res_src", ms, dev)
-    d_atom = _STAGE.dev_buf("res_atom", ma, dev)
-    d_tgt = _STAGE.dev_buf("res_tgt", mt, dev)
-    st = _status(dev)
-    nthreads = max(4, min(32, 2 * n_workers, os.cpu_count() or 4))
-    with ThreadPoolExecutor(nthreads) as pool:
-        for fprog, cprog, lprog, jobs, s_at, a_at, t_at, atoms, outs in wins:
-            hv = memoryview(h_src.numpy())
-            list(pool.map(lambda j: codec.read_payload_into(j[0], j[1], hv[j[2]:j[2] + j[1].nbytes]),
-                          jobs))
-            d_src[:s_at].copy_(h_src[:s_at], non_blocking=True)
-            st.reset()
-            fprog.launch(d_src.data_ptr(), d_atom.data_ptr(), d_tgt.data_ptr(), st)
-            cprog.launch(True, d_src.data_ptr(), d_atom.data_ptr(), st)
-            lprog.launch(False, d_atom.data_ptr(), d_tgt.data_ptr(), st)
-            h_atom[:a_at].copy_(d_atom[:a_at], non_blocking=True)
-            h_tgt[:t_at].copy_(d_tgt[:t_at], non_blocking=True)
-            torch.cuda.synchronize(dev)
-            first, _ = st.read()
-            if first != (1 << 64) - 1:  # localise: re-run the source-reading launches
-                for prog in (fprog, cprog):
-                    st.reset()
-                    if prog is fprog:
-                        prog.launch(d_src.data_ptr(), d_atom.data_ptr(), d_tgt.data_ptr(), st)
-                    else:
-                        prog.launch(True, d_src.data_ptr(), d_atom.data_ptr(), st)
-                    torch.cuda.synchronize(dev)
-                    f, _ = st.read()
-                    if f != (1 << 64) - 1:
-                        raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, d_src.data_ptr())
-                raise RuntimeError("fused resume reported a failure that did not reproduce")
-            av, tv = memoryview(h_atom.numpy()), h_tgt.numpy()
-            list(pool.map(lambda o: _write_atomic(atomic_dir, o, av), atoms))
-            for g, i, m, odt, at, n, shape, g_at in outs:
-                host[g_at:g_at + n * odt.itemsize] = tv[at:at + n * odt.itemsize]
+
+    def emit(o, ov):
+        tag, o = o
+        if tag == "a":
+            _write_atomic(atomic_dir, o, ov)
+            return
+        _, _, _, odt, _, n, _, at, g_at = o
+        nb = n * odt.itemsize
+        host[g_at:g_at + nb] = np.frombuffer(ov, dtype=np.uint8, count=nb, offset=at)
+
+    _pipeline(wins, dev, "res", n_workers, emit)
     with open(os.path.join(atomic_dir, codec.MODEL_JSON), "w") as f:
         f.write(spec_to_json(spec))
     codec.write_json(os.path.join(atomic_dir, UCP_META_JSON), {
