@@ -141,30 +141,79 @@ def ncu_traffic_ratio(config: str):
         return None
 
 
-def cpu_reshard(spec, src, tgt, frags: dict, threads: int) -> float:
-    """The reference algorithm (oracle port) over a sample: union of every
-    (param, kind) unit, then extract_fragment of every target record of it,
-    materialised. Returns seconds."""
-    from oracle import ucp_oracle as O
-    from paper_2406_18820_b200.layout import all_rank_records
+def reference_ucp():
+    """The unmodified reference package from baseline/_ref (the offline pip
+    install of /root/reference; git-ignored, shipped with the repo), or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref, "ucp", "__init__.py")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import ucp
+    except Exception:  # noqa: BLE001 - an unusable install means "port"
+        return None
+    return ucp if os.path.dirname(os.path.dirname(ucp.__file__)) == ref else None
 
-    tgt_recs = all_rank_records(spec, tgt)
-    by_unit = {}
-    for g in range(tgt.world_size):
-        for m in tgt_recs[g]:
-            if (m.param, m.kind) in frags:
-                by_unit.setdefault((m.param, m.kind), []).append(m)
 
-    def unit(key):
-        p = spec.param(key[0])
-        full = O.union(p, src, frags[key], True)
-        for m in by_unit.get(key, ()):
-            O.extract(p, tgt, m, full).copy()
+class CpuArm:
+    """The reference algorithm on the host over a bounded sample: union of
+    every (param, kind) unit, then extract_fragment of every target record of
+    it, materialised. kind "reference" runs the reference's own functions
+    (ucp.union, ucp.parallel.extract_fragment on its own types) from
+    baseline/_ref; kind "port" runs the oracle restatement (oracle/). Inputs
+    are converted to the arm's types outside the timed region."""
 
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=threads) as pool:
-        list(pool.map(unit, list(frags)))
-    return time.perf_counter() - t0
+    def __init__(self, spec, src, tgt, frags: dict, prefer_reference: bool = True):
+        from paper_2406_18820_b200.layout import all_rank_records
+
+        self.ucp = reference_ucp() if prefer_reference else None
+        if self.ucp is not None and getattr(tgt, "vocab_multiple", 1) != 1:
+            self.ucp = None  # vocab padding is an extension the reference lacks
+        by_unit = {}
+        tgt_recs = all_rank_records(spec, tgt)
+        for g in range(tgt.world_size):
+            for m in tgt_recs[g]:
+                if (m.param, m.kind) in frags:
+                    by_unit.setdefault((m.param, m.kind), []).append(m)
+        if self.ucp is None:
+            from oracle import ucp_oracle as O
+
+            self.kind = "port"
+            self.union, self.extract = (lambda p, c, fs: O.union(p, c, fs, True)), O.extract
+            self.spec, self.src, self.tgt, self.frags, self.by_unit = spec, src, tgt, frags, by_unit
+            return
+        from paper_2406_18820_b200.spec import format_config_string, spec_to_dict
+
+        u = self.ucp
+        self.kind = "reference"
+        self.spec = u.models.spec_from_dict(spec_to_dict(spec))
+        self.src = u.parse_config_string(format_config_string(src))
+        self.tgt = u.parse_config_string(format_config_string(tgt))
+        RM, FM = u.parallel.RecordMeta, sys.modules["ucp.convert"].FragmentMsg
+        meta = lambda m: RM(m.param, m.kind, m.pattern, tuple(m.placement), tuple(m.shape),
+                            m.segments, m.flat_range, m.pad_elems)
+        self.frags = {k: [FM(meta(m), a) for m, a in v] for k, v in frags.items()}
+        self.by_unit = {k: [meta(m) for m in v] for k, v in by_unit.items()}
+        self.union = lambda p, c, fs: sys.modules["ucp.convert"].union(p, c, fs, True)
+        self.extract = u.parallel.extract_fragment
+
+    def run(self, threads: int) -> float:
+        """Seconds for one pass over the sample."""
+        def unit(key):
+            p = self.spec.param(key[0])
+            full = self.union(p, self.src, self.frags[key])
+            for m in self.by_unit.get(key, ()):
+                np_copy(self.extract(p, self.tgt, m, full))
+
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            list(pool.map(unit, list(self.frags)))
+        return time.perf_counter() - t0
+
+
+def np_copy(a):
+    return a.copy()
 
 
 def sample_params(spec, budget_state_bytes: float) -> list:
@@ -229,19 +278,23 @@ def run_reference(args):
     names = sample_params(spec, 3e9)
     S = sum(12 * spec.param(n).numel for n in names)
     frags = oracle_frags(spec, src, names, args.cpu_threads)
+    arm = CpuArm(spec, src, tgt, frags)
     for _ in range(args.warmup):
-        cpu_reshard(spec, src, tgt, frags, args.cpu_threads)
-    times = [cpu_reshard(spec, src, tgt, frags, args.cpu_threads) for _ in range(args.steps)]
+        arm.run(args.cpu_threads)
+    times = [arm.run(args.cpu_threads) for _ in range(args.steps)]
     t = statistics.mean(times)
     v = S / t / GB
-    sample = f"{len(names)} params ({names[0]} .. {names[-1]}), {S / GB:.2f} GB state"
+    what = ("ucp.union + ucp.parallel.extract_fragment from baseline/_ref (unmodified reference)"
+            if arm.kind == "reference" else "oracle port of union + extract_fragment")
+    sample = (f"{len(names)} params ({names[0]} .. {names[-1]}), {S / GB:.2f} GB state: {what}, "
+              f"materialised, {args.cpu_threads} threads")
     emit({"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
           "data": "synthetic: reference generator init_state(seed=7), partitioned under src",
           "config": {"workload": desc, "src": format_config_string(src),
                      "tgt": format_config_string(tgt), "sample": sample},
-          "cpu_baseline": {"value": v, "unit": "GB/s", "cores": args.cpu_threads, "kind": "port",
+          "cpu_baseline": {"value": v, "unit": "GB/s", "cores": args.cpu_threads, "kind": arm.kind,
                            "sample": sample},
           "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}},
          0)
@@ -513,14 +566,20 @@ def run_ours(args):
             cpu_names = sample_params(spec, 3e9)
             host_cpu_frags = oracle_frags(spec, src, cpu_names, args.cpu_threads)
         S_cpu = sum(12 * spec.param(n).numel for n in cpu_names)
-        t_cpu = cpu_reshard(spec, src, tgt, host_cpu_frags, args.cpu_threads)
-        t_cpu1 = cpu_reshard(spec, src, tgt, host_cpu_frags, 1)
+        arm = CpuArm(spec, src, tgt, host_cpu_frags)
+        t_cpu = arm.run(args.cpu_threads)
+        t_cpu1 = arm.run(1)
+        what = ("ucp.union + ucp.parallel.extract_fragment from baseline/_ref (unmodified "
+                "reference)" if arm.kind == "reference" else "oracle union + extract_fragment")
         cpu = {"value": S_cpu / t_cpu / GB, "unit": "GB/s", "cores": args.cpu_threads,
                "value_1_thread": S_cpu / t_cpu1 / GB,
-               "kind": "port",
+               "kind": arm.kind,
                "sample": f"{len(cpu_names)} params ({cpu_names[0]} .. {cpu_names[-1]}), "
-                         f"{S_cpu / GB:.2f} GB state: oracle union + extract_fragment "
+                         f"{S_cpu / GB:.2f} GB state: {what} "
                          f"(materialised), {args.cpu_threads} threads, one pass"}
+        if arm.kind == "reference":
+            cpu["port_value"] = S_cpu / CpuArm(spec, src, tgt, host_cpu_frags, False).run(
+                args.cpu_threads) / GB
       except Exception as exc:  # rank 0 only: no collective to skip
         cpu = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:300]}
 

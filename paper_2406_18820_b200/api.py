@@ -33,7 +33,7 @@ from ._errors import (
     UnsupportedCastError,
 )
 from .engine import Program, Status, align_up, gen_state, require_device
-from .layout import all_rank_records, layer_of, pp_layer_map, validate_model_config
+from .layout import all_rank_records, layer_of, pp_layer_map, same_config, validate_model_config
 from .plan import RunTable, compile_extract, compile_union, fragment_elems, fragment_shape
 from .spec import (
     FORMAT_VERSION,
@@ -732,7 +732,7 @@ def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1,
     src = codec.load_checkpoint(src_root)
     validate_model_config(src.spec, tgt)
     before = INVOCATIONS
-    if src.cfg == tgt:
+    if same_config(src.cfg, tgt):
         stats = LoadStats(bypass=bypass)
         stats.resident_bound = resident_bound_elements(src.spec, tgt.dp)
         stats.per_rank = {g: {"files_read": 0, "bytes_read": 0} for g in range(tgt.world_size)}

@@ -43,6 +43,19 @@ def zero_of(cfg) -> ZeroStage:
     return z if isinstance(z, ZeroStage) else ZeroStage(getattr(z, "value", z))
 
 
+def config_key(cfg) -> tuple:
+    """Field-wise identity of a ParallelConfig that also holds across the
+    reference's class (its dataclass ``==`` compares class first)."""
+    s = cfg.pp_schedule
+    return (cfg.dp, cfg.tp, cfg.pp, cfg.sp, zero_of(cfg), s.kind, s.v,
+            getattr(cfg, "vocab_multiple", 1))
+
+
+def same_config(a, b) -> bool:
+    """``a == b`` as ucp/load.py:250 means it, for either package's configs."""
+    return config_key(a) == config_key(b)
+
+
 def validate_model_config(spec: ModelSpec, cfg: ParallelConfig) -> None:
     cfg.validate()
     if cfg.pp > max(spec.n_layers, 1):

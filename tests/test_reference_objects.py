@@ -1,7 +1,7 @@
 """Duck-typing of the reference's own objects (ParamSpec / ParallelConfig /
 RecordMeta from /root/reference) through the descriptor compiler, as the
 hot-swap shim in INTEGRATION.md relies on. Runs only where the reference is
-importable (the build container); the GPU box skips it."""
+importable (baseline/_ref or /root/reference); skipped elsewhere."""
 
 import os
 import sys
@@ -9,10 +9,13 @@ import sys
 import numpy as np
 import pytest
 
-REF = "/root/reference/pkg/src"
-if not os.path.isdir(REF):
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CANDIDATES = [os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"]
+REF = next((c for c in CANDIDATES if os.path.isfile(os.path.join(c, "ucp", "__init__.py"))), None)
+if REF is None:
     pytest.skip("reference package not present", allow_module_level=True)
-sys.path.insert(0, REF)
+if REF not in sys.path:
+    sys.path.insert(0, REF)
 sys.dont_write_bytecode = True
 ucp = pytest.importorskip("ucp")
 
