@@ -260,6 +260,69 @@ def oracle_frags(spec, src, names, threads):
     return frags
 
 
+def pcie_peaks(dev, stream, nbytes: int = 1 << 30, reps: int = 5) -> dict:
+    """Pinned cudaMemcpyAsync peaks of this process's GPU link, measured in
+    the same run (the host staging stage is judged against them):
+    H2D alone, D2H alone, and both at once on two streams (GB/s, best of
+    `reps`, CUDA events)."""
+    import torch
+
+    try:
+        h_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        d_in = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        d_out = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    except RuntimeError:
+        return {}
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn):
+        best = float("inf")
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            s1.wait_stream(stream)
+            s2.wait_stream(stream)
+            fn()
+            stream.wait_stream(s1)
+            stream.wait_stream(s2)
+            b.record(stream)
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b) / 1e3)
+        return best
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+
+    def both():
+        h2d()
+        d2h()
+
+    t_in, t_out, t_both = timed(h2d), timed(d2h), timed(both)
+    return {"h2d_GBps": nbytes / t_in / GB, "d2h_GBps": nbytes / t_out / GB,
+            "bidir_GBps": 2 * nbytes / t_both / GB,
+            "how": f"pinned {nbytes >> 20} MiB cudaMemcpyAsync, best of {reps}, same process"}
+
+
+def link_roofline(link: dict, h2d: int, d2h: int, ms: float) -> dict:
+    """The e2e step against the link: bytes over PCIe per step / step time
+    vs the bidirectional pinned peak (and each direction vs its own)."""
+    if not link:
+        return {}
+    t = ms / 1e3
+    out = dict(link)
+    out.update({"achieved_GBps": (h2d + d2h) / t / GB, "h2d_GBps_in_step": h2d / t / GB,
+                "d2h_GBps_in_step": d2h / t / GB,
+                "frac": (h2d + d2h) / t / GB / link["bidir_GBps"]})
+    return out
+
+
 def emit(obj, rank):
     if rank == 0:
         print(json.dumps(obj), flush=True)
@@ -521,17 +584,24 @@ def run_ours(args):
             if e2e_err is not None:
                 raise RuntimeError(e2e_err)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            words = [torch.empty(2, dtype=torch.int64, pin_memory=True)
+                     for _ in range(args.e2e_steps)]
             torch.cuda.synchronize()
             e0.record(stream)
             for s_ in streams:
                 s_.wait_stream(stream)
-            for _ in range(args.e2e_steps):
-                eplan.stream_host(host_src, host_tgt, None, streams)
+            for k in range(args.e2e_steps):
+                # the public pinned-host entry; each step's result (the
+                # device status word) is read back to the host in the step
+                eplan.run_pinned(host_src, host_tgt, streams, status_out=words[k], sync=False)
             for s_ in streams:
                 stream.wait_stream(s_)
             e1.record(stream)
             torch.cuda.synchronize()
+            if not all(eplan.status_ok(w) for w in words):
+                eplan._check_windows(host_src)
             e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+            link = pcie_peaks(dev, stream)
             S_e2e_local = eplan.state_bytes
             e2e_meta = {"h2d": int(eplan.src_total), "d2h": int(eplan.tgt_total),
                         "windows": len(eplan.windows), "names": names}
@@ -551,6 +621,9 @@ def run_ours(args):
             e2e = {"value": S_e2e / (e2e_ms / 1e3) / GB, "unit": "GB/s",
                    "h2d_bytes_per_step": e2e_meta["h2d"], "d2h_bytes_per_step": e2e_meta["d2h"],
                    "ms_per_step": e2e_ms, "state_bytes_per_step": int(S_e2e),
+                   "api": "ReshardPlan.run_pinned (public pinned-host entry; reshard() = "
+                          "pack_host + run_pinned + unpack_host)",
+                   "link": link_roofline(link, e2e_meta["h2d"], e2e_meta["d2h"], e2e_ms),
                    "sample": f"{len(names)} params ({names[0]} .. {names[-1]}; "
                              f"{S_e2e_local / GB:.2f} GB state/rank) from pinned host memory: "
                              f"H2D + fused reshard + D2H in {e2e_meta['windows']} double-buffered "

@@ -51,6 +51,7 @@ from .api import (
     ucp_info,
     union,
 )
+from .reshard import ReshardPlan
 from .codec import DistributedCheckpoint, load_checkpoint, read_manifest, read_tensor, write_tensor
 from .layout import (
     enumerate_rank_records,

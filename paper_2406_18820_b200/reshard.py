@@ -469,15 +469,40 @@ class ReshardPlan:
                 out.setdefault(g, {})[i] = hv[at:at + dt.itemsize * n].view(dt.storage).reshape(shape)
         return {g: [d[i] for i in sorted(d)] for g, d in out.items()}
 
+    def run_pinned(self, host_src: torch.Tensor, host_tgt: torch.Tensor, streams=None,
+                   status_out: torch.Tensor | None = None, sync: bool = True) -> None:
+        """Public zero-copy entry: pinned host source arena (``pack_host``
+        layout) -> H2D -> fused convert+load -> D2H into the pinned host
+        target arena (``unpack_host`` layout), double-buffered over windows.
+
+        The call's result is the device status word: it is copied to
+        ``status_out`` (pinned int64[2]) on the D2H stream after the last
+        window. With ``sync`` the call waits and raises the reference's
+        exception on a data-dependent failure (ReplicateMismatchError,
+        PaddingError, ...); without it the caller checks ``status_out``
+        later with ``check_status_word``."""
+        streams = streams or (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device),
+                              torch.cuda.Stream(self.device))
+        self.stream_host(host_src, host_tgt, None, streams)
+        if status_out is not None:
+            with torch.cuda.stream(streams[2]):
+                status_out.copy_(self.status.t, non_blocking=True)
+        if sync:
+            streams[2].synchronize()
+            if status_out is None or not self.status_ok(status_out):
+                self._check_windows(host_src)
+
+    @staticmethod
+    def status_ok(word: torch.Tensor) -> bool:
+        return int(word.numpy().view(np.uint64)[0]) == (1 << 64) - 1
+
     def run_host(self, shards: dict) -> dict:
         """End-to-end in-memory reshard of host arrays; returns target arrays
         per rank in canonical record order."""
         host_src = self.pack_host(shards)
         host_tgt = torch.empty(max(self.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
         self.status.reset()
-        self.stream_host(host_src, host_tgt)
-        torch.cuda.synchronize(self.device)
-        self._check_windows(host_src)
+        self.run_pinned(host_src, host_tgt)
         return self.unpack_host(host_tgt)
 
     def _check_windows(self, host_src=None) -> None:

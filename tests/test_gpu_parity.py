@@ -342,6 +342,43 @@ def test_fused_replica_mismatch_detected():
     assert "layers.1.attn_qkv.weight" in str(ei.value) and "dp" in str(ei.value)
 
 
+def test_run_pinned_async_status_word():
+    """The public pinned-host entry the bench's e2e leg uses: an unsynced
+    call reports through the pinned status word; a clean call leaves it
+    clean and produces the oracle's world; a replica fault flips it and the
+    synced call raises the reference's exception."""
+    spec = U.make_model("GQA", {"n_layers": 2, "hidden": 64, "q_heads": 8, "kv_heads": 2})
+    src_cfg, tgt_cfg = cfg(dp=2, tp=2, zero="z1"), cfg(dp=2, tp=4, zero="z1")
+    state = O.init_state(spec, 7)
+    shards = O.partition_mem(spec, state, src_cfg)
+    host = {g: [a.copy() for _, a in v] for g, v in shards.items()}
+    plan = U.ReshardPlan(spec, src_cfg, tgt_cfg, fused=True, window_bytes=1 << 16)
+    h_src = plan.pack_host(host)
+    h_tgt = torch.empty(max(plan.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
+    word = torch.empty(2, dtype=torch.int64, pin_memory=True)
+    plan.status.reset()
+    for _ in range(2):  # back-to-back unsynced calls share the three streams
+        plan.run_pinned(h_src, h_tgt, status_out=word, sync=False)
+    torch.cuda.synchronize()
+    assert plan.status_ok(word)
+    want = O.load_mem(spec, O.convert_mem(spec, src_cfg, shards), tgt_cfg, "F32")
+    got = plan.unpack_host(h_tgt)
+    for g in range(tgt_cfg.world_size):
+        for a, (_, b) in zip(got[g], want[g]):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    recs = U.enumerate_rank_records(spec, src_cfg, 1)
+    i = next(k for k, m in enumerate(recs) if m.param == "layers.0.attn_out" and m.kind == "weight")
+    host[1][i].reshape(-1)[3] = np.float32(-2.0)
+    h_src = plan.pack_host(host, h_src)
+    plan.status.reset()
+    plan.run_pinned(h_src, h_tgt, status_out=word, sync=False)
+    torch.cuda.synchronize()
+    assert not plan.status_ok(word)
+    plan.status.reset()
+    with pytest.raises(U.ReplicateMismatchError):
+        plan.run_pinned(h_src, h_tgt, status_out=word)
+
+
 def test_shard_hy_union_gpu():
     p = ParamSpec("g", (64, 96), 0, ParamKind.MATMUL2D, 0)
     full = np.arange(64 * 96, dtype=np.float32).reshape(64, 96)
