@@ -46,7 +46,7 @@ constexpr int kMaxAux = 256;             // host splits runs beyond this
 // ---------------------------------------------------------------- memory ops
 
 #ifndef UCP_L2_PREFETCH
-#define UCP_L2_PREFETCH 0  // 0, 128 or 256: L2 sector prefetch hint on streaming loads
+#define UCP_L2_PREFETCH 0  // 0, 128 or 256: L2 sector prefetch hint on streaming loads; 1: L2 evict_first
 #endif
 
 __device__ __forceinline__ float4 ld_stream4(const void* p) {
@@ -55,6 +55,12 @@ __device__ __forceinline__ float4 ld_stream4(const void* p) {
   asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
       : "l"(p));
+#elif UCP_L2_PREFETCH == 1  // L2 evict-first policy on the read-once sources
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p), "l"(pol));
 #elif UCP_L2_PREFETCH == 128
   asm("ld.global.nc.L1::no_allocate.L2::128B.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
@@ -73,8 +79,38 @@ __device__ __forceinline__ float ld_stream1(const void* p) {
   return r;
 }
 
+#ifndef UCP_ST_HINT
+#define UCP_ST_HINT 0  // 0: plain st.global; 1: st.global.cs (evict-first streaming); 2: L2::evict_first policy
+#endif
+
 __device__ __forceinline__ void st4(void* p, float4 v) {
+#if UCP_ST_HINT == 1
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+#elif UCP_ST_HINT == 2
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+#else
   *reinterpret_cast<float4*>(p) = v;
+#endif
+}
+
+__device__ __forceinline__ void st2u(void* p, uint2 v) {
+#if UCP_ST_HINT == 1
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+#elif UCP_ST_HINT == 2
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y),
+               "l"(pol)
+               : "memory");
+#else
+  *reinterpret_cast<uint2*>(p) = v;
+#endif
 }
 
 // ---------------------------------------------------------------- bit ops
@@ -189,7 +225,7 @@ __device__ __forceinline__ void store_w(char* p, const Lanes<W>& x, int dtype) {
       uint2 h;
       h.x = cvt16(x.v[0], dtype) | (cvt16(x.v[1], dtype) << 16);
       h.y = cvt16(x.v[2], dtype) | (cvt16(x.v[3], dtype) << 16);
-      *reinterpret_cast<uint2*>(p) = h;
+      st2u(p, h);
     } else {
       *reinterpret_cast<uint16_t*>(p) = (uint16_t)cvt16(x.v[0], dtype);
     }
@@ -431,7 +467,7 @@ __device__ __forceinline__ void store4(char* p, const float4& v) {
     uint2 h;
     h.x = cvt16(v.x, DT) | (cvt16(v.y, DT) << 16);
     h.y = cvt16(v.z, DT) | (cvt16(v.w, DT) << 16);
-    *reinterpret_cast<uint2*>(p) = h;
+    st2u(p, h);
   }
 }
 
