@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--e2e-gb", type=float, default=24.0, help="pinned host budget of the e2e sample")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-window-gb", type=float, default=0.4)
+    ap.add_argument("--e2e-slots", type=int, default=3, help="device slots per direction")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -569,6 +570,7 @@ def run_ours(args):
                             a = hv[at:at + 4 * n].view("<f4").copy().reshape(m.shape)
                             host_cpu_frags.setdefault((m.param, m.kind), []).append((m, a))
             streams = tuple(torch.cuda.Stream(dev) for _ in range(3))
+            eplan.host_slots = args.e2e_slots
             eplan.status.reset()
             eplan.stream_host(host_src, host_tgt, None, streams)
             torch.cuda.synchronize()

@@ -152,6 +152,7 @@ class ReshardPlan:
         self._layout()
         self._compile()
         self.status = Status(self.device)
+        self.host_slots = 3  # device slots per direction of the host-streamed pipeline (3 > 2 by 6 % e2e)
         self._bufs = {}
 
     # ------------------------------------------------------------------ planning
@@ -415,16 +416,18 @@ class ReshardPlan:
         return host
 
     def stream_host(self, host_src: torch.Tensor, host_tgt: torch.Tensor, windows=None,
-                    streams=None) -> None:
+                    streams=None, slots: int | None = None) -> None:
         """Pinned host source arena -> device -> pinned host target arena,
-        double-buffered over windows on three streams. Asynchronous: the
-        caller synchronises (the last event is on the D2H stream)."""
+        multi-buffered (``slots`` device slots per direction, default
+        ``self.host_slots``) over windows on three streams. Asynchronous:
+        the caller synchronises (the last event is on the D2H stream)."""
         wins = self.windows if windows is None else windows
         s_in, s_cmp, s_out = streams or (torch.cuda.Stream(self.device),
                                          torch.cuda.Stream(self.device),
                                          torch.cuda.Stream(self.device))
-        dsrc = [self.buf("ssrc0", self.max_src), self.buf("ssrc1", self.max_src)]
-        dtgt = [self.buf("stgt0", self.max_tgt), self.buf("stgt1", self.max_tgt)]
+        ns = max(2, slots or self.host_slots)
+        dsrc = [self.buf(f"ssrc{j}", self.max_src) for j in range(ns)]
+        dtgt = [self.buf(f"stgt{j}", self.max_tgt) for j in range(ns)]
         atom = self.buf("atom", self.max_atom)
         # buffers are reused across calls: the first H2D must not overwrite a
         # source slot still being read, the first kernel must not overwrite a
@@ -435,16 +438,16 @@ class ReshardPlan:
         ev_cmp = [torch.cuda.Event() for _ in wins]
         ev_out = [torch.cuda.Event() for _ in wins]
         for i, W in enumerate(wins):
-            slot = i % 2
+            slot = i % ns
             with torch.cuda.stream(s_in):
-                if i >= 2:
-                    s_in.wait_event(ev_cmp[i - 2])
+                if i >= ns:
+                    s_in.wait_event(ev_cmp[i - ns])
                 dsrc[slot][:W.src_bytes].copy_(host_src[W.src_base:W.src_base + W.src_bytes],
                                                non_blocking=True)
                 ev_in[i].record(s_in)
             s_cmp.wait_event(ev_in[i])
-            if i >= 2:
-                s_cmp.wait_event(ev_out[i - 2])
+            if i >= ns:
+                s_cmp.wait_event(ev_out[i - ns])
             W.fused.launch(dsrc[slot].data_ptr(), atom.data_ptr(), dtgt[slot].data_ptr(),
                            self.status, s_cmp)
             W.conv.launch(True, dsrc[slot].data_ptr(), atom.data_ptr(), self.status, s_cmp)
