@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--unfused", action="store_true",
                     help="separate convert and load launches (atomic re-read from HBM)")
     ap.add_argument("--cpu-threads", type=int, default=os.cpu_count())
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16"],
+                    help="target weight dtype of load (moments stay f32), ucp/load.py:204-205")
     return ap.parse_args()
 
 
@@ -380,16 +382,18 @@ def run_ours(args):
 
     spec, src, tgt, desc = bench_config(args.config, args.layers)
     mine = owned_params(spec, rank, world) if world > 1 else None
+    from paper_2406_18820_b200.spec import DType as _DTy
+
+    wdt = {"f32": _DTy.F32, "bf16": _DTy.BF16, "f16": _DTy.F16}[args.dtype]
     homed = args.home == "rank"
     exch = peer = None
     if homed:
         from paper_2406_18820_b200.dist import PeerBuffers, build_exchange
-        from paper_2406_18820_b200.spec import DType as _DT
 
-        exch = build_exchange(spec, src, tgt, world, rank, int(args.window_gb * GB), _DT.F32)
+        exch = build_exchange(spec, src, tgt, world, rank, int(args.window_gb * GB), wdt)
         if args.exchange == "peer":
             peer = PeerBuffers(exch.max_recv, n_slots=2)
-    plan = ReshardPlan(spec, src, tgt, params=mine, device=dev,
+    plan = ReshardPlan(spec, src, tgt, params=mine, device=dev, dtype=wdt,
                        window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024,
                        fused=not args.unfused, strict=not args.non_strict,
                        materialize_atomic=not args.no_atomic,
@@ -548,7 +552,7 @@ def run_ours(args):
             names = [p.name for W in wins for p in W.params]
             # the e2e path gets its own plan with small windows so PCIe in, HBM
             # work and PCIe out overlap with little pipeline fill / drain
-            eplan = ReshardPlan(spec, src, tgt, params=names, device=dev,
+            eplan = ReshardPlan(spec, src, tgt, params=names, device=dev, dtype=wdt,
                                 window_bytes=int(args.e2e_window_gb * GB),
                                 tile_bytes=args.tile_kb * 1024, fused=not args.unfused)
             # inputs of the sample: synthesised by the GPU generator into the
@@ -684,6 +688,7 @@ def run_ours(args):
                                    "events; value = S / sum of per-window reshard time")
                      if windowed else "whole source arena resident in HBM",
                      "strict_replicate": not args.non_strict,
+                     "target_weight_dtype": args.dtype,
                      "atomic_materialised": not args.no_atomic},
           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
           "gpu_launches": gpu_launches, "parity": parity}, rank)
