@@ -31,6 +31,8 @@ import tempfile
 import time
 from concurrent.futures import ThreadPoolExecutor
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -178,7 +180,7 @@ class CpuArm:
         for g in range(tgt.world_size):
             for m in tgt_recs[g]:
                 if (m.param, m.kind) in frags:
-                    by_unit.setdefault((m.param, m.kind), []).append(m)
+                    by_unit.setdefault((m.param, m.kind), []).append((g, m))
         if self.ucp is None:
             from oracle import ucp_oracle as O
 
@@ -197,17 +199,20 @@ class CpuArm:
         meta = lambda m: RM(m.param, m.kind, m.pattern, tuple(m.placement), tuple(m.shape),
                             m.segments, m.flat_range, m.pad_elems)
         self.frags = {k: [FM(meta(m), a) for m, a in v] for k, v in frags.items()}
-        self.by_unit = {k: [meta(m) for m in v] for k, v in by_unit.items()}
+        self.by_unit = {k: [(g, meta(m)) for g, m in v] for k, v in by_unit.items()}
         self.union = lambda p, c, fs: sys.modules["ucp.convert"].union(p, c, fs, True)
         self.extract = u.parallel.extract_fragment
 
-    def run(self, threads: int) -> float:
-        """Seconds for one pass over the sample."""
+    def run(self, threads: int, collect: dict | None = None) -> float:
+        """Seconds for one pass over the sample. ``collect`` (optional)
+        receives every target fragment as {(g, param, kind): array}."""
         def unit(key):
             p = self.spec.param(key[0])
             full = self.union(p, self.src, self.frags[key])
-            for m in self.by_unit.get(key, ()):
-                np_copy(self.extract(p, self.tgt, m, full))
+            for g, m in self.by_unit.get(key, ()):
+                out = np_copy(self.extract(p, self.tgt, m, full))
+                if collect is not None:
+                    collect[(g, key[0], key[1])] = out
 
         t0 = time.perf_counter()
         with ThreadPoolExecutor(max_workers=threads) as pool:
@@ -539,6 +544,7 @@ def run_ours(args):
     e2e = None
     host_cpu_frags = None
     cpu_names = None
+    gpu_index = None
     if not args.no_e2e and peer is None:
         e2e_ms, S_e2e_local, e2e_err, e2e_meta = float("inf"), 0, None, {}
         try:
@@ -611,6 +617,10 @@ def run_ours(args):
             S_e2e_local = eplan.state_bytes
             e2e_meta = {"h2d": int(eplan.src_total), "d2h": int(eplan.tgt_total),
                         "windows": len(eplan.windows), "names": names}
+            if cpu_names:  # where the GPU wrote the CPU sample's target fragments
+                gpu_index = {(g, m.param, m.kind): (W.tgt_base + off, n)
+                             for W in eplan.windows for g, i, m, off, n, dt in W.tgt_frags
+                             if m.param in cpu_names and dt.itemsize == 4}
             del eplan
         except Exception as exc:  # the main line must survive a host-memory failure
             e2e_err = f"{type(exc).__name__}: {exc}"[:300]
@@ -646,8 +656,27 @@ def run_ours(args):
             host_cpu_frags = oracle_frags(spec, src, cpu_names, args.cpu_threads)
         S_cpu = sum(12 * spec.param(n).numel for n in cpu_names)
         arm = CpuArm(spec, src, tgt, host_cpu_frags)
-        t_cpu = arm.run(args.cpu_threads)
+        ref_out: dict = {}
+        t_cpu = arm.run(args.cpu_threads, ref_out)
         t_cpu1 = arm.run(1)
+        parity_cpu = None
+        if gpu_index:
+            # the reference's own outputs vs the GPU's e2e outputs, same sample
+            hv = host_tgt.numpy()
+            same = nbytes = compared = 0
+            for key, want in ref_out.items():
+                if key not in gpu_index:  # bf16/f16 weights: the CPU arm does not cast
+                    continue
+                compared += 1
+                at, n = gpu_index[key]
+                got = hv[at:at + 4 * n]
+                w = np.ascontiguousarray(want).reshape(-1).view(np.uint8)
+                same += int(w.size == got.size and np.array_equal(w, got))
+                nbytes += w.size
+            parity_cpu = {"fragments": compared, "identical": same, "bytes": int(nbytes),
+                          "bit_exact": same == compared == len(gpu_index) > 0,
+                          "what": "every target fragment the CPU arm produced vs the GPU "
+                                  "e2e leg's D2H output for the same params"}
         what = ("ucp.union + ucp.parallel.extract_fragment from baseline/_ref (unmodified "
                 "reference)" if arm.kind == "reference" else "oracle union + extract_fragment")
         cpu = {"value": S_cpu / t_cpu / GB, "unit": "GB/s", "cores": args.cpu_threads,
@@ -656,6 +685,7 @@ def run_ours(args):
                "sample": f"{len(cpu_names)} params ({cpu_names[0]} .. {cpu_names[-1]}), "
                          f"{S_cpu / GB:.2f} GB state: {what} "
                          f"(materialised), {args.cpu_threads} threads, one pass"}
+        cpu["parity_vs_gpu"] = parity_cpu
         if arm.kind == "reference":
             cpu["port_value"] = S_cpu / CpuArm(spec, src, tgt, host_cpu_frags, False).run(
                 args.cpu_threads) / GB
