@@ -32,7 +32,7 @@ from ._errors import (
     ShapeError,
     UnsupportedCastError,
 )
-from .engine import Program, Status, align_up, gen_state, require_device
+from .engine import Program, Status, align_up, gen_state, pinned_host, require_device
 from .layout import all_rank_records, layer_of, pp_layer_map, same_config, validate_model_config
 from .plan import RunTable, compile_extract, compile_union, fragment_elems, fragment_shape
 from .spec import (
@@ -183,8 +183,8 @@ class _Staging:
     def host_buf(self, key: str, nbytes: int) -> torch.Tensor:
         b = self.host.get(key)
         if b is None or b.numel() < nbytes:
-            b = torch.empty(max(align_up(nbytes, 1 << 20), 1 << 20), dtype=torch.uint8,
-                            pin_memory=True)
+            self.host.pop(key, None)
+            b = pinned_host(max(align_up(nbytes, 1 << 20), 1 << 20))
             self.host[key] = b
         return b
 
@@ -382,12 +382,19 @@ def _io_pool(n_workers: int) -> ThreadPoolExecutor:
 # --------------------------------------------------------------------------- pipeline
 
 
-def _write_atomic(out_dir: str, o, ov: memoryview) -> None:
+def _write_atomic(out_dir: str, o, ov: memoryview) -> list:
+    """One job writing one atomic file. Whole-file writes: concurrent
+    ranged writes into one tmpfs file serialise on its inode lock and were
+    2.4x slower (profiles/file_cfg2l4_r01ab_*.json)."""
     p, kind, at = o
-    pdir = os.path.join(out_dir, p.name)
-    os.makedirs(pdir, exist_ok=True)
-    codec.write_raw(os.path.join(pdir, ATOMIC_FILES[kind]), DType.F32, p.shape,
-                    ov[at:at + 4 * p.numel])
+
+    def job():
+        pdir = os.path.join(out_dir, p.name)
+        os.makedirs(pdir, exist_ok=True)
+        codec.write_raw(os.path.join(pdir, ATOMIC_FILES[kind]), DType.F32, p.shape,
+                        ov[at:at + 4 * p.numel])
+
+    return [job]
 
 
 class _Step:
@@ -439,19 +446,41 @@ class _FusedStep:
         raise RuntimeError("fused resume reported a failure that did not reproduce")
 
 
-def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
-    """Windowed file pipeline, double-buffered so file reads of window w+1
-    and the output handling of window w-1 overlap the GPU work of window w:
+IO_CHUNK = int(os.environ.get("UCP_IO_CHUNK", 16 << 20))  # bytes per file read job (0: whole files)
+COPY_CHUNK = int(os.environ.get("UCP_COPY_CHUNK", 64 << 20))  # bytes per host copy job
+SEND_MIN = 4 << 20   # read chunks at least this large issue their own H2D
+ALIGN_GAP = 4096     # unsent ranges closer than this are sent as one copy (gap bytes are junk)
+PIPE_TRACE: dict = {}  # seconds the last _pipeline call spent waiting, by stage
 
-        read files (thread pool) -> pinned -> H2D -> kernel(s) -> D2H -> pinned
-        -> emit(o, view) per output (thread pool)
+
+def _chunks(nbytes: int, chunk: int = 0):
+    chunk = chunk or IO_CHUNK
+    if chunk <= 0 or nbytes <= chunk:
+        return [(0, nbytes)]
+    return [(o, min(chunk, nbytes - o)) for o in range(0, nbytes, chunk)]
+
+
+def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
+    """Windowed file pipeline, double-buffered so file reads of windows w
+    and w+1 and the output handling of window w-1 overlap the GPU work of
+    window w:
+
+        read files (thread pool, <=IO_CHUNK pread jobs) -> pinned -> H2D ->
+        kernel(s) -> D2H -> pinned -> emit jobs (thread pool)
 
     wplans: [(step, read jobs (path, header, offset), src bytes, outs, dst
-    bytes)] with step a _Step/_FusedStep. Data-dependent failures raise after
-    their window syncs, so a failing window never reaches emit (torn output,
+    bytes)] with step a _Step/_FusedStep. ``emit(o, view)`` runs on this
+    thread and returns zero-argument jobs (file-range writes, host copies)
+    that the write pool runs. Data-dependent failures raise after their
+    window syncs, so a failing window never reaches emit (torn output,
     ucp/convert.py:503)."""
+    import time
+
+    PIPE_TRACE.clear()
     if not wplans:
         return
+    t_start = time.perf_counter()
+    tr = {"read_wait_s": 0.0, "gpu_wait_s": 0.0, "emit_wait_s": 0.0, "emit_submit_s": 0.0}
     ms = max(w[2] for w in wplans)
     md = max(w[4] for w in wplans)
     h_src = [_STAGE.host_buf(f"{key}_src{i}", ms) for i in range(2)]
@@ -460,48 +489,114 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
     d_dst = [_STAGE.dev_buf(f"{key}_dst{i}", md, dev) for i in range(2)]
     st = _status(dev)
     stream = torch.cuda.current_stream(dev)
+    # one H2D stream per slot: each read job enqueues the H2D of its own
+    # chunk as soon as the bytes land, so PCIe-in overlaps the file reads
+    s_h2d = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     nthreads = max(4, min(32, 2 * n_workers, os.cpu_count() or 4))
     with ThreadPoolExecutor(nthreads) as rpool, ThreadPoolExecutor(nthreads) as wpool:
 
+        def read_and_send(slot, path, file_off, at, n, send):
+            codec.read_range_into(path, file_off, memoryview(h_src[slot].numpy())[at:at + n])
+            if send:
+                with torch.cuda.device(dev), torch.cuda.stream(s_h2d[slot]):
+                    d_src[slot][at:at + n].copy_(h_src[slot][at:at + n], non_blocking=True)
+
+        unsent: dict = {}
+
         def reads(w):
-            hv = memoryview(h_src[w % 2].numpy())
-            return [rpool.submit(codec.read_payload_into, path, hdr, hv[at:at + hdr.nbytes])
-                    for path, hdr, at in wplans[w][1]]
+            # chunks below SEND_MIN are not sent by their job (a copy call
+            # per small file costs more than it overlaps); they are coalesced
+            # into few H2D copies once the window's reads are done
+            slot, futs, rest = w % 2, [], []
+            for path, hdr, at in wplans[w][1]:
+                for c, n in _chunks(hdr.nbytes):
+                    if n:
+                        send = n >= SEND_MIN
+                        futs.append(rpool.submit(read_and_send, slot, path, hdr.offset + c,
+                                                 at + c, n, send))
+                        if not send:
+                            rest.append((at + c, n))
+            unsent[w] = rest
+            return futs
+
+        def send_rest(w, slot):
+            runs = []
+            for at, n in sorted(unsent.pop(w)):
+                if runs and at - (runs[-1][0] + runs[-1][1]) <= ALIGN_GAP:
+                    runs[-1][1] = at + n - runs[-1][0]
+                else:
+                    runs.append([at, n])
+            with torch.cuda.stream(s_h2d[slot]):
+                for at, n in runs:
+                    d_src[slot][at:at + n].copy_(h_src[slot][at:at + n], non_blocking=True)
 
         pending = {0: reads(0)}
         written: dict = {}
         h2d_ev: dict = {}
+        kern_ev: dict = {}
         try:
             for w, (step, _, s_at, outs, d_at) in enumerate(wplans):
                 slot = w % 2
+                if w + 1 < len(wplans):
+                    # start reading window w+1 before waiting for window w:
+                    # h_src[(w+1)%2] is free once window w-1's H2D drained,
+                    # d_src[(w+1)%2] once window w-1's kernels ran
+                    if w >= 1:
+                        h2d_ev.pop(w - 1).synchronize()
+                        s_h2d[(w + 1) % 2].wait_event(kern_ev.pop(w - 1))
+                    pending[w + 1] = reads(w + 1)
+                t0 = time.perf_counter()
                 for f in pending.pop(w):
                     f.result()
-                d_src[slot][:s_at].copy_(h_src[slot][:s_at], non_blocking=True)
+                tr["read_wait_s"] += time.perf_counter() - t0
+                send_rest(w, slot)
                 h2d_ev[w] = torch.cuda.Event()
-                h2d_ev[w].record(stream)
+                h2d_ev[w].record(s_h2d[slot])
+                stream.wait_event(h2d_ev[w])
                 st.reset(stream)
                 step.launch(d_src[slot].data_ptr(), d_dst[slot].data_ptr(), st, stream)
+                kern_ev[w] = torch.cuda.Event()
+                kern_ev[w].record(stream)
+                t0 = time.perf_counter()
                 for f in written.pop(w - 2, ()):  # h_dst[slot] is free again
                     f.result()
+                tr["emit_wait_s"] += time.perf_counter() - t0
                 h_dst[slot][:d_at].copy_(d_dst[slot][:d_at], non_blocking=True)
                 done = torch.cuda.Event()
                 done.record(stream)
-                if w + 1 < len(wplans):
-                    if w >= 1:
-                        h2d_ev.pop(w - 1).synchronize()  # h_src[(w+1)%2] drained
-                    pending[w + 1] = reads(w + 1)
+                t0 = time.perf_counter()
                 done.synchronize()
+                tr["gpu_wait_s"] += time.perf_counter() - t0
                 step.check(st, d_src[slot].data_ptr(), d_dst[slot].data_ptr(), stream)
                 ov = memoryview(h_dst[slot].numpy())
-                written[w] = [wpool.submit(emit, o, ov) for o in outs]
+                t0 = time.perf_counter()
+                written[w] = [wpool.submit(job) for o in outs for job in emit(o, ov)]
+                tr["emit_submit_s"] += time.perf_counter() - t0
+            t0 = time.perf_counter()
             for fs in written.values():
                 for f in fs:
                     f.result()
+            tr["emit_wait_s"] += time.perf_counter() - t0
         except BaseException:
             for fs in list(pending.values()) + list(written.values()):
                 for f in fs:
                     f.cancel()
             raise
+    tr["total_s"] = time.perf_counter() - t_start
+    tr["windows"] = len(wplans)
+    PIPE_TRACE.update(tr)
+
+
+def _copy_jobs(host: np.ndarray, g_at: int, ov: memoryview, at: int, nb: int) -> list:
+    """Jobs copying ov[at:at+nb] to host[g_at:g_at+nb] in IO_CHUNK pieces."""
+    src = np.frombuffer(ov, dtype=np.uint8, count=nb, offset=at) if nb else None
+
+    def job(c, n):
+        def run():
+            host[g_at + c:g_at + c + n] = src[c:c + n]
+        return run
+
+    return [job(c, n) for c, n in _chunks(nb, COPY_CHUNK)] if nb else []
 
 
 # --------------------------------------------------------------------------- convert
@@ -701,8 +796,7 @@ def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass
 
     def emit(o, ov):
         _, _, _, odt, at, n, _, g_at = o
-        host[g_at:g_at + n * odt.itemsize] = np.frombuffer(ov, dtype=np.uint8, count=n * odt.itemsize,
-                                                           offset=at)
+        return _copy_jobs(host, g_at, ov, at, n * odt.itemsize)
 
     _pipeline(wplans, dev, "load", 4, emit)
     filled = {}
@@ -837,11 +931,9 @@ def _resume_fused(src_root: str, atomic_dir: str, tgt: ParallelConfig, dtype: DT
     def emit(o, ov):
         tag, o = o
         if tag == "a":
-            _write_atomic(atomic_dir, o, ov)
-            return
+            return _write_atomic(atomic_dir, o, ov)
         _, _, _, odt, _, n, _, at, g_at = o
-        nb = n * odt.itemsize
-        host[g_at:g_at + nb] = np.frombuffer(ov, dtype=np.uint8, count=nb, offset=at)
+        return _copy_jobs(host, g_at, ov, at, n * odt.itemsize)
 
     _pipeline(wins, dev, "res", n_workers, emit)
     with open(os.path.join(atomic_dir, codec.MODEL_JSON), "w") as f:

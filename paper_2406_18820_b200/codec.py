@@ -117,6 +117,59 @@ def read_payload_into(path: str, hdr: Header, dest: memoryview) -> None:
         raise TensorIOError(f"reading {path}: {e}") from e
 
 
+def read_range_into(path: str, file_off: int, dest: memoryview) -> None:
+    """pread ``len(dest)`` bytes at ``file_off`` (one chunk of a payload;
+    several chunks of one file are read by different threads)."""
+    try:
+        fd = os.open(path, os.O_RDONLY)
+        try:
+            got = 0
+            while got < len(dest):
+                n = os.preadv(fd, [dest[got:]], file_off + got)
+                if not n:
+                    raise TruncatedPayloadError(f"{path}: payload ended early")
+                got += n
+        finally:
+            os.close(fd)
+    except OSError as e:
+        raise TensorIOError(f"reading {path}: {e}") from e
+
+
+def payload_chunks(hdr: Header, chunk: int):
+    """(payload offset, nbytes) pieces of at most ``chunk`` bytes."""
+    if chunk <= 0 or hdr.nbytes <= chunk:
+        return [(0, hdr.nbytes)]
+    return [(o, min(chunk, hdr.nbytes - o)) for o in range(0, hdr.nbytes, chunk)]
+
+
+def create_raw(path: str, dtype: DType, shape, nbytes: int) -> int:
+    """Create a UCPT file of its final size with the header written; the
+    payload is filled by ``write_range`` (possibly from several threads).
+    Returns the payload offset."""
+    hb = header_bytes(dtype, shape)
+    try:
+        with open(path, "wb") as f:
+            f.write(hb)
+            f.truncate(len(hb) + nbytes)
+    except OSError as e:
+        raise TensorIOError(f"writing {path}: {e}") from e
+    return len(hb)
+
+
+def write_range(path: str, file_off: int, payload) -> None:
+    try:
+        fd = os.open(path, os.O_WRONLY)
+        try:
+            mv = memoryview(payload).cast("B")
+            done = 0
+            while done < len(mv):
+                done += os.pwritev(fd, [mv[done:]], file_off + done)
+        finally:
+            os.close(fd)
+    except OSError as e:
+        raise TensorIOError(f"writing {path}: {e}") from e
+
+
 def read_tensor(path: str) -> Tensor:
     hdr = read_header(path)
     arr = np.empty(hdr.numel, dtype=hdr.dtype.storage)

@@ -34,6 +34,9 @@ def main():
     import torch
 
     import paper_2406_18820_b200 as U
+    from paper_2406_18820_b200 import api as A
+
+    traces = {}
 
     spec, src, tgt, desc = U.bench_config(args.config, args.layers)
     S = 12 * spec.total_numel
@@ -50,9 +53,11 @@ def main():
         t = time.perf_counter()
         U.convert(src_dir, out, n_workers=args.workers)
         conv.append(time.perf_counter() - t)
+        traces["convert"] = dict(A.PIPE_TRACE)
         t = time.perf_counter()
         world = U.load(out, tgt)
         load.append(time.perf_counter() - t)
+        traces["load"] = dict(A.PIPE_TRACE)
         del world
         shutil.rmtree(out)
     res = {True: [], False: []}
@@ -62,6 +67,8 @@ def main():
             t = time.perf_counter()
             world = U.resume(src_dir, tgt, scratch, n_workers=args.workers, fused=fused)
             res[fused].append(time.perf_counter() - t)
+            if fused:
+                traces["resume_fused"] = dict(A.PIPE_TRACE)
             del world
             shutil.rmtree(scratch)
     c, lo = min(conv[1:]), min(load[1:])
@@ -73,7 +80,8 @@ def main():
         "convert_plus_load_GBps": S / (c + lo) / 1e9, "reps": args.reps,
         "resume_fused_s": rf, "resume_fused_GBps": S / rf / 1e9,
         "resume_two_pass_s": ru, "resume_two_pass_GBps": S / ru / 1e9,
-        "all_convert_s": conv, "all_load_s": load}))
+        "all_convert_s": conv, "all_load_s": load, "io_chunk": A.IO_CHUNK,
+        "pipeline_wait_s_last_rep": traces}))
     shutil.rmtree(args.root, ignore_errors=True)
 
 
