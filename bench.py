@@ -193,8 +193,10 @@ class CpuArm:
         u = self.ucp
         self.kind = "reference"
         self.spec = u.models.spec_from_dict(spec_to_dict(spec))
-        self.src = u.parse_config_string(format_config_string(src))
-        self.tgt = u.parse_config_string(format_config_string(tgt))
+        # ZeRO-2 (extension G1) lays out exactly like ZeRO-1, which the
+        # reference knows; vocab padding has no such equivalent (port above)
+        ref_cfg = lambda c: u.parse_config_string(format_config_string(c).replace(",z2,", ",z1,"))
+        self.src, self.tgt = ref_cfg(src), ref_cfg(tgt)
         RM, FM = u.parallel.RecordMeta, sys.modules["ucp.convert"].FragmentMsg
         meta = lambda m: RM(m.param, m.kind, m.pattern, tuple(m.placement), tuple(m.shape),
                             m.segments, m.flat_range, m.pad_elems)
