@@ -30,6 +30,9 @@ def main():
     ap.add_argument("--root", default="/dev/shm/ucpbench")
     ap.add_argument("--workers", type=int, default=os.cpu_count())
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"],
+                    help="reference: the unmodified reference's convert()/load() from "
+                         "baseline/_ref on the same source tree (same box, same tmpfs)")
     args = ap.parse_args()
     import torch
 
@@ -46,6 +49,9 @@ def main():
     t = time.perf_counter()
     U.partition(U.init_state(spec, 7), src, src_dir)
     t_part = time.perf_counter() - t
+    if args.impl == "reference":
+        run_reference(args, src_dir, tgt, S, desc, t_part)
+        return
     conv, load = [], []
     for r in range(args.reps + 1):
         out = os.path.join(args.root, f"atomic{r}")
@@ -82,6 +88,39 @@ def main():
         "resume_two_pass_s": ru, "resume_two_pass_GBps": S / ru / 1e9,
         "all_convert_s": conv, "all_load_s": load, "io_chunk": A.IO_CHUNK,
         "pipeline_wait_s_last_rep": traces}))
+    shutil.rmtree(args.root, ignore_errors=True)
+
+
+def run_reference(args, src_dir, tgt, S, desc, t_part):
+    """The reference's own file pipeline (ucp/convert.py:422, ucp/load.py:131)
+    with n_workers = the host's cores, on the tree our partition() wrote
+    (byte-identical to the reference's own, tests/golden src digests)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    sys.path.insert(0, ref)
+    import ucp
+
+    assert os.path.dirname(os.path.dirname(ucp.__file__)) == ref, ucp.__file__
+    import paper_2406_18820_b200 as U
+
+    rtgt = ucp.parse_config_string(U.format_config_string(tgt))
+    conv, load = [], []
+    for r in range(args.reps):
+        out = os.path.join(args.root, f"ref_atomic{r}")
+        t = time.perf_counter()
+        ucp.convert(src_dir, out, n_workers=args.workers)
+        conv.append(time.perf_counter() - t)
+        t = time.perf_counter()
+        world = ucp.load(out, rtgt)
+        load.append(time.perf_counter() - t)
+        del world
+        shutil.rmtree(out)
+    c, lo = min(conv), min(load)
+    print(json.dumps({
+        "impl": "reference", "workload": desc, "config": args.config, "state_bytes": S,
+        "root": args.root, "workers": args.workers, "partition_s": t_part,
+        "convert_s": c, "convert_GBps": S / c / 1e9, "load_s": lo, "load_GBps": S / lo / 1e9,
+        "convert_plus_load_GBps": S / (c + lo) / 1e9, "reps": args.reps,
+        "all_convert_s": conv, "all_load_s": load}))
     shutil.rmtree(args.root, ignore_errors=True)
 
 
