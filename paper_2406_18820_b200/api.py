@@ -460,6 +460,18 @@ def _chunks(nbytes: int, chunk: int = 0):
     return [(o, min(chunk, nbytes - o)) for o in range(0, nbytes, chunk)]
 
 
+def _coalesce(ranges, gap: int) -> list:
+    """Merge (offset, nbytes) ranges whose holes are at most ``gap`` bytes
+    into [offset, nbytes] runs (the holes are copied along)."""
+    runs = []
+    for at, n in sorted(ranges):
+        if runs and at - (runs[-1][0] + runs[-1][1]) <= gap:
+            runs[-1][1] = max(runs[-1][1], at + n - runs[-1][0])
+        else:
+            runs.append([at, n])
+    return runs
+
+
 def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
     """Windowed file pipeline, double-buffered so file reads of windows w
     and w+1 and the output handling of window w-1 overlap the GPU work of
@@ -520,12 +532,7 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
             return futs
 
         def send_rest(w, slot):
-            runs = []
-            for at, n in sorted(unsent.pop(w)):
-                if runs and at - (runs[-1][0] + runs[-1][1]) <= ALIGN_GAP:
-                    runs[-1][1] = at + n - runs[-1][0]
-                else:
-                    runs.append([at, n])
+            runs = _coalesce(unsent.pop(w), ALIGN_GAP)
             with torch.cuda.stream(s_h2d[slot]):
                 for at, n in runs:
                     d_src[slot][at:at + n].copy_(h_src[slot][at:at + n], non_blocking=True)
