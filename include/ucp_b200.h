@@ -21,7 +21,12 @@
  * group-major: source (g, k) is the k-th replica of group g; replicas must be
  * bit-identical to replica 0 of their group (strict replica check), groups
  * are averaged in f64 in ascending order (MEAN). The table is executed by a
- * grid of one CTA per tile; tiles never straddle runs.
+ * grid of one CTA per tile; tiles never straddle runs. Runs are sorted by
+ * kernel class; each run carries a ucp_runtile (its tile size and count),
+ * ucp_runtile_scan turns the counts into per-class tile offsets on the
+ * device (a block-wide scan built from warp shuffles), and each CTA finds
+ * its run with a warp-cooperative 32-ary search over those offsets, so no
+ * per-tile table exists in memory.
  *
  * Conventions: all pointers are device pointers, all calls are
  * stream-ordered and reentrant (no global state besides the caller's status
@@ -39,7 +44,7 @@
 extern "C" {
 #endif
 
-#define UCP_ABI_VERSION 1
+#define UCP_ABI_VERSION 2
 
 /* status / return codes (mirrored in paper_2406_18820_b200/_errors.py) */
 #define UCP_OK 0
@@ -60,7 +65,7 @@ extern "C" {
 #define UCP_DT_F16 1
 #define UCP_DT_BF16 2
 
-/* tile classes: tiles are sorted by class, each class runs its own kernel */
+/* kernel classes: runs are sorted by class, each class runs its own kernel */
 #define UCP_CLASS_VEC_F32 0   /* COPY, UCP_RUN_VEC, f32 destinations */
 #define UCP_CLASS_VEC_BF16 1  /* COPY, UCP_RUN_VEC, bf16 destinations */
 #define UCP_CLASS_VEC_F16 2   /* COPY, UCP_RUN_VEC, f16 destinations */
@@ -117,6 +122,18 @@ typedef struct ucp_xrun {
   uint32_t flags;      /* UCP_RUN_VEC is required; UCP_RUN_ROWSPLIT as for ucp_run */
 } ucp_xrun;            /* 64 bytes */
 
+/* Per-run tiling, parallel to the run array. The host fills per / tpr /
+ * ntiles; ucp_runtile_scan fills first. Tile k of a run covers
+ *   default:          rows [k*per, min((k+1)*per, rows)), all columns
+ *   UCP_RUN_ROWSPLIT: row k / tpr, columns [(k % tpr)*per, +per) clipped. */
+typedef struct ucp_runtile {
+  uint32_t first;      /* exclusive prefix of ntiles within the run's class */
+  uint32_t per;        /* rows per tile, or columns per tile (ROWSPLIT) */
+  uint32_t tpr;        /* tiles per row (ROWSPLIT), else 0 */
+  uint32_t ntiles;
+} ucp_runtile;         /* 16 bytes */
+
+/* A tile as one CTA derives it (device-internal; not stored anywhere). */
 typedef struct ucp_tile {
   uint32_t run;
   uint32_t row0;
@@ -137,13 +154,22 @@ int ucp_version(void);
 int ucp_status_reset(ucp_status* status, void* stream);
 
 /*
+ * Fill ucp_runtile.first: per class, the exclusive prefix sum of ntiles over
+ * the class's runs (one CTA per class, warp-shuffle scans). Call once after
+ * uploading a table; class_info is a HOST array of 2*UCP_NCLASS int64:
+ * tiles per class, then runs per class (runs sorted by class).
+ */
+int ucp_runtile_scan(ucp_runtile* rt, const int64_t* class_info, void* stream);
+
+/*
  * Consolidate fragments into atomic tensors (union). One launch covers any
  * number of (param, kind) units. src_base: base of the source-fragment arena;
- * dst_base: base of the atomic arena. aux: uint64 byte offsets. tiles: device
- * array sorted by class; class_counts: HOST array of UCP_NCLASS tile counts.
+ * dst_base: base of the atomic arena. aux: uint64 byte offsets. runs sorted by
+ * class, rt: their scanned ucp_runtile array (device); class_info: HOST array
+ * of 2*UCP_NCLASS int64 (tiles per class, then runs per class).
  */
 int ucp_convert_gather(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                       const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
+                       const ucp_runtile* rt, const int64_t* class_info, const void* src_base,
                        void* dst_base, ucp_status* status, void* stream);
 
 /*
@@ -151,7 +177,7 @@ int ucp_convert_gather(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
  * partial noise + weight cast), fanning each read out to n_dst replicas.
  */
 int ucp_load_scatter(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                     const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
+                     const ucp_runtile* rt, const int64_t* class_info, const void* src_base,
                      void* dst_base, ucp_status* status, void* stream);
 
 /*
@@ -164,11 +190,11 @@ int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, f
 
 /*
  * Fused convert + load (the in-memory resume() path, ucp/load.py:276-281):
- * class_counts has UCP_NCLASS entries; only the three VEC classes (target
- * dtype f32 / bf16 / f16) are valid, tiles sorted by class.
+ * class_info as for ucp_convert_gather; only the three VEC classes (target
+ * dtype f32 / bf16 / f16) may be non-empty, runs sorted by class.
  */
 int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
-                      const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
+                      const ucp_runtile* rt, const int64_t* class_info, const void* src_base,
                       void* atom_base, void* dst_base, ucp_status* status, void* stream);
 
 /*

@@ -26,6 +26,9 @@ from ._errors import (
     UcpError,
     UnsupportedCastError,
 )
+# the submodule import binds the package attribute `reshard` to the module;
+# it must precede `from .api import reshard`, which rebinds it to the function
+from .reshard import ReshardPlan  # noqa: E402  (isort: skip)
 from .api import (
     AtomicCheckpoint,
     FragmentMsg,
@@ -51,7 +54,6 @@ from .api import (
     ucp_info,
     union,
 )
-from .reshard import ReshardPlan
 from .codec import DistributedCheckpoint, load_checkpoint, read_manifest, read_tensor, write_tensor
 from .layout import (
     enumerate_rank_records,

@@ -18,10 +18,11 @@ LIB_PATH = os.environ.get("UCP_B200_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), LIB_NAME)  # env override: kernel A/B experiments
 
 # exported symbols declared in include/ucp_b200.h
-EXPORTS = ("ucp_version", "ucp_status_reset", "ucp_convert_gather", "ucp_load_scatter",
+EXPORTS = ("ucp_version", "ucp_status_reset", "ucp_runtile_scan", "ucp_convert_gather",
+           "ucp_load_scatter",
            "ucp_reshard_fused", "ucp_gen_state", "ucp_adam_step", "ucp_compare", "ucp_peek",
            "ucp_dev_alloc", "ucp_dev_free", "ucp_ipc_export", "ucp_ipc_open", "ucp_ipc_close")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 
@@ -30,6 +31,7 @@ _P = _c.c_void_p
 _SIGS = {
     "ucp_version": (_c.c_int, []),
     "ucp_status_reset": (_c.c_int, [_P, _P]),
+    "ucp_runtile_scan": (_c.c_int, [_P, _P, _P]),
     "ucp_convert_gather": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "ucp_load_scatter": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "ucp_reshard_fused": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -422,20 +422,64 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
 
 // ---------------------------------------------------------------- tile prologue
 
+// Largest r in [lo, hi) with rt[r].first <= b, given rt[lo].first == 0 <= b
+// and first non-decreasing: a warp-cooperative 32-ary search (each step one
+// coalesced probe per lane + a ballot), called by all 32 lanes of one warp.
+__device__ __forceinline__ uint32_t find_run(const ucp_runtile* __restrict__ rt, uint32_t lo,
+                                             uint32_t hi, uint32_t b) {
+  const uint32_t lane = threadIdx.x & 31;
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) >> 5;
+    const uint32_t idx = lo + lane * step;
+    const bool le = idx < hi && __ldg(&rt[idx].first) <= b;
+    const unsigned m = __ballot_sync(0xffffffffu, le);  // a prefix of the lanes
+    lo += (31u - (uint32_t)__clz((int)m)) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// Tile b of a class whose runs are [r0, r0 + nr): warp 0 finds the run and
+// stages it in shared memory; every thread then derives the tile rectangle
+// (the inverse of the host's per-run tiling, include/ucp_b200.h ucp_runtile).
+template <class R>
+__device__ __forceinline__ ucp_tile tile_begin(const R* __restrict__ runs,
+                                               const ucp_runtile* __restrict__ rt, uint32_t r0,
+                                               uint32_t nr, uint32_t b, R& s_run, uint4& s_t) {
+  static_assert(sizeof(R) == 64, "run records are 64 bytes");
+  if (threadIdx.x < 32) {
+    const uint32_t run = find_run(rt, r0, r0 + nr, b);
+    if (threadIdx.x < 4)
+      reinterpret_cast<uint4*>(&s_run)[threadIdx.x] = reinterpret_cast<const uint4*>(runs + run)[threadIdx.x];
+    if (threadIdx.x == 4) {
+      const ucp_runtile t = rt[run];
+      s_t = make_uint4(run, b - t.first, t.per, t.tpr);
+    }
+  }
+  __syncthreads();
+  const uint4 t = s_t;
+  ucp_tile tile;
+  tile.run = t.x;
+  if (s_run.flags & UCP_RUN_ROWSPLIT) {
+    tile.row0 = t.y / t.w;
+    tile.col0 = (t.y - tile.row0 * t.w) * t.z;
+    tile.count = min(t.z, s_run.cols - tile.col0);
+  } else {
+    tile.row0 = t.y * t.z;
+    tile.col0 = 0;
+    tile.count = min(t.z, s_run.rows - tile.row0);
+  }
+  return tile;
+}
+
 struct TileGeom {
   uint32_t row0, col0, nr, nc, spr, n_items;
 };
 
-// Load the tile's run (and its aux offsets) into shared memory.
-__device__ __forceinline__ TileGeom tile_prologue(const ucp_run* __restrict__ runs,
-                                                  const uint64_t* __restrict__ aux,
-                                                  const ucp_tile& tile, ucp_run& s_run,
+// Stage the run's aux offsets and return the tile's segment geometry.
+__device__ __forceinline__ TileGeom tile_prologue(const uint64_t* __restrict__ aux,
+                                                  const ucp_tile& tile, const ucp_run& s_run,
                                                   uint64_t* s_aux) {
-  if (threadIdx.x < 4) {
-    reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
-        reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
-  }
-  __syncthreads();
   const int n_aux = (s_run.n_src > 0 ? s_run.n_src - 1 : 0) + (s_run.n_dst > 0 ? s_run.n_dst - 1 : 0);
   if (n_aux > 0) {
     for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
@@ -449,6 +493,51 @@ __device__ __forceinline__ TileGeom tile_prologue(const ucp_run* __restrict__ ru
   g.spr = (g.nc + kSeg - 1) / kSeg;
   g.n_items = g.nr * g.spr;
   return g;
+}
+
+// Per-class exclusive prefix of ucp_runtile.ntiles (one CTA of 1024 threads
+// per class): warp inclusive scans with __shfl_up_sync, a scan of the 32
+// warp totals by warp 0, and a carry across 1024-run chunks.
+struct ClassRange {
+  uint32_t begin[UCP_NCLASS];
+  uint32_t n[UCP_NCLASS];
+};
+
+__global__ void __launch_bounds__(1024) runtile_scan_kernel(ucp_runtile* rt, ClassRange cr) {
+  const unsigned full = 0xffffffffu;
+  const uint32_t begin = cr.begin[blockIdx.x], n = cr.n[blockIdx.x];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < n; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t x = i < n ? rt[begin + i].ntiles : 0u;
+    uint32_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(full, v, o);
+      if ((int)lane >= o) v += y;
+    }
+    if (lane == 31) warp_sums[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(full, w, o);
+        if ((int)lane >= o) w += y;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t excl = carry + (warp ? warp_sums[warp - 1] : 0u) + v - x;
+    if (i < n) rt[begin + i].first = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + x;
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------- vector kernel
@@ -488,24 +577,33 @@ __device__ __forceinline__ int diff4(const float4& a, const float4& b) {
 template <int DT>
 __device__ __forceinline__ void vec_body(const ucp_run* __restrict__ runs,
                                          const uint64_t* __restrict__ aux,
-                                         const ucp_tile* __restrict__ tiles,
-                                         const char* __restrict__ sb, char* __restrict__ db,
-                                         ucp_status* st) {
+                                         const ucp_runtile* __restrict__ rt, uint32_t r0,
+                                         uint32_t nr, const char* __restrict__ sb,
+                                         char* __restrict__ db, ucp_status* st) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  __shared__ ucp_run s_run;
+  __shared__ __align__(16) ucp_run s_run;
+  __shared__ uint4 s_t;
   __shared__ uint64_t s_aux[kMaxAux];
-  const ucp_tile tile = tiles[blockIdx.x];
-  const TileGeom g = tile_prologue(runs, aux, tile, s_run, s_aux);
+  const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
   const int ns = s_run.n_src, nd = s_run.n_dst;
+  const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
+  if (n_aux > 0) {
+    for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
+    __syncthreads();
+  }
+  uint32_t tnr, tnc;
+  if (s_run.flags & UCP_RUN_ROWSPLIT) { tnr = 1; tnc = tile.count; }
+  else { tnr = tile.count; tnc = s_run.cols; }
+  const uint32_t spr = (tnc + kSeg - 1) / kSeg, n_items = tnr * spr;
   const uint64_t s0 = s_run.src, d0 = s_run.dst;
   const uint32_t sp = s_run.src_pitch, dpch = s_run.dst_pitch, cols = s_run.cols;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
-    const uint32_t rr = g.spr == 1 ? it : it / g.spr;
-    const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
-    const uint32_t len = min(cs + kSeg, g.col0 + g.nc) - cs;
-    const uint32_t row = g.row0 + rr;
+  for (uint32_t it = warp; it < n_items; it += kWarps) {
+    const uint32_t rr = spr == 1 ? it : it / spr;
+    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, tile.col0 + tnc) - cs;
+    const uint32_t row = tile.row0 + rr;
     const uint64_t srow = (uint64_t)row * sp + cs;
     const uint64_t drow = (uint64_t)row * dpch + cs;
     const uint32_t phase = (uint32_t)(((s0 >> 2) + srow) & 3);
@@ -569,13 +667,14 @@ __device__ __forceinline__ void vec_body(const ucp_run* __restrict__ runs,
 
 __device__ __forceinline__ void general_body(const ucp_run* __restrict__ runs,
                                              const uint64_t* __restrict__ aux,
-                                             const ucp_tile* __restrict__ tiles,
-                                             const char* __restrict__ sb, char* __restrict__ db,
-                                             ucp_status* st) {
-  __shared__ ucp_run s_run;
+                                             const ucp_runtile* __restrict__ rt, uint32_t r0,
+                                             uint32_t nr, const char* __restrict__ sb,
+                                             char* __restrict__ db, ucp_status* st) {
+  __shared__ __align__(16) ucp_run s_run;
+  __shared__ uint4 s_t;
   __shared__ uint64_t s_aux[kMaxAux];
-  const ucp_tile tile = tiles[blockIdx.x];
-  const TileGeom g = tile_prologue(runs, aux, tile, s_run, s_aux);
+  const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
+  const TileGeom g = tile_prologue(aux, tile, s_run, s_aux);
   const Ctx c{&s_run, s_aux, sb, db, tile.run};
   const uint32_t warp = threadIdx.x >> 5;
   for (uint32_t it = warp; it < g.n_items; it += kWarps) {
@@ -592,22 +691,15 @@ __device__ __forceinline__ void general_body(const ucp_run* __restrict__ runs,
 // verified, written once to the atomic tensor and once per target replica.
 // HBM traffic R_c + W_c + W_l instead of R_c + 2 S + W_l.
 
+// s_run is staged by tile_begin; s_aux here unless aux_loaded.
 template <int DT>
-__device__ __forceinline__ void fused_tile(const ucp_xrun* __restrict__ runs,
-                                           const uint64_t* __restrict__ aux,
-                                           const ucp_tile& tile, ucp_xrun& s_run,
+__device__ __forceinline__ void fused_tile(const uint64_t* __restrict__ aux,
+                                           const ucp_tile& tile, const ucp_xrun& s_run,
                                            uint64_t* s_aux,
                                            const char* __restrict__ sb, char* __restrict__ ab,
                                            char* __restrict__ db, ucp_status* st,
                                            bool preloaded = false) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  if (!preloaded) {
-    if (threadIdx.x < 4) {
-      reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
-          reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
-    }
-    __syncthreads();
-  }
   const int ns = s_run.n_src, nd = s_run.n_dst;
   const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
   if (n_aux > 0 && !preloaded) {
@@ -820,16 +912,18 @@ __device__ __forceinline__ bool fused_tile_tma(const ucp_xrun& r, const uint64_t
 template <int DT>
 __device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
                                            const uint64_t* __restrict__ aux,
-                                           const ucp_tile* __restrict__ tiles, uint32_t n_tiles,
+                                           const ucp_runtile* __restrict__ rt, uint32_t r0,
+                                           uint32_t nr, uint32_t n_tiles,
                                            const char* __restrict__ sb, char* __restrict__ ab,
                                            char* __restrict__ db, ucp_status* st) {
-  __shared__ ucp_xrun s_run;
+  __shared__ __align__(16) ucp_xrun s_run;
+  __shared__ uint4 s_t;
   __shared__ uint64_t s_aux[kMaxAux];
 #if UCP_PERSISTENT
-  // persistent CTAs walk the tile list; the barrier protects s_run / s_aux
+  // persistent CTAs walk the tiles; the barrier protects s_run / s_aux
   for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
-    const ucp_tile tile = tiles[ti];
-    fused_tile<DT>(runs, aux, tile, s_run, s_aux, sb, ab, db, st);
+    const ucp_tile tile = tile_begin(runs, rt, r0, nr, ti, s_run, s_t);
+    fused_tile<DT>(aux, tile, s_run, s_aux, sb, ab, db, st);
     __syncthreads();
   }
 #elif UCP_FUSED_TMA
@@ -841,38 +935,33 @@ __device__ __forceinline__ void fused_body(const ucp_xrun* __restrict__ runs,
     for (int i = 0; i < kTmaStages; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const ucp_tile tile = tiles[blockIdx.x];
-  if (threadIdx.x < 4) {
-    reinterpret_cast<uint4*>(&s_run)[threadIdx.x] =
-        reinterpret_cast<const uint4*>(runs + tile.run)[threadIdx.x];
-  }
-  __syncthreads();
+  const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
   const int n_aux = (s_run.n_src > 0 ? s_run.n_src - 1 : 0) + (s_run.n_dst > 0 ? s_run.n_dst - 1 : 0);
   for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
   __syncthreads();
   uint32_t uses = 0;
   if (DT != UCP_DT_F32 || !fused_tile_tma(s_run, s_aux, tile, sb, ab, db, st, buf, bars, uses))
-    fused_tile<DT>(runs, aux, tile, s_run, s_aux, sb, ab, db, st, true);
+    fused_tile<DT>(aux, tile, s_run, s_aux, sb, ab, db, st, true);
 #else
   (void)n_tiles;
-  const ucp_tile tile = tiles[blockIdx.x];
-  fused_tile<DT>(runs, aux, tile, s_run, s_aux, sb, ab, db, st);
+  const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
+  fused_tile<DT>(aux, tile, s_run, s_aux, sb, ab, db, st);
 #endif
 }
 
 #define UCP_FUSED_ARGS                                                                     \
   const ucp_xrun *__restrict__ runs, const uint64_t *__restrict__ aux,                      \
-      const ucp_tile *__restrict__ tiles, uint32_t n_tiles, const char *__restrict__ sb,     \
-      char *__restrict__ ab, char *__restrict__ db, ucp_status *st
+      const ucp_runtile *__restrict__ rt, uint32_t r0, uint32_t nr, uint32_t n_tiles,        \
+      const char *__restrict__ sb, char *__restrict__ ab, char *__restrict__ db, ucp_status *st
 
 __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f32(UCP_FUSED_ARGS) {
-  fused_body<UCP_DT_F32>(runs, aux, tiles, n_tiles, sb, ab, db, st);
+  fused_body<UCP_DT_F32>(runs, aux, rt, r0, nr, n_tiles, sb, ab, db, st);
 }
 __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_bf16(UCP_FUSED_ARGS) {
-  fused_body<UCP_DT_BF16>(runs, aux, tiles, n_tiles, sb, ab, db, st);
+  fused_body<UCP_DT_BF16>(runs, aux, rt, r0, nr, n_tiles, sb, ab, db, st);
 }
 __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f16(UCP_FUSED_ARGS) {
-  fused_body<UCP_DT_F16>(runs, aux, tiles, n_tiles, sb, ab, db, st);
+  fused_body<UCP_DT_F16>(runs, aux, rt, r0, nr, n_tiles, sb, ab, db, st);
 }
 
 // ---------------------------------------------------------------- entry kernels
@@ -882,26 +971,26 @@ __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f16(UCP_FUSE
 
 #define UCP_MOVE_ARGS                                                                      \
   const ucp_run *__restrict__ runs, const uint64_t *__restrict__ aux,                        \
-      const ucp_tile *__restrict__ tiles, const char *__restrict__ sb, char *__restrict__ db, \
-      ucp_status *st
+      const ucp_runtile *__restrict__ rt, uint32_t r0, uint32_t nr, const char *__restrict__ sb, \
+      char *__restrict__ db, ucp_status *st
 
 __global__ void __launch_bounds__(kThreads, UCP_MINB) convert_gather_f32(UCP_MOVE_ARGS) {
-  vec_body<UCP_DT_F32>(runs, aux, tiles, sb, db, st);
+  vec_body<UCP_DT_F32>(runs, aux, rt, r0, nr, sb, db, st);
 }
 __global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_f32(UCP_MOVE_ARGS) {
-  vec_body<UCP_DT_F32>(runs, aux, tiles, sb, db, st);
+  vec_body<UCP_DT_F32>(runs, aux, rt, r0, nr, sb, db, st);
 }
 __global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_bf16(UCP_MOVE_ARGS) {
-  vec_body<UCP_DT_BF16>(runs, aux, tiles, sb, db, st);
+  vec_body<UCP_DT_BF16>(runs, aux, rt, r0, nr, sb, db, st);
 }
 __global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_f16(UCP_MOVE_ARGS) {
-  vec_body<UCP_DT_F16>(runs, aux, tiles, sb, db, st);
+  vec_body<UCP_DT_F16>(runs, aux, rt, r0, nr, sb, db, st);
 }
 __global__ void __launch_bounds__(kThreads) convert_gather_general(UCP_MOVE_ARGS) {
-  general_body(runs, aux, tiles, sb, db, st);
+  general_body(runs, aux, rt, r0, nr, sb, db, st);
 }
 __global__ void __launch_bounds__(kThreads) load_scatter_general(UCP_MOVE_ARGS) {
-  general_body(runs, aux, tiles, sb, db, st);
+  general_body(runs, aux, rt, r0, nr, sb, db, st);
 }
 
 // ---------------------------------------------------------------- generator
@@ -976,41 +1065,51 @@ compare_kernel(const unsigned char* a, const unsigned char* b, uint64_t n,
   }
 }
 
-int launch_move(bool gather, const ucp_run* runs, int64_t n_runs, const uint64_t* aux, const ucp_tile* tiles,
-                const int64_t* class_counts, const void* src_base, void* dst_base,
-                ucp_status* status, void* stream) {
-  if (n_runs < 0 || !class_counts) return UCP_EINVAL;
-  int64_t total = 0;
+// class_info (host): tiles per class, then runs per class; runs sorted by
+// class. Fills per-class run ranges and tile counts; false on bad input.
+bool parse_classes(const int64_t* class_info, int64_t n_runs, ClassRange& cr, uint32_t* nt) {
+  if (!class_info || n_runs < 0) return false;
+  int64_t r = 0;
   for (int c = 0; c < UCP_NCLASS; ++c) {
-    if (class_counts[c] < 0 || class_counts[c] > 0x7fffffffLL) return UCP_EINVAL;
-    total += class_counts[c];
+    const int64_t t = class_info[c], n = class_info[UCP_NCLASS + c];
+    if (t < 0 || t > 0x7fffffffLL || n < 0 || (t > 0 && n == 0)) return false;
+    cr.begin[c] = (uint32_t)r;
+    cr.n[c] = (uint32_t)n;
+    nt[c] = (uint32_t)t;
+    r += n;
   }
-  if (total == 0) return UCP_OK;
-  if (!runs || !tiles || !status) return UCP_EINVAL;
+  return r == n_runs && r <= 0xffffffffLL;
+}
+
+int launch_move(bool gather, const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
+                const ucp_runtile* rt, const int64_t* class_info, const void* src_base,
+                void* dst_base, ucp_status* status, void* stream) {
+  ClassRange cr;
+  uint32_t nt[UCP_NCLASS];
+  if (!parse_classes(class_info, n_runs, cr, nt)) return UCP_EINVAL;
+  if (nt[0] + nt[1] + nt[2] + nt[3] == 0) return UCP_OK;
+  if (!runs || !rt || !status) return UCP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const char* sb = static_cast<const char*>(src_base);
   char* db = static_cast<char*>(dst_base);
-  int64_t at = 0;
   for (int c = 0; c < UCP_NCLASS; ++c) {
-    const int64_t n = class_counts[c];
-    if (n == 0) continue;
-    const dim3 grid((unsigned)n), block(kThreads);
-    const ucp_tile* t = tiles + at;
+    if (nt[c] == 0) continue;
+    const dim3 grid(nt[c]), block(kThreads);
+    const uint32_t r0 = cr.begin[c], nr = cr.n[c];
     if (gather) {
       switch (c) {
-        case UCP_CLASS_VEC_F32: convert_gather_f32<<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
-        case UCP_CLASS_GENERAL: convert_gather_general<<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
+        case UCP_CLASS_VEC_F32: convert_gather_f32<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
+        case UCP_CLASS_GENERAL: convert_gather_general<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
         default: return UCP_EINVAL;  // convert writes f32 atomics only
       }
     } else {
       switch (c) {
-        case UCP_CLASS_VEC_F32: load_scatter_f32<<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
-        case UCP_CLASS_VEC_BF16: load_scatter_bf16<<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
-        case UCP_CLASS_VEC_F16: load_scatter_f16<<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
-        default: load_scatter_general<<<grid, block, 0, s>>>(runs, aux, t, sb, db, status); break;
+        case UCP_CLASS_VEC_F32: load_scatter_f32<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
+        case UCP_CLASS_VEC_BF16: load_scatter_bf16<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
+        case UCP_CLASS_VEC_F16: load_scatter_f16<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
+        default: load_scatter_general<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
       }
     }
-    at += n;
   }
   return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
 }
@@ -1040,46 +1139,55 @@ int ucp_status_reset(ucp_status* status, void* stream) {
   return UCP_OK;
 }
 
+int ucp_runtile_scan(ucp_runtile* rt, const int64_t* class_info, void* stream) {
+  if (!class_info) return UCP_EINVAL;
+  ClassRange cr;
+  uint32_t nt[UCP_NCLASS];
+  int64_t n_runs = 0;
+  for (int c = 0; c < UCP_NCLASS; ++c) n_runs += class_info[UCP_NCLASS + c] > 0 ? class_info[UCP_NCLASS + c] : 0;
+  if (!parse_classes(class_info, n_runs, cr, nt)) return UCP_EINVAL;
+  if (n_runs == 0) return UCP_OK;
+  if (!rt) return UCP_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  runtile_scan_kernel<<<UCP_NCLASS, 1024, 0, s>>>(rt, cr);
+  return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
+}
+
 int ucp_convert_gather(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                       const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
+                       const ucp_runtile* rt, const int64_t* class_info, const void* src_base,
                        void* dst_base, ucp_status* status, void* stream) {
-  return launch_move(true, runs, n_runs, aux, tiles, class_counts, src_base, dst_base, status, stream);
+  return launch_move(true, runs, n_runs, aux, rt, class_info, src_base, dst_base, status, stream);
 }
 
 int ucp_load_scatter(const ucp_run* runs, int64_t n_runs, const uint64_t* aux,
-                     const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
+                     const ucp_runtile* rt, const int64_t* class_info, const void* src_base,
                      void* dst_base, ucp_status* status, void* stream) {
-  return launch_move(false, runs, n_runs, aux, tiles, class_counts, src_base, dst_base, status, stream);
+  return launch_move(false, runs, n_runs, aux, rt, class_info, src_base, dst_base, status, stream);
 }
 
 int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
-                      const ucp_tile* tiles, const int64_t* class_counts, const void* src_base,
+                      const ucp_runtile* rt, const int64_t* class_info, const void* src_base,
                       void* atom_base, void* dst_base, ucp_status* status, void* stream) {
-  if (n_runs < 0 || !class_counts) return UCP_EINVAL;
-  int64_t total = 0;
-  for (int c = 0; c < UCP_NCLASS; ++c) {
-    if (class_counts[c] < 0 || class_counts[c] > 0x7fffffffLL) return UCP_EINVAL;
-    total += class_counts[c];
-  }
-  if (class_counts[UCP_CLASS_GENERAL] != 0) return UCP_EINVAL;
-  if (total == 0) return UCP_OK;
-  if (!runs || !tiles || !status) return UCP_EINVAL;
+  ClassRange cr;
+  uint32_t nt[UCP_NCLASS];
+  if (!parse_classes(class_info, n_runs, cr, nt)) return UCP_EINVAL;
+  if (nt[UCP_CLASS_GENERAL] != 0) return UCP_EINVAL;
+  if (nt[0] + nt[1] + nt[2] == 0) return UCP_OK;
+  if (!runs || !rt || !status) return UCP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const char* sb = static_cast<const char*>(src_base);
   char* ab = static_cast<char*>(atom_base);
   char* db = static_cast<char*>(dst_base);
-  int64_t at = 0;
   for (int c = 0; c < UCP_CLASS_GENERAL; ++c) {
-    const int64_t n = class_counts[c];
+    const uint32_t n = nt[c];
     if (n == 0) continue;
 #if UCP_PERSISTENT
-    const unsigned g = (unsigned)(n < (int64_t)148 * UCP_MINB ? n : (int64_t)148 * UCP_MINB);
+    const unsigned g = n < 148u * UCP_MINB ? n : 148u * UCP_MINB;
 #else
-    const unsigned g = (unsigned)n;
+    const unsigned g = n;
 #endif
     const dim3 grid(g), block(kThreads);
-    const ucp_tile* t = tiles + at;
-    const uint32_t nt = (uint32_t)n;
+    const uint32_t r0 = cr.begin[c], nr = cr.n[c];
 #if UCP_FUSED_TMA
     static bool attr_set = false;
     if (!attr_set) {
@@ -1092,10 +1200,9 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
 #else
     const size_t dsm = 0;
 #endif
-    if (c == UCP_CLASS_VEC_F32) reshard_fused_f32<<<grid, block, dsm, s>>>(runs, aux, t, nt, sb, ab, db, status);
-    else if (c == UCP_CLASS_VEC_BF16) reshard_fused_bf16<<<grid, block, dsm, s>>>(runs, aux, t, nt, sb, ab, db, status);
-    else reshard_fused_f16<<<grid, block, dsm, s>>>(runs, aux, t, nt, sb, ab, db, status);
-    at += n;
+    if (c == UCP_CLASS_VEC_F32) reshard_fused_f32<<<grid, block, dsm, s>>>(runs, aux, rt, r0, nr, n, sb, ab, db, status);
+    else if (c == UCP_CLASS_VEC_BF16) reshard_fused_bf16<<<grid, block, dsm, s>>>(runs, aux, rt, r0, nr, n, sb, ab, db, status);
+    else reshard_fused_f16<<<grid, block, dsm, s>>>(runs, aux, rt, r0, nr, n, sb, ab, db, status);
   }
   return cudaGetLastError() == cudaSuccess ? UCP_OK : UCP_ECUDA;
 }

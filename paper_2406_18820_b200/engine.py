@@ -13,7 +13,7 @@ import torch
 
 from . import _native
 from ._errors import NativeUnavailableError, PaddingError, ReplicateMismatchError, from_status
-from .plan import OP_CHECKZERO, RunTable
+from .plan import NCLASS, OP_CHECKZERO, RunTable, expand_tiles
 
 ALIGN = 256  # byte alignment of every fragment / atomic / target buffer
 
@@ -42,29 +42,50 @@ def _check(rc: int, what: str) -> None:
         raise from_status(rc, what)
 
 
-class Program:
-    """One kernel launch worth of runs/aux/tiles, resident on a device."""
+class _Table:
+    """Runs (sorted by kernel class) + aux + scanned ucp_runtile array,
+    resident on a device. No per-tile table: each CTA derives its tile
+    (include/ucp_b200.h, ucp_runtile)."""
 
-    def __init__(self, table: RunTable, device: torch.device, tile_bytes: int = 1 << 17):
-        runs, aux, tiles, counts = table.finish_classed(tile_bytes)
-        self.runs_host, self.aux_host, self.tiles_host = runs, aux, tiles
-        self.class_counts = np.ascontiguousarray(counts, dtype=np.int64)
-        self.units = table.units
-        self.src_bytes, self.dst_bytes = table.src_bytes, table.dst_bytes
-        self.n_runs, self.n_tiles = len(runs), len(tiles)
+    def _upload(self, runs, aux, rt, info, order, device, run_bytes: int) -> None:
+        self.runs_host, self.aux_host, self.rt_host, self.run_order = runs, aux, rt, order
+        self.class_info = np.ascontiguousarray(info, dtype=np.int64)
+        self.n_runs, self.n_tiles = len(runs), int(self.class_info[:NCLASS].sum())
         self.device = device
         blob = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).to(device)
-        self._runs = blob(runs) if len(runs) else torch.zeros(64, dtype=torch.uint8, device=device)
+        self._runs = blob(runs) if len(runs) else torch.zeros(run_bytes, dtype=torch.uint8, device=device)
         self._aux = blob(aux)
-        self._tiles = blob(tiles) if len(tiles) else torch.zeros(16, dtype=torch.uint8, device=device)
+        rt_dev = rt.copy()
+        rt_dev["first"] = 0xFFFFFFFF  # written by the device scan below
+        self._rt = blob(rt_dev) if len(rt) else torch.zeros(16, dtype=torch.uint8, device=device)
+        if len(rt):
+            with torch.cuda.device(device):
+                _check(_native.lib().ucp_runtile_scan(self._rt.data_ptr(),
+                                                      self.class_info.ctypes.data,
+                                                      stream_ptr(None)), "runtile_scan")
+
+    @property
+    def tiles_host(self) -> np.ndarray:
+        """Every tile as the kernels derive it (tests / diagnostics)."""
+        return expand_tiles(self.runs_host, self.rt_host)
+
+    @property
+    def n_launches(self) -> int:
+        return int((self.class_info[:NCLASS] > 0).sum())
+
+
+class Program(_Table):
+    """One ucp_convert_gather / ucp_load_scatter worth of runs on a device."""
+
+    def __init__(self, table: RunTable, device: torch.device, tile_bytes: int = 1 << 17):
+        runs, aux, rt, info, order = table.finish_classed(tile_bytes)
+        self.units = table.units
+        self.src_bytes, self.dst_bytes = table.src_bytes, table.dst_bytes
+        self._upload(runs, aux, rt, info, order, device, 64)
 
     @property
     def bytes_moved(self) -> int:
         return self.src_bytes + self.dst_bytes
-
-    @property
-    def n_launches(self) -> int:
-        return int((self.class_counts > 0).sum())
 
     def launch(self, gather: bool, src_base: int, dst_base: int, status: "Status",
                stream: torch.cuda.Stream | None = None) -> None:
@@ -72,44 +93,33 @@ class Program:
             return
         lib = _native.lib()
         fn = lib.ucp_convert_gather if gather else lib.ucp_load_scatter
-        rc = fn(self._runs.data_ptr(), self.n_runs, self._aux.data_ptr(), self._tiles.data_ptr(),
-                self.class_counts.ctypes.data, ctypes.c_void_p(src_base),
+        rc = fn(self._runs.data_ptr(), self.n_runs, self._aux.data_ptr(), self._rt.data_ptr(),
+                self.class_info.ctypes.data, ctypes.c_void_p(src_base),
                 ctypes.c_void_p(dst_base), status.ptr, stream_ptr(stream))
         _check(rc, "convert_gather" if gather else "load_scatter")
 
 
-class XProgram:
+class XProgram(_Table):
     """One ucp_reshard_fused launch: fused convert+load runs on a device."""
 
     def __init__(self, table, device: torch.device, tile_bytes: int = 1 << 17):
-        runs, aux, tiles, counts = table.finish_classed(tile_bytes)
-        self.runs_host, self.aux_host, self.tiles_host = runs, aux, tiles
-        self.class_counts = np.ascontiguousarray(counts, dtype=np.int64)
+        runs, aux, rt, info, order = table.finish_classed(tile_bytes)
         self.units = table.units
         self.src_bytes, self.atom_bytes, self.dst_bytes = (table.src_bytes, table.atom_bytes,
                                                            table.dst_bytes)
-        self.n_runs, self.n_tiles = len(runs), len(tiles)
-        self.device = device
-        blob = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).to(device)
-        self._runs = blob(runs) if len(runs) else torch.zeros(64, dtype=torch.uint8, device=device)
-        self._aux = blob(aux)
-        self._tiles = blob(tiles) if len(tiles) else torch.zeros(16, dtype=torch.uint8, device=device)
+        self._upload(runs, aux, rt, info, order, device, 64)
 
     @property
     def bytes_moved(self) -> int:
         return self.src_bytes + self.atom_bytes + self.dst_bytes
-
-    @property
-    def n_launches(self) -> int:
-        return int((self.class_counts > 0).sum())
 
     def launch(self, src_base: int, atom_base: int, dst_base: int, status: "Status",
                stream: torch.cuda.Stream | None = None) -> None:
         if self.n_tiles == 0:
             return
         rc = _native.lib().ucp_reshard_fused(
-            self._runs.data_ptr(), self.n_runs, self._aux.data_ptr(), self._tiles.data_ptr(),
-            self.class_counts.ctypes.data, ctypes.c_void_p(src_base), ctypes.c_void_p(atom_base),
+            self._runs.data_ptr(), self.n_runs, self._aux.data_ptr(), self._rt.data_ptr(),
+            self.class_info.ctypes.data, ctypes.c_void_p(src_base), ctypes.c_void_p(atom_base),
             ctypes.c_void_p(dst_base), status.ptr, stream_ptr(stream))
         _check(rc, "reshard_fused")
 
@@ -151,7 +161,7 @@ def describe_failure(prog: Program, run_idx: int, elem: int, src_base: int) -> E
     fused = "atom" in r.dtype.names
     if not fused and int(r["op"]) == OP_CHECKZERO:
         return PaddingError(f"{where}: nonzero pad tail (first bad element {elem})")
-    labels = unit.labels.get(run_idx)
+    labels = unit.labels.get(int(prog.run_order[run_idx]))  # keyed by table index
     row, col = divmod(elem, int(r["cols"]))
     n_src, groups = int(r["n_src"]), 1 if fused else max(int(r["groups"]), 1)
     K = n_src // groups

@@ -72,6 +72,9 @@ RUN_DTYPE = np.dtype({
     "itemsize": 64,
 })
 TILE_DTYPE = np.dtype([("run", "<u4"), ("row0", "<u4"), ("col0", "<u4"), ("count", "<u4")])
+# ucp_runtile (include/ucp_b200.h): per-run tiling; `first` is filled on the
+# device by ucp_runtile_scan (host copies keep it for the interpreter)
+RUNTILE_DTYPE = np.dtype([("first", "<u4"), ("per", "<u4"), ("tpr", "<u4"), ("ntiles", "<u4")])
 XRUN_DTYPE = np.dtype({
     "names": ["src", "atom", "dst", "src_pitch", "atom_pitch", "dst_pitch", "rows", "cols", "aux",
               "n_src", "n_dst", "dtype", "tag", "flags"],
@@ -180,25 +183,27 @@ class RunTable:
     def __len__(self):
         return len(self._rows)
 
-    def finish(self, tile_bytes: int = 1 << 17):
+    def finish(self, tile_bytes: int = 1 << 17) -> tuple:
+        """(runs, aux, tiles) in table order, tiles expanded on the host
+        (tests and the interpreter; the kernels derive them per CTA)."""
+        runs, aux = self._runs_aux()
+        return runs, aux, expand_tiles(runs, make_runtiles(runs, tile_bytes))
+
+    def _runs_aux(self) -> tuple:
         runs = np.zeros(len(self._rows), dtype=RUN_DTYPE)
         if self._rows:
             cols = list(zip(*self._rows))
             for name, vals in zip(RUN_DTYPE.names, cols):
                 runs[name] = vals
         aux = np.asarray(self._aux if self._aux else [0], dtype=np.uint64)
-        tiles = make_tiles(runs, tile_bytes)
-        return runs, aux, tiles
+        return runs, aux
 
     def finish_classed(self, tile_bytes: int = 1 << 17):
-        """(runs, aux, tiles sorted by kernel class, per-class tile counts)."""
-        runs, aux, tiles = self.finish(tile_bytes)
-        cls = run_classes(runs)
-        tcls = cls[tiles["run"]] if len(tiles) else np.zeros(0, dtype=np.int64)
-        order = np.argsort(tcls, kind="stable")
-        counts = np.bincount(tcls, minlength=NCLASS).astype(np.int64) if len(tiles) else \
-            np.zeros(NCLASS, dtype=np.int64)
-        return runs, aux, tiles[order], counts
+        """(runs sorted by kernel class, aux, their ucp_runtile array,
+        class_info = tiles per class then runs per class, sorted -> table
+        index). Run order within a class is table order."""
+        runs, aux = self._runs_aux()
+        return classed(runs, aux, run_classes(runs), tile_bytes)
 
 
 def run_classes(runs: np.ndarray) -> np.ndarray:
@@ -211,11 +216,16 @@ def run_classes(runs: np.ndarray) -> np.ndarray:
     return np.where(vec, by_dt, CLASS_GENERAL).astype(np.int64)
 
 
-def make_tiles(runs: np.ndarray, tile_bytes: int, extra_bpe=None) -> np.ndarray:
-    """One CTA per tile; a tile never straddles runs. Tile size is
-    normalised by bytes moved per element so tiles cost about the same."""
+def make_runtiles(runs: np.ndarray, tile_bytes: int, extra_bpe=None) -> np.ndarray:
+    """Per-run tiling (ucp_runtile), one CTA per tile; a tile never
+    straddles runs. Tile size is normalised by bytes moved per element so
+    tiles cost about the same. Runs wider than a tile are cut into column
+    tiles of single rows (UCP_RUN_ROWSPLIT, set here); the others into
+    blocks of whole rows. ``first`` is the exclusive prefix of ``ntiles`` in
+    array order (the device recomputes it per class, ucp_runtile_scan)."""
+    rt = np.zeros(len(runs), dtype=RUNTILE_DTYPE)
     if len(runs) == 0:
-        return np.zeros(0, dtype=TILE_DTYPE)
+        return rt
     esz = np.where(runs["dtype"] == 0, 4, 2).astype(np.int64)
     bpe = 4 * runs["n_src"].astype(np.int64) + esz * runs["n_dst"].astype(np.int64)
     if extra_bpe is not None:
@@ -226,40 +236,69 @@ def make_tiles(runs: np.ndarray, tile_bytes: int, extra_bpe=None) -> np.ndarray:
     cols = runs["cols"].astype(np.int64)
     split = cols > telems
     runs["flags"] = np.where(split, runs["flags"] | RUN_ROWSPLIT, runs["flags"] & ~np.uint32(RUN_ROWSPLIT))
-    out = []
-    idx = np.arange(len(runs))
-    # column-split runs: rows * ceil(cols / telems) tiles
-    for i in idx[split]:
-        tpr = -(-cols[i] // telems[i])
-        c0 = np.arange(tpr, dtype=np.int64) * telems[i]
-        cnt = np.minimum(telems[i], cols[i] - c0)
-        r = np.repeat(np.arange(rows[i], dtype=np.int64), tpr)
-        t = np.zeros(len(r), dtype=TILE_DTYPE)
-        t["run"] = i
-        t["row0"] = r
-        t["col0"] = np.tile(c0, rows[i])
-        t["count"] = np.tile(cnt, rows[i])
-        out.append(t)
-    # row-block runs
-    whole = idx[~split]
-    if len(whole):
-        rpt = np.maximum(1, telems[whole] // np.maximum(cols[whole], 1))
-        ntile = -(-rows[whole] // rpt)
-        run_of = np.repeat(whole, ntile)
-        first = np.repeat(np.cumsum(ntile) - ntile, ntile)
-        k = np.arange(len(run_of)) - first
-        rp = np.repeat(rpt, ntile)
-        t = np.zeros(len(run_of), dtype=TILE_DTYPE)
-        t["run"] = run_of
-        t["row0"] = k * rp
-        t["col0"] = 0
-        t["count"] = np.minimum(rp, rows[run_of] - k * rp)
-        out.append(t)
-    tiles = np.concatenate(out) if out else np.zeros(0, dtype=TILE_DTYPE)
-    # interleave big and small runs' tiles? keep run order: it is the order
-    # of the destination buffers, which keeps writes sequential per run
-    order = np.argsort(tiles["run"], kind="stable")
-    return tiles[order]
+    tpr = np.where(split, -(-cols // telems), 0)
+    rpt = np.maximum(1, telems // np.maximum(cols, 1))
+    rt["per"] = np.where(split, telems, rpt)
+    rt["tpr"] = tpr
+    ntiles = np.where(split, rows * tpr, -(-rows // rpt))
+    if ntiles.sum() >= 1 << 31:
+        raise ValueError("too many tiles for one launch; use smaller windows")
+    rt["ntiles"] = ntiles
+    rt["first"] = np.cumsum(ntiles) - ntiles
+    return rt
+
+
+def make_tiles(runs: np.ndarray, tile_bytes: int, extra_bpe=None) -> np.ndarray:
+    """Expanded tile list of runs in table order (host-side view)."""
+    return expand_tiles(runs, make_runtiles(runs, tile_bytes, extra_bpe))
+
+
+def expand_tiles(runs: np.ndarray, rt: np.ndarray) -> np.ndarray:
+    """Every tile of a classed table as the kernels derive it per CTA
+    (ucp_tile: run, row0, col0, count), in launch order. Host mirror of
+    tile_begin() in csrc/ucp_b200.cu, for the interpreter and the tests."""
+    n = rt["ntiles"].astype(np.int64)
+    run = np.repeat(np.arange(len(runs), dtype=np.int64), n)
+    k = np.arange(int(n.sum()), dtype=np.int64) - np.repeat(np.cumsum(n) - n, n)
+    per = rt["per"].astype(np.int64)[run]
+    tpr = rt["tpr"].astype(np.int64)[run]
+    split = (runs["flags"][run] & RUN_ROWSPLIT) != 0
+    t = np.zeros(len(run), dtype=TILE_DTYPE)
+    t["run"] = run
+    row0 = np.where(split, k // np.maximum(tpr, 1), k * per)
+    col0 = np.where(split, (k - row0 * np.maximum(tpr, 1)) * per, 0)
+    t["row0"] = row0
+    t["col0"] = col0
+    t["count"] = np.where(split, np.minimum(per, runs["cols"][run].astype(np.int64) - col0),
+                          np.minimum(per, runs["rows"][run].astype(np.int64) - row0))
+    return t
+
+
+def classed(runs: np.ndarray, aux: np.ndarray, cls: np.ndarray, tile_bytes: int,
+            extra_bpe=None) -> tuple:
+    """Stable-sort runs by kernel class and tile them: (runs, aux, rt,
+    class_info[2 * NCLASS] = tiles per class, then runs per class, order)
+    with order[i] = table index of sorted run i (run labels are keyed by
+    table index)."""
+    order = np.argsort(cls, kind="stable")
+    runs = runs[order]
+    cls = cls[order]
+    extra = None if extra_bpe is None else np.asarray(extra_bpe)[order]
+    rt = make_runtiles(runs, tile_bytes, extra)
+    info = np.zeros(2 * NCLASS, dtype=np.int64)
+    nt = rt["ntiles"].astype(np.int64)
+    for c in range(NCLASS):
+        sel = cls == c
+        info[c] = int(nt[sel].sum())
+        info[NCLASS + c] = int(sel.sum())
+    # per-class exclusive prefix, as ucp_runtile_scan computes it on the device
+    start = 0
+    for c in range(NCLASS):
+        n = int(info[NCLASS + c])
+        seg = nt[start:start + n]
+        rt["first"][start:start + n] = np.cumsum(seg) - seg
+        start += n
+    return runs, aux, rt, info, order
 
 
 # --------------------------------------------------------------------------- geometry
@@ -677,14 +716,9 @@ class XRunTable:
                 runs[name] = vals
         aux = np.asarray(self._aux if self._aux else [0], dtype=np.uint64)
         extra = np.where(runs["atom"] == np.uint64(NO_ATOM), 0, 4).astype(np.int64)
-        tiles = make_tiles(runs, tile_bytes, extra)
         cls = np.select([runs["dtype"] == DType.F32.value, runs["dtype"] == DType.BF16.value],
                         [CLASS_VEC_F32, CLASS_VEC_BF16], CLASS_VEC_F16).astype(np.int64)
-        tcls = cls[tiles["run"]] if len(tiles) else np.zeros(0, dtype=np.int64)
-        order = np.argsort(tcls, kind="stable")
-        counts = np.bincount(tcls, minlength=NCLASS).astype(np.int64) if len(tiles) else \
-            np.zeros(NCLASS, dtype=np.int64)
-        return runs, aux, tiles[order], counts
+        return classed(runs, aux, cls, tile_bytes, extra)
 
 
 def _rects(x0, xp, rows, cols, exts, ep, esz, R, W):

@@ -32,7 +32,7 @@ def test_native_loaded_and_device_present():
     assert torch.cuda.is_available()
     from paper_2406_18820_b200 import _native
 
-    assert _native.lib().ucp_version() == 1
+    assert _native.lib().ucp_version() == _native.ABI_VERSION
 
 
 def test_gen_kernel_matches_golden(golden):

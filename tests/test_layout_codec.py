@@ -149,3 +149,14 @@ def test_error_tree():
                 U.MissingFragmentError, U.OverlappingRangeError, U.CheckpointLayoutError,
                 U.IncompatibleConfigError, U.PatternCoverageError, U.UnsupportedCastError):
         assert issubclass(cls, U.UcpError)
+
+
+def test_public_names_are_the_api_functions():
+    """Submodule imports must not shadow the drop-in functions of the same
+    name (e.g. the `reshard` module vs the `reshard()` entry point)."""
+    import inspect
+
+    for name in ("convert", "load", "resume", "union", "extract_fragment", "reshard", "partition",
+                 "init_state", "ucp_info", "cast", "load_atomic", "consolidate_world"):
+        assert inspect.isfunction(getattr(U, name)), name
+    assert inspect.isclass(U.ReshardPlan)

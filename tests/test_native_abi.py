@@ -8,7 +8,7 @@ import re
 import numpy as np
 
 from paper_2406_18820_b200 import _native
-from paper_2406_18820_b200.plan import RUN_DTYPE, TILE_DTYPE
+from paper_2406_18820_b200.plan import RUN_DTYPE, RUNTILE_DTYPE, TILE_DTYPE
 
 HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
                    "ucp_b200.h")
@@ -41,18 +41,26 @@ def test_abi_constants_match_header():
     assert int(consts["UCP_NCLASS"]) == plan.NCLASS
     assert int(consts["UCP_CLASS_GENERAL"]) == plan.CLASS_GENERAL
     assert int(consts["UCP_CLASS_VEC_BF16"]) == plan.CLASS_VEC_BF16
-    assert RUN_DTYPE.itemsize == 64 and TILE_DTYPE.itemsize == 16
+    assert RUN_DTYPE.itemsize == 64 and TILE_DTYPE.itemsize == 16 and RUNTILE_DTYPE.itemsize == 16
 
 
 def test_argument_errors_without_device():
     lib = _native.load_library()
     # invalid arguments are rejected before any CUDA call
     import numpy as np
-    bad = np.array([0, -1, 0, 0], dtype=np.int64)
-    zero = np.zeros(4, dtype=np.int64)
+    bad = np.array([0, -1, 0, 0] + [0] * 4, dtype=np.int64)
+    zero = np.zeros(8, dtype=np.int64)
+    tiles_without_runs = np.array([5, 0, 0, 0] + [0] * 4, dtype=np.int64)
+    runs_mismatch = np.array([0] * 4 + [2, 0, 0, 0], dtype=np.int64)  # n_runs passed as 3
     assert lib.ucp_convert_gather(None, 0, None, None, bad.ctypes.data, None, None, None, None) == -10
     assert lib.ucp_convert_gather(None, 0, None, None, None, None, None, None, None) == -10
+    assert lib.ucp_convert_gather(None, 0, None, None, tiles_without_runs.ctypes.data, None, None,
+                                  None, None) == -10
+    assert lib.ucp_load_scatter(None, 3, None, None, runs_mismatch.ctypes.data, None, None, None,
+                                None) == -10
     assert lib.ucp_load_scatter(None, 0, None, None, zero.ctypes.data, None, None, None, None) == 0
+    assert lib.ucp_runtile_scan(None, zero.ctypes.data, None) == 0
+    assert lib.ucp_runtile_scan(None, None, None) == -10
     assert lib.ucp_gen_state(0, 0, 0, 0, None, None) == 0
     assert lib.ucp_status_reset(None, None) == -10
 

@@ -19,6 +19,7 @@ from paper_2406_18820_b200.plan import (
     compile_extract,
     compile_union,
     fragment_elems,
+    expand_tiles,
     make_tiles,
     split_rows,
 )
@@ -248,11 +249,65 @@ def test_finish_classed_partitions_tiles():
     cfg = ParallelConfig(dp=3, tp=2, zero_stage=ZeroStage.Z1)
     atomic = O.init_state(spec, 7)
     _, tab = _arena_extract(spec, cfg, atomic, DType.BF16)
-    runs, aux, tiles, counts = tab.finish_classed(4096)
-    assert counts.sum() == len(tiles) and len(counts) == NCLASS
-    cls = run_classes(runs)[tiles["run"]]
-    assert (np.diff(cls) >= 0).all()
-    assert counts[CLASS_GENERAL] > 0  # noise + misaligned dp=3 pieces
+    runs, aux, rt, info, order = tab.finish_classed(4096)
+    assert sorted(order) == list(range(len(runs)))
+    assert len(info) == 2 * NCLASS
+    assert info[:NCLASS].sum() == rt["ntiles"].sum() and info[NCLASS:].sum() == len(runs)
+    cls = run_classes(runs)
+    assert (np.diff(cls) >= 0).all()  # runs sorted by kernel class
+    assert info[CLASS_GENERAL] > 0  # noise + misaligned dp=3 pieces
+    # the interpreter over the classed table reproduces the table-order result
+    assert len(expand_tiles(runs, rt)) == info[:NCLASS].sum()
+
+
+def _find_run(first, lo, hi, b):
+    """Python mirror of find_run() in csrc/ucp_b200.cu (32-ary warp search)."""
+    while hi - lo > 1:
+        step = (hi - lo + 31) // 32
+        le = [lo + i * step < hi and first[lo + i * step] <= b for i in range(32)]
+        assert le == sorted(le, reverse=True)  # the ballot is a prefix of the lanes
+        last = max(i for i in range(32) if le[i])
+        lo += last * step
+        hi = min(hi, lo + step)
+    return lo
+
+
+@pytest.mark.parametrize("tb", [512, 4096, 1 << 17])
+def test_device_tile_derivation_matches_expansion(tb):
+    """Per class, CTA b finds its run by the warp search over the
+    class-relative `first` (what ucp_runtile_scan writes) and derives the
+    same rectangle expand_tiles lists -- including zero-tile runs."""
+    from paper_2406_18820_b200.plan import NCLASS, RUN_ROWSPLIT, classed, run_classes
+
+    spec = U.make_model("GQA", {"n_layers": 2, "hidden": 64, "q_heads": 8, "kv_heads": 2})
+    cfg = ParallelConfig(dp=3, tp=2, zero_stage=ZeroStage.Z1)
+    _, tab = _arena_extract(spec, cfg, O.init_state(spec, 7), DType.BF16)
+    runs0, aux = tab._runs_aux()
+    empty = runs0[:1].copy()
+    empty["rows"] = 0  # a zero-tile run in the middle of a class
+    runs0 = np.concatenate([runs0[:3], empty, runs0[3:]])
+    runs, aux, rt, info, _ = classed(runs0, aux, run_classes(runs0), tb)
+    want = expand_tiles(runs, rt)
+    got, r0 = [], 0
+    for c in range(NCLASS):
+        nr, nt = int(info[NCLASS + c]), int(info[c])
+        first = rt["first"][r0:r0 + nr].astype(np.int64)
+        assert nr == 0 or first[0] == 0
+        for b in range(nt):
+            run = r0 + _find_run(list(first), 0, nr, b)
+            k = b - int(rt["first"][run])
+            per, tpr, r = int(rt["per"][run]), int(rt["tpr"][run]), runs[run]
+            assert 0 <= k < int(rt["ntiles"][run])
+            if r["flags"] & RUN_ROWSPLIT:
+                row0 = k // tpr
+                col0 = (k - row0 * tpr) * per
+                cnt = min(per, int(r["cols"]) - col0)
+            else:
+                row0, col0 = k * per, 0
+                cnt = min(per, int(r["rows"]) - row0)
+            got.append((run, row0, col0, cnt))
+        r0 += nr
+    assert got == [tuple(int(x) for x in t) for t in want]
 
 
 def _fused_world(spec, src_cfg, tgt_cfg, shards, dtype, tile_bytes=4096, materialize=True):
@@ -289,8 +344,8 @@ def _fused_world(spec, src_cfg, tgt_cfg, shards, dtype, tile_bytes=4096, materia
             aat += align_up(4 * p.numel)
     atom = np.zeros(max(aat, 16), dtype=np.uint8)
     dst = np.full(max(tat, 16), 0xCD, dtype=np.uint8)
-    xr, xa, xt, _ = fx.finish_classed(tile_bytes)
-    assert execute_fused(xr, xa, xt, src, atom, dst) == []
+    xr, xa, xrt, _, _ = fx.finish_classed(tile_bytes)
+    assert execute_fused(xr, xa, expand_tiles(xr, xrt), src, atom, dst) == []
     r1, a1, t1 = rc.finish(tile_bytes)
     assert execute(r1, a1, t1, src, atom) == []
     r2, a2, t2 = rl.finish(tile_bytes)
