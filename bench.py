@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--window-gb", type=float, default=2.5)
     ap.add_argument("--tile-kb", type=int, default=128)
     ap.add_argument("--e2e-gb", type=float, default=24.0, help="pinned host budget of the e2e sample")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-window-gb", type=float, default=0.4)
     ap.add_argument("--e2e-slots", type=int, default=3, help="device slots per direction")
     ap.add_argument("--no-e2e", action="store_true")
