@@ -422,13 +422,18 @@ class ReshardPlan:
         ``self.host_slots``) over windows on three streams. Asynchronous:
         the caller synchronises (the last event is on the D2H stream)."""
         wins = self.windows if windows is None else windows
-        s_in, s_cmp, s_out = streams or (torch.cuda.Stream(self.device),
-                                         torch.cuda.Stream(self.device),
-                                         torch.cuda.Stream(self.device))
+        s_in, s_cmp, s_out = streams or self.host_streams()
         ns = max(2, slots or self.host_slots)
         dsrc = [self.buf(f"ssrc{j}", self.max_src) for j in range(ns)]
         dtgt = [self.buf(f"stgt{j}", self.max_tgt) for j in range(ns)]
         atom = self.buf("atom", self.max_atom)
+        # the caller's stream first: work it queued before this call (the
+        # status reset, writes into host_src) must precede our copies and
+        # kernels -- the side streams do not synchronise with it implicitly
+        cur = torch.cuda.current_stream(self.device)
+        for s_ in (s_in, s_cmp, s_out):
+            if s_ is not cur:
+                s_.wait_stream(cur)
         # buffers are reused across calls: the first H2D must not overwrite a
         # source slot still being read, the first kernel must not overwrite a
         # target slot still being copied out
@@ -484,8 +489,7 @@ class ReshardPlan:
         exception on a data-dependent failure (ReplicateMismatchError,
         PaddingError, ...); without it the caller checks ``status_out``
         later with ``check_status_word``."""
-        streams = streams or (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device),
-                              torch.cuda.Stream(self.device))
+        streams = streams or self.host_streams()
         self.stream_host(host_src, host_tgt, None, streams)
         if status_out is not None:
             with torch.cuda.stream(streams[2]):
@@ -494,6 +498,14 @@ class ReshardPlan:
             streams[2].synchronize()
             if status_out is None or not self.status_ok(status_out):
                 self._check_windows(host_src)
+
+    def host_streams(self) -> tuple:
+        """The plan's own (H2D, compute, D2H) streams: calls that do not pass
+        streams reuse them, so back-to-back unsynchronised calls are ordered
+        against each other (device slots are reused across calls)."""
+        if getattr(self, "_host_streams", None) is None:
+            self._host_streams = tuple(torch.cuda.Stream(self.device) for _ in range(3))
+        return self._host_streams
 
     @staticmethod
     def status_ok(word: torch.Tensor) -> bool:
