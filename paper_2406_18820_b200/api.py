@@ -504,6 +504,8 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
     # one H2D stream per slot: each read job enqueues the H2D of its own
     # chunk as soon as the bytes land, so PCIe-in overlaps the file reads
     s_h2d = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    for s_ in s_h2d:  # after everything already queued on the caller's stream
+        s_.wait_stream(stream)
     nthreads = max(4, min(32, 2 * n_workers, os.cpu_count() or 4))
     with ThreadPoolExecutor(nthreads) as rpool, ThreadPoolExecutor(nthreads) as wpool:
 
