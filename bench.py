@@ -278,11 +278,12 @@ def pcie_peaks(dev, stream, nbytes: int = 1 << 30, reps: int = 5) -> dict:
     import torch
 
     try:
-        h_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-        h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        from paper_2406_18820_b200.engine import pinned_host
+
+        h_in, h_out = pinned_host(nbytes), pinned_host(nbytes)
         d_in = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         d_out = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    except RuntimeError:
+    except (RuntimeError, OSError):
         return {}
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
@@ -566,8 +567,11 @@ def run_ours(args):
             # inputs of the sample: synthesised by the GPU generator into the
             # e2e plan's own arena, then copied to pinned host memory (untimed)
             eplan.synthesize(7)
-            host_src = torch.empty(max(eplan.src_total, 256), dtype=torch.uint8, pin_memory=True)
-            host_tgt = torch.empty(max(eplan.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
+            from paper_2406_18820_b200.engine import pinned_host
+
+            # exact-size page-locked buffers (torch's pinned allocator rounds
+            # up to a power of two)
+            host_src, host_tgt = pinned_host(eplan.src_total), pinned_host(eplan.tgt_total)
             host_src[:eplan.src_total].copy_(eplan._bufs["src_arena"][:eplan.src_total])
             eplan._bufs.pop("src_arena", None)
             torch.cuda.empty_cache()

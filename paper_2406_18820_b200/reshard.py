@@ -28,7 +28,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .engine import Program, Status, XProgram, align_up, gen_state, require_device, stream_ptr
+from .engine import (Program, Status, XProgram, align_up, gen_state, pinned_host, require_device,
+                     stream_ptr)
 from .layout import all_rank_records, validate_model_config
 from .plan import (
     RunTable,
@@ -401,8 +402,7 @@ class ReshardPlan:
 
     def pack_host(self, shards: dict, pinned: torch.Tensor | None = None) -> torch.Tensor:
         """Copy {g: [array per source record]} into a pinned source arena."""
-        host = pinned if pinned is not None else torch.empty(
-            max(self.src_total, 256), dtype=torch.uint8, pin_memory=True)
+        host = pinned if pinned is not None else pinned_host(self.src_total)
         hv = host.numpy()
         for W in self.windows:
             for g, i, m, off, n in W.src_frags:
@@ -515,7 +515,7 @@ class ReshardPlan:
         """End-to-end in-memory reshard of host arrays; returns target arrays
         per rank in canonical record order."""
         host_src = self.pack_host(shards)
-        host_tgt = torch.empty(max(self.tgt_total, 256), dtype=torch.uint8, pin_memory=True)
+        host_tgt = pinned_host(self.tgt_total)
         self.status.reset()
         self.run_pinned(host_src, host_tgt)
         return self.unpack_host(host_tgt)
