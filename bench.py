@@ -334,6 +334,50 @@ def link_roofline(link: dict, h2d: int, d2h: int, ms: float) -> dict:
     return out
 
 
+def cpu_leg(args, spec, src, tgt, host_cpu_frags, cpu_names, gpu_index, host_tgt) -> dict:
+    """cpu_baseline: the reference's union + extract_fragment on the host's
+    cores over a bounded sample (the last e2e window's params when the e2e
+    leg ran, else the first layers), plus the bit-exact comparison of its
+    outputs with the GPU e2e leg's D2H bytes for the same params."""
+    if host_cpu_frags is None:
+        cpu_names = sample_params(spec, 3e9)
+        host_cpu_frags = oracle_frags(spec, src, cpu_names, args.cpu_threads)
+    S_cpu = sum(12 * spec.param(n).numel for n in cpu_names)
+    arm = CpuArm(spec, src, tgt, host_cpu_frags)
+    ref_out: dict = {}
+    t_cpu = arm.run(args.cpu_threads, ref_out)
+    t_cpu1 = arm.run(1)
+    parity_cpu = None
+    if gpu_index:
+        hv = host_tgt.numpy()
+        same = nbytes = compared = 0
+        for key, want in ref_out.items():
+            if key not in gpu_index:  # bf16/f16 weights: the CPU arm does not cast
+                continue
+            compared += 1
+            at, n = gpu_index[key]
+            got = hv[at:at + 4 * n]
+            w = np.ascontiguousarray(want).reshape(-1).view(np.uint8)
+            same += int(w.size == got.size and np.array_equal(w, got))
+            nbytes += w.size
+        parity_cpu = {"fragments": compared, "identical": same, "bytes": int(nbytes),
+                      "bit_exact": same == compared == len(gpu_index) > 0,
+                      "what": "every target fragment the CPU arm produced vs the GPU "
+                              "e2e leg's D2H output for the same params"}
+    what = ("ucp.union + ucp.parallel.extract_fragment from baseline/_ref (unmodified "
+            "reference)" if arm.kind == "reference" else "oracle union + extract_fragment")
+    cpu = {"value": S_cpu / t_cpu / GB, "unit": "GB/s", "cores": args.cpu_threads,
+           "value_1_thread": S_cpu / t_cpu1 / GB, "kind": arm.kind,
+           "sample": f"{len(cpu_names)} params ({cpu_names[0]} .. {cpu_names[-1]}), "
+                     f"{S_cpu / GB:.2f} GB state: {what} "
+                     f"(materialised), {args.cpu_threads} threads, one pass",
+           "parity_vs_gpu": parity_cpu}
+    if arm.kind == "reference":
+        cpu["port_value"] = S_cpu / CpuArm(spec, src, tgt, host_cpu_frags, False).run(
+            args.cpu_threads) / GB
+    return cpu
+
+
 def emit(obj, rank):
     if rank == 0:
         print(json.dumps(obj), flush=True)
@@ -656,47 +700,11 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-      try:
-        if host_cpu_frags is None:
-            cpu_names = sample_params(spec, 3e9)
-            host_cpu_frags = oracle_frags(spec, src, cpu_names, args.cpu_threads)
-        S_cpu = sum(12 * spec.param(n).numel for n in cpu_names)
-        arm = CpuArm(spec, src, tgt, host_cpu_frags)
-        ref_out: dict = {}
-        t_cpu = arm.run(args.cpu_threads, ref_out)
-        t_cpu1 = arm.run(1)
-        parity_cpu = None
-        if gpu_index:
-            # the reference's own outputs vs the GPU's e2e outputs, same sample
-            hv = host_tgt.numpy()
-            same = nbytes = compared = 0
-            for key, want in ref_out.items():
-                if key not in gpu_index:  # bf16/f16 weights: the CPU arm does not cast
-                    continue
-                compared += 1
-                at, n = gpu_index[key]
-                got = hv[at:at + 4 * n]
-                w = np.ascontiguousarray(want).reshape(-1).view(np.uint8)
-                same += int(w.size == got.size and np.array_equal(w, got))
-                nbytes += w.size
-            parity_cpu = {"fragments": compared, "identical": same, "bytes": int(nbytes),
-                          "bit_exact": same == compared == len(gpu_index) > 0,
-                          "what": "every target fragment the CPU arm produced vs the GPU "
-                                  "e2e leg's D2H output for the same params"}
-        what = ("ucp.union + ucp.parallel.extract_fragment from baseline/_ref (unmodified "
-                "reference)" if arm.kind == "reference" else "oracle union + extract_fragment")
-        cpu = {"value": S_cpu / t_cpu / GB, "unit": "GB/s", "cores": args.cpu_threads,
-               "value_1_thread": S_cpu / t_cpu1 / GB,
-               "kind": arm.kind,
-               "sample": f"{len(cpu_names)} params ({cpu_names[0]} .. {cpu_names[-1]}), "
-                         f"{S_cpu / GB:.2f} GB state: {what} "
-                         f"(materialised), {args.cpu_threads} threads, one pass"}
-        cpu["parity_vs_gpu"] = parity_cpu
-        if arm.kind == "reference":
-            cpu["port_value"] = S_cpu / CpuArm(spec, src, tgt, host_cpu_frags, False).run(
-                args.cpu_threads) / GB
-      except Exception as exc:  # rank 0 only: no collective to skip
-        cpu = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:300]}
+        try:
+            cpu = cpu_leg(args, spec, src, tgt, host_cpu_frags, cpu_names, gpu_index,
+                          host_tgt if gpu_index else None)
+        except Exception as exc:  # rank 0 only: no collective to skip
+            cpu = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:300]}
 
     emit({"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

@@ -8,6 +8,7 @@ Deselected: the two CLI tests that plot with matplotlib, which this image
 lacks. They fail the same way on the unmodified reference, and the plots are
 out of scope."""
 
+import ast
 import os
 import re
 import subprocess
@@ -37,7 +38,7 @@ def test_reference_suite_passes_on_the_b200_engine():
     assert m and int(m.group(1)) >= 180, out[-2000:]
     calls = re.search(r"B200 engine calls served under the reference suite: (\{.*\})", out)
     assert calls, out[-2000:]
-    served = eval(calls.group(1))  # noqa: S307 - our own plugin's dict repr
+    served = ast.literal_eval(calls.group(1))
     for name in ("convert", "load", "resume", "union"):
         assert served.get(name, 0) > 0, served
     assert "libucp_b200.so" in out
