@@ -190,8 +190,10 @@ int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, f
 
 /*
  * Fused convert + load (the in-memory resume() path, ucp/load.py:276-281):
- * class_info as for ucp_convert_gather; only the three VEC classes (target
- * dtype f32 / bf16 / f16) may be non-empty, runs sorted by class.
+ * class_info as for ucp_convert_gather, runs sorted by class. Classes
+ * VEC_F32 / VEC_BF16 / VEC_F16 hold runs of one target dtype each; for fused
+ * tables the GENERAL slot means "mixed target dtypes": one launch whose CTAs
+ * dispatch on their run's dtype (kernel reshard_fused_mixed).
  */
 int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
                       const ucp_runtile* rt, const int64_t* class_info, const void* src_base,

@@ -964,6 +964,22 @@ __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f16(UCP_FUSE
   fused_body<UCP_DT_F16>(runs, aux, rt, r0, nr, n_tiles, sb, ab, db, st);
 }
 
+// Mixed target dtypes in one grid (bf16/f16 weights next to f32 moments):
+// each CTA dispatches on its run's dtype. One launch interleaves the
+// read-heavy weight tiles (strict replicas, 2-B targets) with the
+// write-heavy moment tiles, instead of two launches with skewed DRAM
+// read/write mixes.
+__global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_mixed(UCP_FUSED_ARGS) {
+  (void)n_tiles;
+  __shared__ __align__(16) ucp_xrun s_run;
+  __shared__ uint4 s_t;
+  __shared__ uint64_t s_aux[kMaxAux];
+  const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
+  if (s_run.dtype == UCP_DT_F32) fused_tile<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st);
+  else if (s_run.dtype == UCP_DT_BF16) fused_tile<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st);
+  else fused_tile<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st);
+}
+
 // ---------------------------------------------------------------- entry kernels
 // Distinct names per stage and destination dtype so launch lists and ncu
 // filters read like the pipeline: convert_gather_* (union) and
@@ -1171,16 +1187,20 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
   ClassRange cr;
   uint32_t nt[UCP_NCLASS];
   if (!parse_classes(class_info, n_runs, cr, nt)) return UCP_EINVAL;
-  if (nt[UCP_CLASS_GENERAL] != 0) return UCP_EINVAL;
-  if (nt[0] + nt[1] + nt[2] == 0) return UCP_OK;
+  if (nt[0] + nt[1] + nt[2] + nt[3] == 0) return UCP_OK;
   if (!runs || !rt || !status) return UCP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const char* sb = static_cast<const char*>(src_base);
   char* ab = static_cast<char*>(atom_base);
   char* db = static_cast<char*>(dst_base);
-  for (int c = 0; c < UCP_CLASS_GENERAL; ++c) {
+  for (int c = 0; c < UCP_NCLASS; ++c) {
     const uint32_t n = nt[c];
     if (n == 0) continue;
+    if (c == UCP_CLASS_GENERAL) {  // fused tables: mixed target dtypes, per-tile dispatch
+      reshard_fused_mixed<<<dim3(n), dim3(kThreads), 0, s>>>(runs, aux, rt, cr.begin[c], cr.n[c], n,
+                                                           sb, ab, db, status);
+      continue;
+    }
 #if UCP_PERSISTENT
     const unsigned g = n < 148u * UCP_MINB ? n : 148u * UCP_MINB;
 #else

@@ -28,6 +28,8 @@ from __future__ import annotations
 from collections import defaultdict
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 from ._errors import (
@@ -678,6 +680,11 @@ def fragment_shape(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta) -> tuple
 class XRunTable:
     """Fused convert+load runs (ucp_xrun) for one ucp_reshard_fused launch."""
 
+    # UCP_FUSED_MIXED=1: all target dtypes in one launch (reshard_fused_mixed).
+    # Measured 0.5-1 % slower than one launch per dtype for bf16 targets
+    # (DESIGN §3 tuning log), so off by default.
+    MIXED = os.environ.get("UCP_FUSED_MIXED", "0") != "0"
+
     def __init__(self):
         self._rows: list = []
         self._aux: list = []
@@ -685,6 +692,7 @@ class XRunTable:
         self.src_bytes = 0
         self.atom_bytes = 0
         self.dst_bytes = 0
+        self.mixed = self.MIXED
 
     def unit(self, param: str, kind: str) -> int:
         self.units.append(Unit(param, kind))
@@ -718,6 +726,11 @@ class XRunTable:
         extra = np.where(runs["atom"] == np.uint64(NO_ATOM), 0, 4).astype(np.int64)
         cls = np.select([runs["dtype"] == DType.F32.value, runs["dtype"] == DType.BF16.value],
                         [CLASS_VEC_F32, CLASS_VEC_BF16], CLASS_VEC_F16).astype(np.int64)
+        if self.mixed and len(np.unique(cls)) > 1:
+            # one launch over every target dtype (reshard_fused_mixed): the
+            # read-heavy 2-B-target weight tiles interleave with the f32
+            # moment tiles in table order
+            cls = np.full(len(runs), CLASS_GENERAL, dtype=np.int64)
         return classed(runs, aux, cls, tile_bytes, extra)
 
 
