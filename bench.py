@@ -615,7 +615,11 @@ def run_ours(args):
 
             # exact-size page-locked buffers (torch's pinned allocator rounds
             # up to a power of two)
-            host_src, host_tgt = pinned_host(eplan.src_total), pinned_host(eplan.tgt_total)
+            if os.environ.get("UCP_PIN_MODE", "mmap") == "torch":  # A/B switch
+                host_src = torch.empty(eplan.src_total, dtype=torch.uint8, pin_memory=True)
+                host_tgt = torch.empty(eplan.tgt_total, dtype=torch.uint8, pin_memory=True)
+            else:
+                host_src, host_tgt = pinned_host(eplan.src_total), pinned_host(eplan.tgt_total)
             host_src[:eplan.src_total].copy_(eplan._bufs["src_arena"][:eplan.src_total])
             eplan._bufs.pop("src_arena", None)
             torch.cuda.empty_cache()

@@ -7,6 +7,7 @@ data movement on the hot path goes through libucp_b200.so.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -217,7 +218,7 @@ class _Pinned:
             pass
 
 
-def pinned_host(nbytes: int, threads: int = 16) -> torch.Tensor:
+def pinned_host(nbytes: int, threads: int = 16, huge: bool | None = None) -> torch.Tensor:
     """Page-locked host bytes, exact size: anonymous mmap, first-touched
     from ``threads`` threads (page zeroing is the cost; torch's pinned
     allocator does it on one thread and rounds up to a power of two), then
@@ -228,6 +229,12 @@ def pinned_host(nbytes: int, threads: int = 16) -> torch.Tensor:
 
     nbytes = max(int(nbytes), 4096)
     mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    if huge is None:
+        huge = os.environ.get("UCP_PIN_HUGE", "1") != "0"
+    if huge and hasattr(mm, "madvise") and hasattr(mmap, "MADV_HUGEPAGE"):
+        # transparent huge pages (THP is "madvise" on the B200 hosts): fewer
+        # pages to pin and fewer IOMMU translations per DMA byte
+        mm.madvise(mmap.MADV_HUGEPAGE)
     arr = np.frombuffer(mm, dtype=np.uint8)
     step = 64 << 20
     with ThreadPoolExecutor(max(1, threads)) as pool:
