@@ -110,7 +110,7 @@ def _build_move(rng, n_runs):
     return tab, src, max(dst_a.top, 16)
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(48))
 def test_move_kernels_match_interpreter(seed):
     rng = np.random.default_rng(1000 + seed)
     tab, src, dst_n = _build_move(rng, int(rng.integers(1, 14)))
@@ -134,7 +134,7 @@ def test_move_kernels_match_interpreter(seed):
         assert bad.size == 0, (seed, gather, bad[:8], len(runs), tile_bytes)
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(32))
 def test_fused_kernel_matches_interpreter(seed):
     rng = np.random.default_rng(2000 + seed)
     fx = XRunTable()
