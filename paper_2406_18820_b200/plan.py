@@ -49,7 +49,6 @@ from .layout import (
     SHARD_V,
     frag_shape,
     mode_of,
-    tp_fragment_shape,
     vocab_padded_rows,
 )
 from .spec import DType, ParallelConfig, ParamSpec, RecordMeta

@@ -28,8 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .engine import (Program, Status, XProgram, align_up, gen_state, pinned_host, require_device,
-                     stream_ptr)
+from .engine import Program, Status, XProgram, align_up, gen_state, pinned_host, require_device
 from .layout import all_rank_records, validate_model_config
 from .plan import (
     RunTable,
