@@ -375,8 +375,17 @@ def _windows(items: list, size_of, budget: int) -> list:
     return out
 
 
+def _io_threads(n_workers: int) -> int:
+    """File I/O threads of one pipeline pool. The bytes written do not depend
+    on it (ucp/convert.py:422-428: output independent of n_workers), so the
+    pool uses the host's cores even at the reference's default n_workers=1;
+    a larger n_workers can still raise it (up to 32)."""
+    cores = os.cpu_count() or 4
+    return max(4, min(32, max(cores, 2 * n_workers)))
+
+
 def _io_pool(n_workers: int) -> ThreadPoolExecutor:
-    return ThreadPoolExecutor(max_workers=max(4, min(32, 2 * n_workers, os.cpu_count() or 4)))
+    return ThreadPoolExecutor(max_workers=_io_threads(n_workers))
 
 
 # --------------------------------------------------------------------------- pipeline
@@ -506,7 +515,7 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
     s_h2d = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     for s_ in s_h2d:  # after everything already queued on the caller's stream
         s_.wait_stream(stream)
-    nthreads = max(4, min(32, 2 * n_workers, os.cpu_count() or 4))
+    nthreads = _io_threads(n_workers)
     with ThreadPoolExecutor(nthreads) as rpool, ThreadPoolExecutor(nthreads) as wpool:
 
         def read_and_send(slot, path, file_off, at, n, send):
