@@ -602,3 +602,26 @@ def test_baseline_config_slice_vs_oracle(name):
             assert np.array_equal(a.view(np.uint32), want.view(np.uint32)), (name, g, m.param, m.kind)
             n_checked += 1
     assert n_checked > 0
+
+
+def test_pinned_host_staging():
+    """engine.pinned_host: exact-size, page-locked (cudaHostRegister) host
+    bytes usable for async copies; numpy views outlive the tensor safely."""
+    from paper_2406_18820_b200.engine import pinned_host
+
+    for n in (1, 4096, (3 << 20) + 5):
+        t = pinned_host(n)
+        assert t.numel() >= n and t.dtype == torch.uint8 and t.is_pinned()
+        src = torch.randint(0, 255, (t.numel(),), dtype=torch.uint8)
+        t.copy_(src)
+        d = torch.empty_like(t, device="cuda")
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            d.copy_(t, non_blocking=True)
+            t2 = pinned_host(n)
+            t2.copy_(d, non_blocking=True)
+        s.synchronize()
+        assert torch.equal(t2, src)
+        view = t2.numpy()[:16]
+        del t, t2
+        assert np.array_equal(view, src.numpy()[:16])
