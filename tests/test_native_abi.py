@@ -74,3 +74,38 @@ def test_comm_library_exports():
         assert hasattr(lib, n)
     assert lib.ucp_comm_version() == 1
     assert lib.ucp_comm_init(0, 0, None, None) == -10
+
+
+def test_no_cpu_fallback_without_a_device(tmp_path):
+    """The product path raises NativeUnavailableError instead of computing on
+    the CPU: every public compute entry on a host without a CUDA device, and
+    the library loader when the .so is absent or of another ABI."""
+    import pytest
+    import torch
+
+    import paper_2406_18820_b200 as U
+    from paper_2406_18820_b200.spec import ParamKind, ParamSpec, RecordMeta
+
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    p = ParamSpec("w", (4, 2), 0, ParamKind.MATMUL2D, 0)
+    full = np.arange(8, dtype=np.float32).reshape(4, 2)
+    meta = RecordMeta(p.name, "weight", "replicate", (0, 0, 0), p.shape)
+    with pytest.raises(U.NativeUnavailableError):
+        U.union(p, U.ParallelConfig(), [U.FragmentMsg(meta, full)])
+    with pytest.raises(U.NativeUnavailableError):
+        U.extract_fragment(p, U.ParallelConfig(), meta, full)
+    spec = U.make_model("DenseGPT", {"n_layers": 2, "hidden": 32})
+    with pytest.raises(U.NativeUnavailableError):
+        U.init_state(spec, 7)
+    from oracle import ucp_oracle as O
+
+    src_cfg = U.ParallelConfig(dp=2, zero_stage=U.ZeroStage.Z1)
+    O.write_tree(spec, src_cfg, O.partition_mem(spec, O.init_state(spec, 7), src_cfg),
+                 str(tmp_path / "src"))
+    with pytest.raises(U.NativeUnavailableError):
+        U.convert(str(tmp_path / "src"), str(tmp_path / "out"))
+    with pytest.raises(U.NativeUnavailableError):
+        U.ReshardPlan(spec, U.ParallelConfig(dp=2, zero_stage=U.ZeroStage.Z1), U.ParallelConfig())
+    with pytest.raises(U.NativeUnavailableError):
+        _native.load_library(str(tmp_path / "missing.so"))
