@@ -45,6 +45,10 @@ constexpr int kMaxAux = 256;             // host splits runs beyond this
 
 // ---------------------------------------------------------------- memory ops
 
+#ifndef UCP_PREFETCH_NEXT
+#define UCP_PREFETCH_NEXT 0  // fused kernel: L2 bulk prefetch distance in warp items (0: off)
+#endif
+
 #ifndef UCP_L2_PREFETCH
 #define UCP_L2_PREFETCH 0  // 0, 128 or 256: L2 sector prefetch hint on streaming loads; 1: L2 evict_first
 #endif
@@ -717,6 +721,28 @@ __device__ __forceinline__ void fused_tile(const uint64_t* __restrict__ aux,
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   for (uint32_t it = warp; it < n_items; it += kWarps) {
+#if UCP_PREFETCH_NEXT
+    // experiment: bulk-prefetch this warp's segment UCP_PREFETCH_NEXT items
+    // ahead into L2 (one cp.async.bulk.prefetch per source replica, lanes
+    // 0..ns-1), so more DRAM reads are in flight than the registers hold
+    {
+      const uint32_t nit = it + UCP_PREFETCH_NEXT * kWarps;
+      if (nit < n_items && lane < (uint32_t)ns) {
+        const uint32_t nrr = spr == 1 ? nit : nit / spr;
+        const uint32_t ncs = tile.col0 + (nit - nrr * spr) * kSeg;
+        const uint32_t nlen = min(ncs + kSeg, tile.col0 + nc) - ncs;
+        const uint64_t nsrow = (uint64_t)(tile.row0 + nrr) * sp + ncs;
+        const uint64_t rb = lane == 0 ? s0 : s_aux[lane - 1];
+        uint64_t a = reinterpret_cast<uint64_t>(sb + rb + 4 * nsrow);
+        uint64_t e = a + 4ull * nlen;
+        a = (a + 15) & ~15ull;
+        e &= ~15ull;
+        if (e > a)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a))
+                       : "memory");
+      }
+    }
+#endif
     const uint32_t rr = spr == 1 ? it : it / spr;
     const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
     const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
