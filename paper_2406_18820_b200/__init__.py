@@ -31,6 +31,7 @@ from ._errors import (
 from .reshard import ReshardPlan  # noqa: E402  (isort: skip)
 from .api import (
     AtomicCheckpoint,
+    DeviceTensor,
     FragmentMsg,
     LoadedWorld,
     LoadStats,

@@ -109,6 +109,50 @@ class AtomicCheckpoint:
         return out
 
 
+_TORCH_DT = {DType.F32: torch.float32, DType.BF16: torch.bfloat16, DType.F16: torch.float16}
+
+
+class DeviceTensor:
+    """A loaded shard that stays in HBM (``load(..., keep_on_device=True)``):
+    the ``Tensor`` interface, with ``data`` materialised to host numpy on
+    first access (cached) and ``device`` the zero-copy CUDA tensor (bf16 /
+    f16 weights as torch.bfloat16 / float16 views of the same bits).
+    SURVEY §8b: the GPU build keeps device buffers and materialises numpy
+    lazily, so consolidate_world and the reference's checks work unchanged."""
+
+    __slots__ = ("dtype", "shape", "_dev", "_host")
+
+    def __init__(self, dtype: DType, shape: tuple, dev_bytes: torch.Tensor):
+        self.dtype, self.shape, self._host = dtype, tuple(shape), None
+        self._dev = dev_bytes.view(_TORCH_DT[dtype]).view(self.shape)
+
+    @property
+    def device(self) -> torch.Tensor:
+        return self._dev
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._host is None:
+            t = self._dev.contiguous().view(torch.uint8).cpu().numpy()
+            self._host = t.view(self.dtype.storage).reshape(self.shape)
+        return self._host
+
+    @property
+    def numel(self) -> int:
+        return int(np.prod(self.shape, dtype=np.int64)) if self.shape else 1
+
+    @property
+    def nbytes(self) -> int:
+        return self.numel * self.dtype.itemsize
+
+    def tobytes(self) -> bytes:
+        return np.ascontiguousarray(self.data).tobytes()
+
+    def bits_equal(self, other) -> bool:
+        return (self.dtype is other.dtype and tuple(self.shape) == tuple(other.shape)
+                and self.tobytes() == other.tobytes())
+
+
 @dataclass(frozen=True)
 class WorldShard:
     meta: RecordMeta
@@ -481,7 +525,7 @@ def _coalesce(ranges, gap: int) -> list:
     return runs
 
 
-def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
+def _pipeline(wplans: list, dev, key: str, n_workers: int, emit, sink=None) -> None:
     """Windowed file pipeline, double-buffered so file reads of windows w
     and w+1 and the output handling of window w-1 overlap the GPU work of
     window w:
@@ -492,7 +536,9 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
     wplans: [(step, read jobs (path, header, offset), src bytes, outs, dst
     bytes)] with step a _Step/_FusedStep. ``emit(o, view)`` runs on this
     thread and returns zero-argument jobs (file-range writes, host copies)
-    that the write pool runs. Data-dependent failures raise after their
+    that the write pool runs. With ``sink`` (one device address per window)
+    the kernels write straight into device memory the caller keeps: no D2H,
+    no emit. Data-dependent failures raise after their
     window syncs, so a failing window never reaches emit (torn output,
     ucp/convert.py:503)."""
     import time
@@ -505,9 +551,10 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
     ms = max(w[2] for w in wplans)
     md = max(w[4] for w in wplans)
     h_src = [_STAGE.host_buf(f"{key}_src{i}", ms) for i in range(2)]
-    h_dst = [_STAGE.host_buf(f"{key}_dst{i}", md) for i in range(2)]
+    if sink is None:
+        h_dst = [_STAGE.host_buf(f"{key}_dst{i}", md) for i in range(2)]
+        d_dst = [_STAGE.dev_buf(f"{key}_dst{i}", md, dev) for i in range(2)]
     d_src = [_STAGE.dev_buf(f"{key}_src{i}", ms, dev) for i in range(2)]
-    d_dst = [_STAGE.dev_buf(f"{key}_dst{i}", md, dev) for i in range(2)]
     st = _status(dev)
     stream = torch.cuda.current_stream(dev)
     # one H2D stream per slot: each read job enqueues the H2D of its own
@@ -572,9 +619,16 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit) -> None:
                 h2d_ev[w].record(s_h2d[slot])
                 stream.wait_event(h2d_ev[w])
                 st.reset(stream)
-                step.launch(d_src[slot].data_ptr(), d_dst[slot].data_ptr(), st, stream)
+                dst_ptr = sink[w] if sink is not None else d_dst[slot].data_ptr()
+                step.launch(d_src[slot].data_ptr(), dst_ptr, st, stream)
                 kern_ev[w] = torch.cuda.Event()
                 kern_ev[w].record(stream)
+                if sink is not None:
+                    t0 = time.perf_counter()
+                    kern_ev[w].synchronize()
+                    tr["gpu_wait_s"] += time.perf_counter() - t0
+                    step.check(st, d_src[slot].data_ptr(), dst_ptr, stream)
+                    continue
                 t0 = time.perf_counter()
                 for f in written.pop(w - 2, ()):  # h_dst[slot] is free again
                     f.result()
@@ -759,9 +813,15 @@ def _load_stats(atomic: AtomicCheckpoint, spec: ModelSpec, tgt: ParallelConfig,
 
 
 def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass: bool = True,
-         *, device=None, window_bytes: int = DEFAULT_WINDOW_BYTES) -> LoadedWorld:
+         *, device=None, window_bytes: int = DEFAULT_WINDOW_BYTES,
+         keep_on_device: bool = False) -> LoadedWorld:
     """Materialise every shard of a target world from an atomic checkpoint
-    (ucp/load.py:131-223). Weights are cast to dtype; moments stay f32."""
+    (ucp/load.py:131-223). Weights are cast to dtype; moments stay f32.
+
+    ``keep_on_device`` (extension): the shards stay in HBM as
+    ``DeviceTensor`` (numpy on first ``.data`` access), written by the
+    kernels straight into one device arena -- no D2H, no host copies; raises
+    MemoryError when the world does not fit the device."""
     atomic = load_atomic(atomic_root)
     spec = atomic.spec
     validate_model_config(spec, tgt)
@@ -810,17 +870,33 @@ def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass
                 compile_extract(tab, p, tgt, targets, s_at, odt)
                 s_at += align_up(hdr.nbytes)
         wplans.append((_Step(Program(tab, dev), False), jobs, s_at, outs, t_at))
-    host = np.empty(max(total, 1), dtype=np.uint8)
-
-    def emit(o, ov):
-        _, _, _, odt, at, n, _, g_at = o
-        return _copy_jobs(host, g_at, ov, at, n * odt.itemsize)
-
-    _pipeline(wplans, dev, "load", 4, emit)
     filled = {}
-    for g, i, m, odt, at, n, shape, g_at in outs_all:
-        arr = host[g_at:g_at + n * odt.itemsize].view(odt.storage).reshape(shape)
-        filled[(g, i)] = Tensor(odt, tuple(shape), arr)
+    if keep_on_device:
+        need = sum(w[4] for w in wplans)
+        free, _ = torch.cuda.mem_get_info(dev)
+        if need + (1 << 30) > free:
+            raise MemoryError(f"target world needs {need} B of HBM, {free} B free")
+        arena = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        bases, b = [], 0
+        for w in wplans:
+            bases.append(b)
+            b += w[4]
+        _pipeline(wplans, dev, "load", 4, None, sink=[arena.data_ptr() + x for x in bases])
+        for w, base in zip(wplans, bases):
+            for g, i, m, odt, at, n, shape, _ in w[3]:
+                nb = n * odt.itemsize
+                filled[(g, i)] = DeviceTensor(odt, tuple(shape), arena[base + at:base + at + nb])
+    else:
+        host = np.empty(max(total, 1), dtype=np.uint8)
+
+        def emit(o, ov):
+            _, _, _, odt, at, n, _, g_at = o
+            return _copy_jobs(host, g_at, ov, at, n * odt.itemsize)
+
+        _pipeline(wplans, dev, "load", 4, emit)
+        for g, i, m, odt, at, n, shape, g_at in outs_all:
+            arr = host[g_at:g_at + n * odt.itemsize].view(odt.storage).reshape(shape)
+            filled[(g, i)] = Tensor(odt, tuple(shape), arr)
     shards = {g: [WorldShard(m, filled[(g, i)]) for i, m in enumerate(info.records[g])]
               for g in range(tgt.world_size)}
     return LoadedWorld(tgt, spec, atomic.step, dict(atomic.metadata), shards, stats)
@@ -1076,7 +1152,9 @@ def consolidate_world(world: LoadedWorld) -> ModelState:
         for s in world.shards[g]:
             if s.tensor.dtype is not DType.F32:
                 raise ShapeError(f"{s.meta.param}.{s.meta.kind}: consolidate needs f32 shards")
-            by_unit[(s.meta.param, s.meta.kind)].append(FragmentMsg(s.meta, s.tensor.data))
+            # device-resident shards go to union() as CUDA tensors (zero copy)
+            payload = s.tensor.device if isinstance(s.tensor, DeviceTensor) else s.tensor.data
+            by_unit[(s.meta.param, s.meta.kind)].append(FragmentMsg(s.meta, payload))
     params = {}
     for p in spec.params:
         lead = spec.tied_leader(p.name)
@@ -1086,6 +1164,8 @@ def consolidate_world(world: LoadedWorld) -> ModelState:
         ts = []
         for kind in STATE_KINDS:
             arr = union(p, tgt, by_unit.get((p.name, kind), []), strict=True)
+            if _is_cuda(arr):
+                arr = arr.cpu().numpy()
             ts.append(Tensor(DType.F32, tuple(p.shape), np.ascontiguousarray(arr)))
         params[p.name] = ParamState(*ts)
     return ModelState(spec, params, world.step, dict(world.metadata))

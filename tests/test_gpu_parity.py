@@ -625,3 +625,31 @@ def test_pinned_host_staging():
         view = t2.numpy()[:16]
         del t, t2
         assert np.array_equal(view, src.numpy()[:16])
+
+
+@pytest.mark.parametrize("name", ["gqa", "moe", "pad", "cfg1"])
+def test_load_keep_on_device(golden, tmp_path, name):
+    """load(..., keep_on_device=True): shards stay in HBM (DeviceTensor) and
+    are the golden world bit for bit, with numpy materialised lazily;
+    consolidate_world reads the device shards zero-copy and recovers the
+    state."""
+    row = next(r for r in golden["pipelines"] if r["name"] == name)
+    spec = cell_spec(golden, row)
+    src_cfg, tgt_cfg = cell_cfgs(row)
+    src, _ = _src_tree(tmp_path, spec, src_cfg)
+    atom = str(tmp_path / "atomic")
+    U.convert(src, atom)
+    for dt in (DType.F32, DType.BF16):
+        world = U.load(atom, tgt_cfg, dtype=dt, keep_on_device=True)
+        first = world.shards[0][0].tensor
+        assert isinstance(first, U.DeviceTensor) and first.device.is_cuda
+        assert first._host is None  # nothing copied back yet
+        wd = {g: [(s.meta, s.tensor.data) for s in world.shards[g]] for g in world.shards}
+        assert O.world_digest(wd) == row[f"world_{dt.name}"], dt
+        if dt is DType.F32:
+            state = U.consolidate_world(world)
+            want = O.init_state(spec, 7)
+            for p in spec.params:
+                for k in ("weight", "m", "v"):
+                    got = getattr(state.params[p.name], k).data
+                    assert np.array_equal(got.view(np.uint32), want[p.name][k].view(np.uint32))
