@@ -52,7 +52,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, src_dir, tgt, S, desc, t_part)
         return
-    conv, load = [], []
+    conv, load, load_dev = [], [], []
     for r in range(args.reps + 1):
         out = os.path.join(args.root, f"atomic{r}")
         torch.cuda.synchronize()
@@ -64,6 +64,12 @@ def main():
         world = U.load(out, tgt)
         load.append(time.perf_counter() - t)
         traces["load"] = dict(A.PIPE_TRACE)
+        del world
+        t = time.perf_counter()
+        world = U.load(out, tgt, keep_on_device=True)
+        torch.cuda.synchronize()
+        load_dev.append(time.perf_counter() - t)
+        traces["load_keep_on_device"] = dict(A.PIPE_TRACE)
         del world
         shutil.rmtree(out)
     res = {True: [], False: []}
@@ -86,6 +92,8 @@ def main():
         "convert_plus_load_GBps": S / (c + lo) / 1e9, "reps": args.reps,
         "resume_fused_s": rf, "resume_fused_GBps": S / rf / 1e9,
         "resume_two_pass_s": ru, "resume_two_pass_GBps": S / ru / 1e9,
+        "load_keep_on_device_s": min(load_dev[1:]),
+        "load_keep_on_device_GBps": S / min(load_dev[1:]) / 1e9,
         "all_convert_s": conv, "all_load_s": load, "io_chunk": A.IO_CHUNK,
         "pipeline_wait_s_last_rep": traces}))
     shutil.rmtree(args.root, ignore_errors=True)
