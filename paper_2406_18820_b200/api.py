@@ -457,8 +457,8 @@ class _Step:
     def __init__(self, prog: Program, gather: bool):
         self.prog, self.gather = prog, gather
 
-    def launch(self, src: int, dst: int, st, stream) -> None:
-        self.prog.launch(self.gather, src, dst, st, stream)
+    def launch(self, src: int, dst: int, st, stream, tgt: int | None = None) -> None:
+        self.prog.launch(self.gather, src, dst if tgt is None else tgt, st, stream)
 
     def check(self, st, src: int, dst: int, stream) -> None:
         st.raise_if_bad(self.prog, src)
@@ -472,11 +472,15 @@ class _FusedStep:
 
     def __init__(self, fprog, cprog: Program, lprog: Program, atom_at: int):
         self.fprog, self.cprog, self.lprog, self.atom_at = fprog, cprog, lprog, atom_at
+        self._tgt = None
 
-    def launch(self, src: int, dst: int, st, stream) -> None:
-        self.fprog.launch(src, dst, dst + self.atom_at, st, stream)
+    def launch(self, src: int, dst: int, st, stream, tgt: int | None = None) -> None:
+        # tgt: the target shards' base when they go to a device sink instead
+        # of the dst arena (resume(keep_on_device=True))
+        self._tgt = dst + self.atom_at if tgt is None else tgt
+        self.fprog.launch(src, dst, self._tgt, st, stream)
         self.cprog.launch(True, src, dst, st, stream)
-        self.lprog.launch(False, dst, dst + self.atom_at, st, stream)
+        self.lprog.launch(False, dst, self._tgt, st, stream)
 
     def check(self, st, src: int, dst: int, stream) -> None:
         from .engine import describe_failure
@@ -489,7 +493,7 @@ class _FusedStep:
         for prog in (self.fprog, self.cprog):
             st.reset(stream)
             if prog is self.fprog:
-                prog.launch(src, dst, dst + self.atom_at, st, stream)
+                prog.launch(src, dst, self._tgt, st, stream)
             else:
                 prog.launch(True, src, dst, st, stream)
             stream.synchronize()
@@ -537,8 +541,9 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit, sink=None) -> N
     bytes)] with step a _Step/_FusedStep. ``emit(o, view)`` runs on this
     thread and returns zero-argument jobs (file-range writes, host copies)
     that the write pool runs. With ``sink`` (one device address per window)
-    the kernels write straight into device memory the caller keeps: no D2H,
-    no emit. Data-dependent failures raise after their
+    the target shards go straight into device memory the caller keeps; the
+    D2H then covers only the window's first d_at bytes (the atomic tensors
+    of a fused resume; nothing for load). Data-dependent failures raise after their
     window syncs, so a failing window never reaches emit (torn output,
     ucp/convert.py:503)."""
     import time
@@ -551,9 +556,9 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit, sink=None) -> N
     ms = max(w[2] for w in wplans)
     md = max(w[4] for w in wplans)
     h_src = [_STAGE.host_buf(f"{key}_src{i}", ms) for i in range(2)]
-    if sink is None:
-        h_dst = [_STAGE.host_buf(f"{key}_dst{i}", md) for i in range(2)]
-        d_dst = [_STAGE.dev_buf(f"{key}_dst{i}", md, dev) for i in range(2)]
+    if md or sink is None:
+        h_dst = [_STAGE.host_buf(f"{key}_dst{i}", max(md, 1)) for i in range(2)]
+        d_dst = [_STAGE.dev_buf(f"{key}_dst{i}", max(md, 1), dev) for i in range(2)]
     d_src = [_STAGE.dev_buf(f"{key}_src{i}", ms, dev) for i in range(2)]
     st = _status(dev)
     stream = torch.cuda.current_stream(dev)
@@ -619,11 +624,12 @@ def _pipeline(wplans: list, dev, key: str, n_workers: int, emit, sink=None) -> N
                 h2d_ev[w].record(s_h2d[slot])
                 stream.wait_event(h2d_ev[w])
                 st.reset(stream)
-                dst_ptr = sink[w] if sink is not None else d_dst[slot].data_ptr()
-                step.launch(d_src[slot].data_ptr(), dst_ptr, st, stream)
+                dst_ptr = d_dst[slot].data_ptr() if (md or sink is None) else 0
+                step.launch(d_src[slot].data_ptr(), dst_ptr, st, stream,
+                            None if sink is None else sink[w])
                 kern_ev[w] = torch.cuda.Event()
                 kern_ev[w].record(stream)
-                if sink is not None:
+                if sink is not None and d_at == 0:  # everything went to the sink
                     t0 = time.perf_counter()
                     kern_ev[w].synchronize()
                     tr["gpu_wait_s"] += time.perf_counter() - t0
@@ -881,7 +887,8 @@ def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass
         for w in wplans:
             bases.append(b)
             b += w[4]
-        _pipeline(wplans, dev, "load", 4, None, sink=[arena.data_ptr() + x for x in bases])
+        _pipeline([(st_, jobs, s_at, [], 0) for st_, jobs, s_at, _, _ in wplans], dev, "load", 4,
+                  None, sink=[arena.data_ptr() + x for x in bases])
         for w, base in zip(wplans, bases):
             for g, i, m, odt, at, n, shape, _ in w[3]:
                 nb = n * odt.itemsize
@@ -907,7 +914,8 @@ def load(atomic_root: str, tgt: ParallelConfig, dtype: DType = DType.F32, bypass
 
 def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1, inner: int = 1,
            dtype: DType = DType.F32, bypass: bool = True, *, device=None,
-           fused: bool = True, window_bytes: int = DEFAULT_WINDOW_BYTES) -> LoadedWorld:
+           fused: bool = True, window_bytes: int = DEFAULT_WINDOW_BYTES,
+           keep_on_device: bool = False) -> LoadedWorld:
     """Reload a distributed checkpoint under tgt (ucp/load.py:231-281): lazy
     direct read when the layouts match, else convert into scratch + load.
 
@@ -916,7 +924,8 @@ def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1,
     tensors (saved to ``scratch/atomic`` exactly as convert() would) and the
     target shards from the same registers, so the atomic tree is never read
     back. Observable results (world, stats, scratch tree, conversion count)
-    equal the two-pass path."""
+    equal the two-pass path. ``keep_on_device`` as for load(): the target
+    shards stay in HBM (DeviceTensor); only the atomic tensors cross PCIe."""
     src = codec.load_checkpoint(src_root)
     validate_model_config(src.spec, tgt)
     before = INVOCATIONS
@@ -939,6 +948,9 @@ def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1,
                 stats.per_rank[g]["bytes_read"] += nbytes
                 if meta.kind == "weight" and dtype is not DType.F32:
                     t = cast(t, dtype)
+                if keep_on_device:
+                    d = torch.from_numpy(np.ascontiguousarray(t.data).reshape(-1).view(np.uint8))
+                    t = DeviceTensor(t.dtype, t.shape, d.to(require_device(device)))
                 out.append(WorldShard(meta, t))
             shards[g] = out
         stats.conversions_invoked = INVOCATIONS - before
@@ -947,18 +959,19 @@ def resume(src_root: str, tgt: ParallelConfig, scratch: str, n_workers: int = 1,
     atomic_dir = os.path.join(scratch, "atomic")
     if fused:
         world = _resume_fused(src_root, atomic_dir, tgt, dtype, bypass, n_workers, device,
-                              window_bytes)
+                              window_bytes, keep_on_device)
     else:
         convert(src_root, atomic_dir, n_workers=n_workers, inner=inner, device=device,
                 window_bytes=window_bytes)
         world = load(atomic_dir, tgt, dtype=dtype, bypass=bypass, device=device,
-                     window_bytes=window_bytes)
+                     window_bytes=window_bytes, keep_on_device=keep_on_device)
     world.stats.conversions_invoked = INVOCATIONS - before
     return world
 
 
 def _resume_fused(src_root: str, atomic_dir: str, tgt: ParallelConfig, dtype: DType,
-                  bypass: bool, n_workers: int, device, window_bytes: int) -> LoadedWorld:
+                  bypass: bool, n_workers: int, device, window_bytes: int,
+                  keep_on_device: bool = False) -> LoadedWorld:
     """convert(src_root, atomic_dir) + load(atomic_dir, tgt) in one pass."""
     from .engine import XProgram
     from .plan import XRunTable, compile_fused
@@ -1020,16 +1033,40 @@ def _resume_fused(src_root: str, atomic_dir: str, tgt: ParallelConfig, dtype: DT
         wouts = [("a", o) for o in atoms] + [("t", o[:7] + (a_at + o[4],) + o[7:]) for o in outs]
         wins.append((_FusedStep(XProgram(fx, dev), Program(rc, dev), Program(rl, dev), a_at),
                      jobs, s_at, wouts, a_at + t_at))
-    host = np.empty(max(total, 1), dtype=np.uint8)
+    filled = {}
+    if keep_on_device:
+        # targets straight into one device arena; only the atomics go D2H
+        t_sizes = [w[4] - w[0].atom_at for w in wins]
+        need = sum(t_sizes)
+        free, _ = torch.cuda.mem_get_info(dev)
+        if need + (1 << 30) > free:
+            raise MemoryError(f"target world needs {need} B of HBM, {free} B free")
+        arena = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        bases, b = [], 0
+        for n in t_sizes:
+            bases.append(b)
+            b += n
+        _pipeline([(st_, jobs, s_at, [o for o in wo if o[0] == "a"], st_.atom_at)
+                   for st_, jobs, s_at, wo, _ in wins], dev, "res", n_workers,
+                  lambda o, ov: _write_atomic(atomic_dir, o[1], ov),
+                  sink=[arena.data_ptr() + x for x in bases])
+        for w, base in zip(wins, bases):
+            for tag, o in w[3]:
+                if tag == "t":
+                    g, i, m, odt, at, n, shape = o[:7]
+                    filled[(g, i)] = DeviceTensor(
+                        odt, tuple(shape), arena[base + at:base + at + n * odt.itemsize])
+    else:
+        host = np.empty(max(total, 1), dtype=np.uint8)
 
-    def emit(o, ov):
-        tag, o = o
-        if tag == "a":
-            return _write_atomic(atomic_dir, o, ov)
-        _, _, _, odt, _, n, _, at, g_at = o
-        return _copy_jobs(host, g_at, ov, at, n * odt.itemsize)
+        def emit(o, ov):
+            tag, o = o
+            if tag == "a":
+                return _write_atomic(atomic_dir, o, ov)
+            _, _, _, odt, _, n, _, at, g_at = o
+            return _copy_jobs(host, g_at, ov, at, n * odt.itemsize)
 
-    _pipeline(wins, dev, "res", n_workers, emit)
+        _pipeline(wins, dev, "res", n_workers, emit)
     with open(os.path.join(atomic_dir, codec.MODEL_JSON), "w") as f:
         f.write(spec_to_json(spec))
     codec.write_json(os.path.join(atomic_dir, UCP_META_JSON), {
@@ -1037,10 +1074,10 @@ def _resume_fused(src_root: str, atomic_dir: str, tgt: ParallelConfig, dtype: DT
         "source_config_sha256": fingerprint})
     atomic = load_atomic(atomic_dir)
     stats = _load_stats(atomic, spec, tgt, bypass)
-    filled = {}
-    for g, i, m, odt, at, n, shape, g_at in outs_all:
-        filled[(g, i)] = Tensor(odt, tuple(shape),
-                                host[g_at:g_at + n * odt.itemsize].view(odt.storage).reshape(shape))
+    if not keep_on_device:
+        for g, i, m, odt, at, n, shape, g_at in outs_all:
+            filled[(g, i)] = Tensor(
+                odt, tuple(shape), host[g_at:g_at + n * odt.itemsize].view(odt.storage).reshape(shape))
     shards = {g: [WorldShard(m, filled[(g, i)]) for i, m in enumerate(info.records[g])]
               for g in range(tgt.world_size)}
     return LoadedWorld(tgt, spec, atomic.step, dict(atomic.metadata), shards, stats)

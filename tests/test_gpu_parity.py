@@ -653,3 +653,30 @@ def test_load_keep_on_device(golden, tmp_path, name):
                 for k in ("weight", "m", "v"):
                     got = getattr(state.params[p.name], k).data
                     assert np.array_equal(got.view(np.uint32), want[p.name][k].view(np.uint32))
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_resume_keep_on_device(golden, tmp_path, fused):
+    """resume(..., keep_on_device=True) on the convert path (fused and
+    two-pass) and on the lazy path: the world is the golden world, the
+    scratch atomic tree is the golden tree, the shards live in HBM."""
+    row = next(r for r in golden["pipelines"] if r["name"] == "gqa")
+    spec = cell_spec(golden, row)
+    src_cfg, tgt_cfg = cell_cfgs(row)
+    src, _ = _src_tree(tmp_path, spec, src_cfg)
+    scratch = str(tmp_path / "scratch")
+    for dt in (DType.F32, DType.BF16):
+        shutil.rmtree(scratch, ignore_errors=True)
+        world = U.resume(src, tgt_cfg, scratch, dtype=dt, fused=fused, keep_on_device=True)
+        assert all(isinstance(s.tensor, U.DeviceTensor) for s in world.shards[0])
+        wd = {g: [(s.meta, s.tensor.data) for s in world.shards[g]] for g in world.shards}
+        assert O.world_digest(wd) == row[f"world_{dt.name}"], (fused, dt)
+        assert O.dir_digest(os.path.join(scratch, "atomic")) == row["atomic_digest"]
+        assert world.stats.conversions_invoked == 1
+    lazy = U.resume(src, src_cfg, str(tmp_path / "s2"), keep_on_device=True)
+    assert lazy.stats.conversions_invoked == 0
+    want = {g: [(m, a) for m, a in v] for g, v in O.partition_mem(spec, O.init_state(spec, 7),
+                                                                   src_cfg).items()}
+    got = {g: [(s.meta, s.tensor.data) for s in lazy.shards[g]] for g in lazy.shards}
+    assert O.world_digest(got) == O.world_digest(want)
+    assert lazy.shards[0][0].tensor.device.is_cuda

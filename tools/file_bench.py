@@ -72,12 +72,14 @@ def main():
         traces["load_keep_on_device"] = dict(A.PIPE_TRACE)
         del world
         shutil.rmtree(out)
-    res = {True: [], False: []}
+    res = {True: [], False: [], "dev": []}
     for r in range(args.reps + 1):
-        for fused in (True, False):
-            scratch = os.path.join(args.root, f"scratch{r}{int(fused)}")
+        for fused in (True, False, "dev"):
+            scratch = os.path.join(args.root, f"scratch{r}{fused}")
             t = time.perf_counter()
-            world = U.resume(src_dir, tgt, scratch, n_workers=args.workers, fused=fused)
+            world = U.resume(src_dir, tgt, scratch, n_workers=args.workers, fused=bool(fused),
+                             keep_on_device=fused == "dev")
+            torch.cuda.synchronize()
             res[fused].append(time.perf_counter() - t)
             if fused:
                 traces["resume_fused"] = dict(A.PIPE_TRACE)
@@ -92,6 +94,7 @@ def main():
         "convert_plus_load_GBps": S / (c + lo) / 1e9, "reps": args.reps,
         "resume_fused_s": rf, "resume_fused_GBps": S / rf / 1e9,
         "resume_two_pass_s": ru, "resume_two_pass_GBps": S / ru / 1e9,
+        "resume_fused_keep_on_device_GBps": S / min(res["dev"][1:]) / 1e9,
         "load_keep_on_device_s": min(load_dev[1:]),
         "load_keep_on_device_GBps": S / min(load_dev[1:]) / 1e9,
         "all_convert_s": conv, "all_load_s": load, "io_chunk": A.IO_CHUNK,
