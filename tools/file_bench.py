@@ -81,7 +81,7 @@ def main():
                              keep_on_device=fused == "dev")
             torch.cuda.synchronize()
             res[fused].append(time.perf_counter() - t)
-            if fused:
+            if fused is True:
                 traces["resume_fused"] = dict(A.PIPE_TRACE)
             del world
             shutil.rmtree(scratch)
