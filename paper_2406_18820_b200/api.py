@@ -1170,10 +1170,15 @@ def reshard(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: d
     enumerate_rank_records(spec, src, g)]} -> target fragments {g: [array
     per record of enumerate_rank_records(spec, tgt, g)]} (weights cast to
     dtype), through pinned host staging and the fused convert+load kernel.
+    CUDA-tensor fragments take the zero-copy device-to-device path
+    (reshard.reshard_device) and come back as CUDA tensors.
     Equivalent to convert() then load() without the file system
     (ucp/load.py:276-281); raises the same exceptions."""
-    from .reshard import ReshardPlan
+    from .reshard import ReshardPlan, reshard_device
 
+    if any(_is_cuda(t) for v in shards.values() for t in v):
+        # fragments already in HBM: zero-copy device-to-device reshard
+        return reshard_device(spec, src, tgt, shards, dtype=dtype, strict=strict)
     plan = ReshardPlan(spec, src, tgt, dtype=dtype, strict=strict, device=device, fused=fused)
     return plan.run_host(shards)
 

@@ -602,3 +602,98 @@ class ReshardPlan:
                                   W.atom[(p.name, k)], True)
             rev = W._rev = Program(tab, self.device, self.tile_bytes)
         return rev
+
+
+# --------------------------------------------------------------------------- device to device
+
+
+_TORCH_OF = {DType.F32: torch.float32, DType.BF16: torch.bfloat16, DType.F16: torch.float16}
+
+
+def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: dict,
+                   dtype: DType = DType.F32, strict: bool = True, *,
+                   window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17) -> dict:
+    """Zero-copy device-to-device reshard: source fragments already in HBM
+    ({g: [CUDA tensor per record of enumerate_rank_records(spec, src, g)]})
+    -> freshly allocated CUDA target fragments {g: [tensor per target
+    record]} (weights as torch.bfloat16 / float16 for a 16-bit dtype,
+    holding exactly the reference cast's bits).
+
+    The descriptor tables address the caller's tensors and the outputs by
+    absolute device address (every base pointer is 0), so nothing is staged:
+    one fused launch per window reads each source replica once, checks it
+    and writes every target replica. The atomic tensor is not materialised;
+    only units that cannot fuse (Partial mean / noise) go through a window
+    scratch buffer. Raises the reference's exceptions
+    (ReplicateMismatchError, PaddingError, ShapeError, ...)."""
+    from ._errors import ShapeError
+    from .engine import describe_failure
+
+    validate_model_config(spec, src)
+    validate_model_config(spec, tgt)
+    src_recs, tgt_recs = all_rank_records(spec, src), all_rank_records(spec, tgt)
+    first = next((t for v in shards.values() for t in v), None)
+    device = require_device(first.device if isinstance(first, torch.Tensor) else None)
+    frags: dict = {}
+    for g in range(src.world_size):
+        got = shards.get(g, [])
+        if len(got) != len(src_recs[g]):
+            raise ShapeError(f"rank {g}: {len(got)} fragments, want {len(src_recs[g])}")
+        for m, t in zip(src_recs[g], got):
+            n = fragment_elems(spec.param(m.param), src, m)
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
+                    and t.is_contiguous() and t.numel() == n and t.device == device):
+                raise ShapeError(f"rank {g} {m.param}.{m.kind}: want a contiguous float32 CUDA "
+                                 f"tensor of {n} elements on {device}")
+            frags.setdefault((m.param, m.kind), []).append((m, t.data_ptr(), n))
+    out: dict = {g: [] for g in range(tgt.world_size)}
+    targets: dict = {}
+    for g in range(tgt.world_size):
+        for m in tgt_recs[g]:
+            p = spec.param(m.param)
+            dt = dtype if m.kind == "weight" else DType.F32
+            t = torch.empty(fragment_shape(p, tgt, m), dtype=_TORCH_OF[dt], device=device)
+            out[g].append(t)
+            targets.setdefault((m.param, m.kind), []).append((m, t.data_ptr()))
+    status = Status(device)
+    status.reset()
+    stream = torch.cuda.current_stream(device)
+    wins = make_windows(spec.params, window_bytes)
+    scratch = torch.empty(max(max(sum(3 * align_up(4 * p.numel) for p in W.params)
+                                  for W in wins), 256), dtype=torch.uint8, device=device)
+    launched = []
+    for W in wins:
+        fx, rc, rl = XRunTable(), RunTable(), RunTable()
+        at = scratch.data_ptr()
+        for p in W.params:
+            for k in STATE_KINDS:
+                dt = dtype if k == "weight" else DType.F32
+                compile_fused(fx, rc, rl, p, src, frags.get((p.name, k), []), at, tgt,
+                              targets.get((p.name, k), []), dt, strict, False)
+                at += align_up(4 * p.numel)
+        progs = (XProgram(fx, device, tile_bytes), Program(rc, device, tile_bytes),
+                 Program(rl, device, tile_bytes))
+        progs[0].launch(0, 0, 0, status, stream)
+        progs[1].launch(True, 0, 0, status, stream)
+        progs[2].launch(False, 0, 0, status, stream)
+        launched.append(progs)
+        if len(wins) > 1:
+            # the next window reuses the scratch: keep failures attributable
+            torch.cuda.synchronize(device)
+            if status.read()[0] != (1 << 64) - 1:
+                break
+    torch.cuda.synchronize(device)
+    if status.read()[0] != (1 << 64) - 1:
+        for fused, conv, _ in launched:  # localise: re-run the source-reading launches
+            for prog in (fused, conv):
+                status.reset()
+                if prog is fused:
+                    prog.launch(0, 0, 0, status, stream)
+                else:
+                    prog.launch(True, 0, 0, status, stream)
+                torch.cuda.synchronize(device)
+                f, _ = status.read()
+                if f != (1 << 64) - 1:
+                    raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, 0)
+        raise RuntimeError("reshard reported a failure that did not reproduce")
+    return out

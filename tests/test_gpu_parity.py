@@ -680,3 +680,46 @@ def test_resume_keep_on_device(golden, tmp_path, fused):
     got = {g: [(s.meta, s.tensor.data) for s in lazy.shards[g]] for g in lazy.shards}
     assert O.world_digest(got) == O.world_digest(want)
     assert lazy.shards[0][0].tensor.device.is_cuda
+
+
+def _host_bits(t):
+    """CUDA tensor -> numpy with the reference's storage dtype (bf16 as raw u16)."""
+    if t.dtype in (torch.bfloat16, torch.float16):
+        a = t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        return a if t.dtype == torch.bfloat16 else a.view(np.float16)
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["gqa", "moe", "pad", "DenseGPT.1", "cfg1"])
+def test_reshard_device_to_device(golden, name):
+    """reshard() on CUDA fragments: zero-copy, absolute-address tables, CUDA
+    outputs equal to the golden world (f32, bf16 and f16 weights)."""
+    row = next(r for r in golden["pipelines"] if r["name"] == name)
+    spec = cell_spec(golden, row)
+    src_cfg, tgt_cfg = cell_cfgs(row)
+    shards = O.partition_mem(spec, O.init_state(spec, 7), src_cfg)
+    dev = {g: [torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).cuda() for _, a in v]
+           for g, v in shards.items()}
+    for dt in (DType.F32, DType.BF16, DType.F16):
+        out = U.reshard(spec, src_cfg, tgt_cfg, dev, dtype=dt)
+        assert all(t.is_cuda for v in out.values() for t in v)
+        recs = {g: U.enumerate_rank_records(spec, tgt_cfg, g) for g in out}
+        wd = {g: list(zip(recs[g], [_host_bits(t) for t in out[g]])) for g in out}
+        assert O.world_digest(wd) == row[f"world_{dt.name}"], (name, dt)
+
+
+def test_reshard_device_errors():
+    spec = U.make_model("GQA", {"n_layers": 2, "hidden": 64, "q_heads": 8, "kv_heads": 2})
+    src_cfg, tgt_cfg = cfg(dp=2, tp=2, zero="z1"), cfg(dp=2, tp=4, zero="z1")
+    shards = O.partition_mem(spec, O.init_state(spec, 7), src_cfg)
+    dev = {g: [torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).cuda() for _, a in v]
+           for g, v in shards.items()}
+    recs = U.enumerate_rank_records(spec, src_cfg, 3)
+    i = next(k for k, m in enumerate(recs) if m.param == "layers.1.attn_qkv" and m.kind == "weight")
+    dev[3][i][17] = 7.0
+    with pytest.raises(U.ReplicateMismatchError) as ei:
+        U.reshard(spec, src_cfg, tgt_cfg, dev)
+    assert "layers.1.attn_qkv.weight" in str(ei.value)
+    dev[3][i] = dev[3][i][:-1].clone()
+    with pytest.raises(U.ShapeError):
+        U.reshard(spec, src_cfg, tgt_cfg, dev)
