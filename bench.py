@@ -270,6 +270,36 @@ def oracle_frags(spec, src, names, threads):
     return frags
 
 
+def e2e_to_hbm(eplan, host_src, streams, stream, steps: int):
+    """The e2e leg's sample again with the targets left in HBM (a resume
+    onto the GPU): H2D of the sources + the fused reshard per step, D2H of
+    the status word only. ms per step, or None if HBM is short."""
+    import torch
+
+    try:
+        dev_tgt = torch.empty(max(eplan.tgt_total, 256), dtype=torch.uint8, device=eplan.device)
+    except RuntimeError:
+        return None
+    words = [torch.empty(2, dtype=torch.int64, pin_memory=True) for _ in range(steps)]
+    eplan.run_pinned(host_src, None, streams, dev_tgt=dev_tgt)  # warm-up, synced
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for s_ in streams:
+        s_.wait_stream(stream)
+    for k in range(steps):
+        eplan.run_pinned(host_src, None, streams, status_out=words[k], sync=False,
+                         dev_tgt=dev_tgt)
+    for s_ in streams:
+        stream.wait_stream(s_)
+    b.record(stream)
+    torch.cuda.synchronize()
+    if not all(eplan.status_ok(w) for w in words):
+        eplan._check_windows(host_src)
+    del dev_tgt
+    return a.elapsed_time(b) / steps
+
+
 def pcie_peaks(dev, stream, nbytes: int = 1 << 30, reps: int = 5) -> dict:
     """Pinned cudaMemcpyAsync peaks of this process's GPU link, measured in
     the same run (the host staging stage is judged against them):
@@ -667,6 +697,7 @@ def run_ours(args):
             if not all(eplan.status_ok(w) for w in words):
                 eplan._check_windows(host_src)
             e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+            to_hbm_ms = e2e_to_hbm(eplan, host_src, streams, stream, args.e2e_steps)
             link = pcie_peaks(dev, stream)
             S_e2e_local = eplan.state_bytes
             e2e_meta = {"h2d": int(eplan.src_total), "d2h": int(eplan.tgt_total),
@@ -694,6 +725,13 @@ def run_ours(args):
                    "api": "ReshardPlan.run_pinned (public pinned-host entry; reshard() = "
                           "pack_host + run_pinned + unpack_host)",
                    "link": link_roofline(link, e2e_meta["h2d"], e2e_meta["d2h"], e2e_ms),
+                   "to_hbm": None if to_hbm_ms is None else {
+                       "value": S_e2e_local / (to_hbm_ms / 1e3) / GB, "unit": "GB/s",
+                       "ms_per_step": to_hbm_ms, "h2d_bytes_per_step": e2e_meta["h2d"],
+                       "d2h_bytes_per_step": 16,
+                       "what": "resume straight onto the GPU: the same sample and host sources, "
+                               "targets kept in HBM (run_pinned(dev_tgt=...)), D2H = the "
+                               "status word; rank-local"},
                    "sample": f"{len(names)} params ({names[0]} .. {names[-1]}; "
                              f"{S_e2e_local / GB:.2f} GB state/rank) from pinned host memory: "
                              f"H2D + fused reshard + D2H in {e2e_meta['windows']} double-buffered "

@@ -414,17 +414,22 @@ class ReshardPlan:
                 hv[at:at + 4 * n] = a.view(np.uint8)
         return host
 
-    def stream_host(self, host_src: torch.Tensor, host_tgt: torch.Tensor, windows=None,
-                    streams=None, slots: int | None = None) -> None:
+    def stream_host(self, host_src: torch.Tensor, host_tgt: torch.Tensor | None, windows=None,
+                    streams=None, slots: int | None = None,
+                    dev_tgt: torch.Tensor | None = None) -> None:
         """Pinned host source arena -> device -> pinned host target arena,
         multi-buffered (``slots`` device slots per direction, default
         ``self.host_slots``) over windows on three streams. Asynchronous:
-        the caller synchronises (the last event is on the D2H stream)."""
+        the caller synchronises (the last event is on the D2H stream).
+
+        ``dev_tgt`` (a device byte tensor of ``tgt_total`` bytes, host_tgt
+        None): the target fragments stay in HBM at their arena offsets --
+        a resume straight onto the GPU; only the sources cross PCIe."""
         wins = self.windows if windows is None else windows
         s_in, s_cmp, s_out = streams or self.host_streams()
         ns = max(2, slots or self.host_slots)
         dsrc = [self.buf(f"ssrc{j}", self.max_src) for j in range(ns)]
-        dtgt = [self.buf(f"stgt{j}", self.max_tgt) for j in range(ns)]
+        dtgt = [self.buf(f"stgt{j}", self.max_tgt) for j in range(ns)] if dev_tgt is None else None
         atom = self.buf("atom", self.max_atom)
         # the caller's stream first: work it queued before this call (the
         # status reset, writes into host_src) must precede our copies and
@@ -452,15 +457,17 @@ class ReshardPlan:
             s_cmp.wait_event(ev_in[i])
             if i >= ns:
                 s_cmp.wait_event(ev_out[i - ns])
-            W.fused.launch(dsrc[slot].data_ptr(), atom.data_ptr(), dtgt[slot].data_ptr(),
-                           self.status, s_cmp)
+            tptr = (dtgt[slot].data_ptr() if dev_tgt is None
+                    else dev_tgt.data_ptr() + W.tgt_base)
+            W.fused.launch(dsrc[slot].data_ptr(), atom.data_ptr(), tptr, self.status, s_cmp)
             W.conv.launch(True, dsrc[slot].data_ptr(), atom.data_ptr(), self.status, s_cmp)
-            W.load.launch(False, atom.data_ptr(), dtgt[slot].data_ptr(), self.status, s_cmp)
+            W.load.launch(False, atom.data_ptr(), tptr, self.status, s_cmp)
             ev_cmp[i].record(s_cmp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_cmp[i])
-                host_tgt[W.tgt_base:W.tgt_base + W.tgt_bytes].copy_(dtgt[slot][:W.tgt_bytes],
-                                                                    non_blocking=True)
+                if dev_tgt is None:
+                    host_tgt[W.tgt_base:W.tgt_base + W.tgt_bytes].copy_(
+                        dtgt[slot][:W.tgt_bytes], non_blocking=True)
                 ev_out[i].record(s_out)
         return ev_out[-1] if wins else None
 
@@ -476,8 +483,9 @@ class ReshardPlan:
                 out.setdefault(g, {})[i] = hv[at:at + dt.itemsize * n].view(dt.storage).reshape(shape)
         return {g: [d[i] for i in sorted(d)] for g, d in out.items()}
 
-    def run_pinned(self, host_src: torch.Tensor, host_tgt: torch.Tensor, streams=None,
-                   status_out: torch.Tensor | None = None, sync: bool = True) -> None:
+    def run_pinned(self, host_src: torch.Tensor, host_tgt: torch.Tensor | None, streams=None,
+                   status_out: torch.Tensor | None = None, sync: bool = True,
+                   dev_tgt: torch.Tensor | None = None) -> None:
         """Public zero-copy entry: pinned host source arena (``pack_host``
         layout) -> H2D -> fused convert+load -> D2H into the pinned host
         target arena (``unpack_host`` layout), double-buffered over windows.
@@ -489,7 +497,7 @@ class ReshardPlan:
         PaddingError, ...); without it the caller checks ``status_out``
         later with ``check_status_word``."""
         streams = streams or self.host_streams()
-        self.stream_host(host_src, host_tgt, None, streams)
+        self.stream_host(host_src, host_tgt, None, streams, dev_tgt=dev_tgt)
         if status_out is not None:
             with torch.cuda.stream(streams[2]):
                 status_out.copy_(self.status.t, non_blocking=True)

@@ -377,6 +377,17 @@ def test_run_pinned_async_status_word():
     plan.status.reset()
     with pytest.raises(U.ReplicateMismatchError):
         plan.run_pinned(h_src, h_tgt, status_out=word)
+    # targets kept in HBM (resume onto the GPU): same bytes as the host arena
+    h_src = plan.pack_host({g: [a for _, a in v] for g, v in shards.items()}, h_src)
+    plan.status.reset()
+    plan.run_pinned(h_src, h_tgt)
+    d_tgt = torch.zeros(max(plan.tgt_total, 256), dtype=torch.uint8, device="cuda")
+    plan.status.reset()
+    plan.run_pinned(h_src, None, dev_tgt=d_tgt)
+    a, b = plan.unpack_host(h_tgt), plan.unpack_host(d_tgt.cpu())  # fragments, not the pad gaps
+    for g in a:
+        for x, y in zip(a[g], b[g]):
+            assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
 
 
 def test_shard_hy_union_gpu():
