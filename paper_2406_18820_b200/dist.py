@@ -249,6 +249,124 @@ class PeerBuffers:
             self.local = 0
 
 
+def _ipc_arenas(nbytes: int, group=None) -> tuple:
+    """cudaMalloc ``nbytes`` here, export it, all_gather every rank's handle
+    and map the others: (local address, [address of rank r's arena valid in
+    this process], [mapped addresses to close])."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import _native
+    from ._errors import from_status
+
+    lib = _native.lib()
+    ptr = ctypes.c_void_p()
+    rc = lib.ucp_dev_alloc(max(int(nbytes), 256), ctypes.byref(ptr))
+    if rc:
+        raise from_status(rc, "ucp_dev_alloc")
+    handle = (ctypes.c_ubyte * 64)()
+    rc = lib.ucp_ipc_export(ctypes.c_void_p(ptr.value), handle)
+    if rc:
+        raise from_status(rc, "ucp_ipc_export")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(handle), group=group)
+    bases, mapped = [], []
+    for r, hb in enumerate(handles):
+        if r == rank:
+            bases.append(ptr.value)
+            continue
+        m = ctypes.c_void_p()
+        rc = lib.ucp_ipc_open((ctypes.c_ubyte * 64).from_buffer_copy(hb), ctypes.byref(m))
+        if rc:
+            raise from_status(rc, f"ucp_ipc_open(rank {r})")
+        bases.append(m.value)
+        mapped.append(m.value)
+    return ptr.value, bases, mapped
+
+
+class PeerSources:
+    """Source fragments homed on their source rank's GPU (source rank g on
+    GPU g mod world), one IPC-exported arena per GPU, every arena mapped in
+    every process. The param owner's fused kernel then reads the fragments
+    it needs straight from the home GPUs (NVLink / NVSwitch peer loads) and
+    -- with PeerBuffers -- stores the targets straight into their home GPUs:
+    the whole distributed reshard is one kernel per window and no
+    collective. Layout is deterministic: on home h, source ranks g = h,
+    h + world, ... in order, each rank's records in manifest order."""
+
+    def __init__(self, spec: ModelSpec, src, group=None):
+        import torch.distributed as dist
+
+        from .engine import align_up
+        from .layout import all_rank_records
+        from .plan import fragment_elems
+
+        self.spec, self.src = spec, src
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.recs = all_rank_records(spec, src)
+        self.offset, sizes = {}, [0] * self.world
+        for g in range(src.world_size):
+            h = g % self.world
+            for i, m in enumerate(self.recs[g]):
+                n = fragment_elems(spec.param(m.param), src, m)
+                self.offset[(g, i)] = (h, sizes[h])
+                sizes[h] += align_up(4 * n)
+        self.nbytes = sizes[self.rank]
+        self.local, self.bases, self._mapped = _ipc_arenas(self.nbytes, group)
+
+    def addr(self, g: int, i: int) -> int:
+        """Device address, valid in this process, of source rank g's record i."""
+        h, off = self.offset[(g, i)]
+        return self.bases[h] + off
+
+    def fill(self, seed: int = 7) -> None:
+        """Synthesize this GPU's homed fragments: init_state(spec, seed) one
+        param at a time (ucp_gen_state) sliced under the source layout by the
+        load kernels, written at their absolute local addresses."""
+        import torch
+
+        from .engine import Program, Status, gen_state, require_device
+        from .plan import RunTable, compile_extract
+        from .spec import STATE_KINDS, DType
+        from .synth import stream_base
+
+        dev = require_device(None)
+        mine = {}
+        for g in range(self.src.world_size):
+            if g % self.world == self.rank:
+                for i, m in enumerate(self.recs[g]):
+                    mine.setdefault((m.param, m.kind), []).append((m, self.addr(g, i)))
+        st = Status(dev)
+        st.reset()
+        for p in self.spec.params:
+            lead = self.spec.tied_leader(p.name)
+            full = torch.empty(max(p.numel, 1), dtype=torch.float32, device=dev)
+            for k in STATE_KINDS:
+                tg = mine.get((p.name, k))
+                if not tg:
+                    continue
+                gen_state(stream_base(seed, lead, k), 0, p.numel, k == "v", full.data_ptr())
+                tab = RunTable()
+                compile_extract(tab, p, self.src, tg, full.data_ptr(), DType.F32)
+                Program(tab, dev).launch(False, 0, 0, st)
+                torch.cuda.synchronize(dev)  # `full` is reused for the next kind
+
+    def close(self) -> None:
+        import ctypes
+
+        from . import _native
+
+        lib = _native.lib()
+        for m in self._mapped:
+            lib.ucp_ipc_close(ctypes.c_void_p(m))
+        self._mapped = []
+        if self.local:
+            lib.ucp_dev_free(ctypes.c_void_p(self.local))
+            self.local = 0
+
+
 class NcclComm:
     """libucp_b200_comm.so communicator (one per process / GPU). Rank 0's
     unique id is distributed over the default torch.distributed group."""

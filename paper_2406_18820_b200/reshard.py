@@ -135,7 +135,7 @@ class ReshardPlan:
                  dtype: DType = DType.F32, strict: bool = True, params=None, device=None,
                  window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17, fused: bool = False,
                  materialize_atomic: bool = True, home_of=None, n_homes: int = 1,
-                 peer=None):
+                 peer=None, src_peer=None):
         validate_model_config(spec, src)
         validate_model_config(spec, tgt)
         self.spec, self.src, self.tgt, self.dtype, self.strict = spec, src, tgt, dtype, strict
@@ -144,6 +144,9 @@ class ReshardPlan:
         # peer = (ExchangePlan, PeerBuffers): target fragments are written
         # straight into their home GPU's receive slot (absolute addresses)
         self.peer = peer
+        # src_peer = dist.PeerSources: source fragments stay on their source
+        # rank's GPU and are read at absolute (IPC-mapped) addresses
+        self.src_peer = src_peer
         self.device = require_device(device)
         self.tile_bytes = tile_bytes
         names = None if params is None else set(params)
@@ -177,6 +180,8 @@ class ReshardPlan:
             fx = XRunTable()
             src_by_unit, tgt_by_unit = {}, {}
             for g, i, m, off, n in W.src_frags:
+                if self.src_peer is not None:
+                    off = self.src_peer.addr(g, i)
                 src_by_unit.setdefault((m.param, m.kind), []).append((m, off, n))
             for g, i, m, off, n, dt in W.tgt_frags:
                 if self.peer is not None:
@@ -198,8 +203,9 @@ class ReshardPlan:
                     else:
                         compile_union(conv, p, self.src, frags, a, self.strict)
                         compile_extract(load, p, self.tgt, tg, a, dt)
-                    compile_extract(synth, p, self.src, [(m, off) for m, off, _ in frags], a,
-                                    DType.F32)
+                    if self.src_peer is None:
+                        compile_extract(synth, p, self.src, [(m, off) for m, off, _ in frags], a,
+                                        DType.F32)
             W.conv = Program(conv, self.device, self.tile_bytes)
             W.load = Program(load, self.device, self.tile_bytes)
             W.synth = Program(synth, self.device, self.tile_bytes)
@@ -268,12 +274,12 @@ class ReshardPlan:
         """One device-resident reshard of every window: inputs already in the
         source arena, targets into a two-slot HBM ring. events[i] (optional)
         gets 4 CUDA events around the fused / convert / load launches."""
-        arena = self._bufs["src_arena"]
+        arena = self._bufs["src_arena"] if self.src_peer is None else None
         atom = self.buf("atom", self.max_atom)
         ring = [self.buf("tgt0", self.max_tgt), self.buf("tgt1", self.max_tgt)]
         for i, W in enumerate(self.windows):
             ev = events[i] if events is not None else None
-            src_ptr = arena.data_ptr() + W.src_base
+            src_ptr = 0 if arena is None else arena.data_ptr() + W.src_base
             if ev:
                 ev[0].record(stream)
             tgt_ptr = 0 if self.peer is not None else ring[i % 2].data_ptr()
@@ -374,9 +380,9 @@ class ReshardPlan:
         first, _ = self.status.read()
         if first == (1 << 64) - 1:
             return
-        arena = self._bufs["src_arena"]
+        arena = self._bufs["src_arena"] if self.src_peer is None else None
         for W in self.windows:
-            self._locate(W, arena.data_ptr() + W.src_base)
+            self._locate(W, 0 if arena is None else arena.data_ptr() + W.src_base)
         raise RuntimeError("reshard reported a failure that did not reproduce")
 
     def _locate(self, W: Window, src_ptr: int) -> None:
@@ -385,11 +391,12 @@ class ReshardPlan:
         from .engine import describe_failure
 
         atom = self.buf("atom", self.max_atom)
-        tgt = self.buf("tgt0", self.max_tgt)
+        # rank-homed targets are absolute peer addresses (base 0)
+        tgt_ptr = 0 if self.peer is not None else self.buf("tgt0", self.max_tgt).data_ptr()
         for prog in (W.fused, W.conv):
             self.status.reset()
             if prog is W.fused:
-                prog.launch(src_ptr, atom.data_ptr(), tgt.data_ptr(), self.status)
+                prog.launch(src_ptr, atom.data_ptr(), tgt_ptr, self.status)
             else:
                 prog.launch(True, src_ptr, atom.data_ptr(), self.status)
             torch.cuda.synchronize(self.device)

@@ -76,7 +76,16 @@ def test_peer_homed_fused_reshard_two_processes():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(world)]
+    import queue
+    import time
+
+    res, deadline = [], time.time() + 600
+    while len(res) < world:
+        try:
+            res.append(q.get(timeout=5))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead and time.time() < deadline, f"worker failed: exit codes {dead}"
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
