@@ -63,6 +63,10 @@ def parse():
     ap.add_argument("--home", default="param", choices=["param", "rank"],
                     help="param: targets stay on the param-owner GPU (no collective); rank: "
                          "target rank g is homed on GPU g mod N, one NCCL all-to-all-v per window")
+    ap.add_argument("--src-home", default="param", choices=["param", "rank"],
+                    help="param: each rank's source fragments are staged on the param-owner GPU; "
+                         "rank: source rank g's fragments live on GPU g mod N and the owner's "
+                         "fused kernel reads them over IPC peer memory (dist.PeerSources)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl", "torch"],
                     help="rank-homed transport: peer = the reshard kernel stores into the home "
                          "GPU's CUDA-IPC-mapped buffer over NVLink; nccl = all-to-all-v per "
@@ -455,7 +459,8 @@ def run_ours(args):
     from paper_2406_18820_b200.dist import init_process_group, owned_params
     from paper_2406_18820_b200.reshard import ReshardPlan
 
-    rank, world, local = init_process_group(args.dist_backend, force=args.home == "rank")
+    rank, world, local = init_process_group(args.dist_backend,
+                                            force=args.home == "rank" or args.src_home == "rank")
     local = local % torch.cuda.device_count()  # >1 rank per GPU only for gloo smoke tests
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -475,7 +480,16 @@ def run_ours(args):
         exch = build_exchange(spec, src, tgt, world, rank, int(args.window_gb * GB), wdt)
         if args.exchange == "peer":
             peer = PeerBuffers(exch.max_recv, n_slots=2)
-    plan = ReshardPlan(spec, src, tgt, params=mine, device=dev, dtype=wdt,
+    sources = None
+    if args.src_home == "rank":
+        from paper_2406_18820_b200.dist import PeerSources
+
+        sources = PeerSources(spec, src)
+        sources.fill(7)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    plan = ReshardPlan(spec, src, tgt, params=mine, device=dev, dtype=wdt, src_peer=sources,
                        window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024,
                        fused=not args.unfused, strict=not args.non_strict,
                        materialize_atomic=not args.no_atomic,
@@ -484,14 +498,20 @@ def run_ours(args):
                        peer=(exch, peer) if peer is not None else None)
     S_local = plan.state_bytes
     free, _ = torch.cuda.mem_get_info(dev)
-    need = plan.src_total + plan.max_atom * 3 + plan.max_tgt * 2 + (2 << 30)
+    need = (0 if sources else plan.src_total) + plan.max_atom * 3 + plan.max_tgt * 2 + (2 << 30)
     windowed = args.windowed or need > free
-    if not windowed:
+    if sources is not None and windowed:
+        raise SystemExit("--src-home rank needs every homed source fragment resident")
+    if not windowed and sources is None:
         plan.synthesize(7)
     torch.cuda.synchronize()
 
     parity = None
-    if not args.no_verify:
+    if sources is not None:
+        parity = {"note": "--src-home rank: sources in PeerSources arenas; the status word "
+                          "(replica checks) is checked after warm-up and the timed steps, the "
+                          "bytes by tests/test_gpu_peer_sources.py"}
+    elif not args.no_verify:
         parity = plan.verify(7, windowed=windowed)
         for k in ("atom_ref", "atom_back"):
             plan._bufs.pop(k, None)
@@ -775,6 +795,9 @@ def run_ours(args):
                      if windowed else "whole source arena resident in HBM",
                      "strict_replicate": not args.non_strict,
                      "target_weight_dtype": args.dtype,
+                     "source_home": ("source rank g on GPU g mod N, read over IPC peer memory "
+                                     "(dist.PeerSources)" if sources is not None
+                                     else "staged on the param-owner GPU"),
                      "atomic_materialised": not args.no_atomic},
           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
           "gpu_launches": gpu_launches, "parity": parity}, rank)
@@ -784,6 +807,10 @@ def run_ours(args):
         peer.close()
     if ncomm is not None:
         ncomm.close()
+    if sources is not None:
+        if world > 1:
+            dist.barrier()
+        sources.close()
     if dist.is_initialized():
         dist.destroy_process_group()
 
