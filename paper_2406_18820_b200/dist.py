@@ -286,6 +286,26 @@ def _ipc_arenas(nbytes: int, group=None) -> tuple:
     return ptr.value, bases, mapped
 
 
+def peer_source_layout(spec: ModelSpec, src, world: int) -> tuple:
+    """({(g, i): (home GPU, byte offset in its arena)}, [arena bytes per
+    GPU]) for source rank g's record i homed on GPU g mod world: ranks in
+    order, records in manifest order, 256-B aligned. Identical on every
+    process (no communication needed to address a peer's fragment)."""
+    from .engine import align_up
+    from .layout import all_rank_records
+    from .plan import fragment_elems
+
+    recs = all_rank_records(spec, src)
+    offset, sizes = {}, [0] * world
+    for g in range(src.world_size):
+        h = g % world
+        for i, m in enumerate(recs[g]):
+            n = fragment_elems(spec.param(m.param), src, m)
+            offset[(g, i)] = (h, sizes[h])
+            sizes[h] += align_up(4 * n)
+    return offset, sizes
+
+
 class PeerSources:
     """Source fragments homed on their source rank's GPU (source rank g on
     GPU g mod world), one IPC-exported arena per GPU, every arena mapped in
@@ -299,20 +319,12 @@ class PeerSources:
     def __init__(self, spec: ModelSpec, src, group=None):
         import torch.distributed as dist
 
-        from .engine import align_up
         from .layout import all_rank_records
-        from .plan import fragment_elems
 
         self.spec, self.src = spec, src
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.recs = all_rank_records(spec, src)
-        self.offset, sizes = {}, [0] * self.world
-        for g in range(src.world_size):
-            h = g % self.world
-            for i, m in enumerate(self.recs[g]):
-                n = fragment_elems(spec.param(m.param), src, m)
-                self.offset[(g, i)] = (h, sizes[h])
-                sizes[h] += align_up(4 * n)
+        self.offset, sizes = peer_source_layout(spec, src, self.world)
         self.nbytes = sizes[self.rank]
         self.local, self.bases, self._mapped = _ipc_arenas(self.nbytes, group)
 

@@ -170,3 +170,26 @@ def test_gloo_rank_homed_exchange():
         assert p.exitcode == 0
     for rank, ok, homed in res:
         assert ok == homed > 0
+
+
+def test_peer_source_layout_is_disjoint_and_complete():
+    """dist.peer_source_layout: every source record of every rank gets a
+    256-B aligned, non-overlapping range on its home GPU (g mod world)."""
+    from paper_2406_18820_b200.dist import peer_source_layout
+    from paper_2406_18820_b200.layout import all_rank_records
+    from paper_2406_18820_b200.plan import fragment_elems
+
+    for name, world in (("cfg2", 1), ("cfg3", 2), ("cfg5", 8), ("cfg4", 3)):
+        spec, src, _, _ = U.bench_config(name, {"cfg2": 1, "cfg3": 2, "cfg5": 4, "cfg4": 1}[name])
+        off, sizes = peer_source_layout(spec, src, world)
+        recs = all_rank_records(spec, src)
+        spans = {h: [] for h in range(world)}
+        for g in range(src.world_size):
+            for i, m in enumerate(recs[g]):
+                h, o = off[(g, i)]
+                assert h == g % world and o % 256 == 0
+                spans[h].append((o, o + 4 * fragment_elems(spec.param(m.param), src, m)))
+        for h, sp in spans.items():
+            sp.sort()
+            assert all(a[1] <= b[0] for a, b in zip(sp, sp[1:]))
+            assert not sp or sp[-1][1] <= sizes[h]
