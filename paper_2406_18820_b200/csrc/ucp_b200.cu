@@ -552,15 +552,59 @@ __global__ void __launch_bounds__(1024) runtile_scan_kernel(ucp_runtile* rt, Cla
 // every BASELINE config. Register budget: 4 float4 of primary + 4 float4 of
 // replica per lane, no local memory.
 
+#ifndef UCP_HW_CVT
+#define UCP_HW_CVT 1  // 0: bit-formula casts everywhere (the pre-r01bj vector path)
+#endif
+
+// 4 x f32 -> 4 x bf16 / f16 bits, packed. The hardware pair conversions
+// (cvt.rn.{bf16,f16}x2.f32: IEEE round-to-nearest-even, denormals kept,
+// overflow to inf) equal the reference casts for every non-NaN input; NaN
+// inputs (payloads, sNaN) take the bit-exact formulas (bf16_bits / f16_bits).
+// Two cvt + four compares per vector instead of ~30 integer ops: the
+// 16-bit-target kernels were issue-bound (61 % issue slots, r01bi).
+// NaN -> 16-bit bits exactly as the reference casts do (bf16:
+// ucp/tensor.py:192-201 keeps the top payload bits and sets the quiet bit;
+// f16: numpy keeps the truncated payload, forced non-zero, no quieting).
+template <int DT>
+__device__ __forceinline__ uint32_t nan16(uint32_t u) {
+  if constexpr (DT == UCP_DT_BF16) {
+    return ((u >> 16) | 0x40u) & 0xffffu;
+  } else {
+    const uint32_t r = 0x7c00u + ((u & 0x007fffffu) >> 13);
+    return ((u & 0x80000000u) >> 16) + (r == 0x7c00u ? 0x7c01u : r);
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ uint2 pack16x4(const float4& v) {
+  uint2 h;
+#if UCP_HW_CVT
+  if constexpr (DT == UCP_DT_BF16) {
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h.x) : "f"(v.y), "f"(v.x));
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h.y) : "f"(v.w), "f"(v.z));
+  } else {
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h.x) : "f"(v.y), "f"(v.x));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h.y) : "f"(v.w), "f"(v.z));
+  }
+  if ((v.x != v.x) | (v.y != v.y) | (v.z != v.z) | (v.w != v.w)) {  // rare: NaN payloads
+    if (v.x != v.x) h.x = (h.x & 0xffff0000u) | nan16<DT>(bits_of(v.x));
+    if (v.y != v.y) h.x = (h.x & 0x0000ffffu) | (nan16<DT>(bits_of(v.y)) << 16);
+    if (v.z != v.z) h.y = (h.y & 0xffff0000u) | nan16<DT>(bits_of(v.z));
+    if (v.w != v.w) h.y = (h.y & 0x0000ffffu) | (nan16<DT>(bits_of(v.w)) << 16);
+  }
+#else
+  h.x = cvt16(v.x, DT) | (cvt16(v.y, DT) << 16);
+  h.y = cvt16(v.z, DT) | (cvt16(v.w, DT) << 16);
+#endif
+  return h;
+}
+
 template <int DT>
 __device__ __forceinline__ void store4(char* p, const float4& v) {
   if constexpr (DT == UCP_DT_F32) {
     st4(p, v);
   } else {
-    uint2 h;
-    h.x = cvt16(v.x, DT) | (cvt16(v.y, DT) << 16);
-    h.y = cvt16(v.z, DT) | (cvt16(v.w, DT) << 16);
-    st2u(p, h);
+    st2u(p, pack16x4<DT>(v));
   }
 }
 
