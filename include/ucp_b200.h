@@ -119,7 +119,7 @@ typedef struct ucp_xrun {
   uint8_t pad0_;
   uint16_t pad1_;
   uint32_t tag;
-  uint32_t flags;      /* UCP_RUN_VEC is required; UCP_RUN_ROWSPLIT as for ucp_run */
+  uint32_t flags;      /* UCP_RUN_VEC (vector classes) or clear (GENERAL); UCP_RUN_ROWSPLIT */
 } ucp_xrun;            /* 64 bytes */
 
 /* Per-run tiling, parallel to the run array. The host fills per / tpr /
@@ -191,9 +191,10 @@ int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, f
 /*
  * Fused convert + load (the in-memory resume() path, ucp/load.py:276-281):
  * class_info as for ucp_convert_gather, runs sorted by class. Classes
- * VEC_F32 / VEC_BF16 / VEC_F16 hold runs of one target dtype each; for fused
- * tables the GENERAL slot means "mixed target dtypes": one launch whose CTAs
- * dispatch on their run's dtype (kernel reshard_fused_mixed).
+ * VEC_F32 / VEC_BF16 / VEC_F16 hold vector runs (UCP_RUN_VEC: one shared 16-B
+ * phase) of one target dtype each; for fused tables the GENERAL slot holds
+ * phase-mismatched cells (UCP_RUN_VEC clear, any target dtype), run on a
+ * coalesced 4-B path (kernel reshard_fused_scalar).
  */
 int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
                       const ucp_runtile* rt, const int64_t* class_info, const void* src_base,

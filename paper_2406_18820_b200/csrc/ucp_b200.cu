@@ -1034,20 +1034,84 @@ __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f16(UCP_FUSE
   fused_body<UCP_DT_F16>(runs, aux, rt, r0, nr, n_tiles, sb, ab, db, st);
 }
 
-// Mixed target dtypes in one grid (bf16/f16 weights next to f32 moments):
-// each CTA dispatches on its run's dtype. One launch interleaves the
-// read-heavy weight tiles (strict replicas, 2-B targets) with the
-// write-heavy moment tiles, instead of two launches with skewed DRAM
-// read/write mixes.
-__global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_mixed(UCP_FUSED_ARGS) {
+// Fused cells whose sources, atomic and targets do not share one 16-B
+// phase (ZeRO partitions of dp = 3, 5, ...): the same single pass with
+// coalesced 4-B accesses -- lane l takes elements l, l + 32, ... of a
+// 512-element row segment, 4 per lane per step for memory-level
+// parallelism.
+template <int DT>
+__device__ __forceinline__ void fused_tile_scalar(const uint64_t* __restrict__ aux,
+                                                  const ucp_tile& tile, const ucp_xrun& s_run,
+                                                  uint64_t* s_aux, const char* __restrict__ sb,
+                                                  char* __restrict__ ab, char* __restrict__ db,
+                                                  ucp_status* st) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  constexpr int U = 4;
+  const int ns = s_run.n_src, nd = s_run.n_dst;
+  const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
+  if (n_aux > 0) {
+    for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
+    __syncthreads();
+  }
+  uint32_t nrows, nc;
+  if (s_run.flags & UCP_RUN_ROWSPLIT) { nrows = 1; nc = tile.count; }
+  else { nrows = tile.count; nc = s_run.cols; }
+  const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nrows * spr;
+  const uint64_t s0 = s_run.src, a0 = s_run.atom, d0 = s_run.dst;
+  const bool atom_on = a0 != ~0ull;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t it = warp; it < n_items; it += kWarps) {
+    const uint32_t rr = it / spr;
+    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
+    const uint32_t row = tile.row0 + rr;
+    const uint64_t srow = (uint64_t)row * s_run.src_pitch + cs;
+    const uint64_t arow = (uint64_t)row * s_run.atom_pitch + cs;
+    const uint64_t drow = (uint64_t)row * s_run.dst_pitch + cs;
+    bool bad = false;
+    uint32_t bad_e = 0xffffffffu;
+    for (uint32_t base = 0; base < len; base += 32u * U) {
+      float x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t e = base + lane + 32u * u;
+        if (e < len) x[u] = ld_stream1(sb + s0 + 4 * (srow + e));
+      }
+      for (int k = 1; k < ns; ++k) {
+        const char* pk = sb + s_aux[k - 1];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t e = base + lane + 32u * u;
+          if (e < len && bits_of(ld_stream1(pk + 4 * (srow + e))) != bits_of(x[u])) {
+            bad = true;
+            bad_e = min(bad_e, e);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t e = base + lane + 32u * u;
+        if (e >= len) continue;
+        if (atom_on) *reinterpret_cast<float*>(ab + a0 + 4 * (arow + e)) = x[u];
+        for (int d = 0; d < nd; ++d)
+          store1<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + (uint64_t)ESZ * (drow + e), x[u]);
+      }
+    }
+    report(bad, row * s_run.cols + cs + bad_e, tile.run, st);
+  }
+}
+
+// The GENERAL class of fused tables: phase-mismatched cells, scalar path;
+// each CTA dispatches on its run's target dtype.
+__global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_scalar(UCP_FUSED_ARGS) {
   (void)n_tiles;
   __shared__ __align__(16) ucp_xrun s_run;
   __shared__ uint4 s_t;
   __shared__ uint64_t s_aux[kMaxAux];
   const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
-  if (s_run.dtype == UCP_DT_F32) fused_tile<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st);
-  else if (s_run.dtype == UCP_DT_BF16) fused_tile<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st);
-  else fused_tile<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st);
+  if (s_run.dtype == UCP_DT_F32) fused_tile_scalar<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st);
+  else if (s_run.dtype == UCP_DT_BF16) fused_tile_scalar<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st);
+  else fused_tile_scalar<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st);
 }
 
 // ---------------------------------------------------------------- entry kernels
@@ -1266,9 +1330,9 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
   for (int c = 0; c < UCP_NCLASS; ++c) {
     const uint32_t n = nt[c];
     if (n == 0) continue;
-    if (c == UCP_CLASS_GENERAL) {  // fused tables: mixed target dtypes, per-tile dispatch
-      reshard_fused_mixed<<<dim3(n), dim3(kThreads), 0, s>>>(runs, aux, rt, cr.begin[c], cr.n[c], n,
-                                                           sb, ab, db, status);
+    if (c == UCP_CLASS_GENERAL) {  // fused tables: phase-mismatched cells, scalar path
+      reshard_fused_scalar<<<dim3(n), dim3(kThreads), 0, s>>>(runs, aux, rt, cr.begin[c], cr.n[c], n,
+                                                            sb, ab, db, status);
       continue;
     }
 #if UCP_PERSISTENT

@@ -28,8 +28,6 @@ from __future__ import annotations
 from collections import defaultdict
 from dataclasses import dataclass, field
 
-import os
-
 import numpy as np
 
 from ._errors import (
@@ -679,11 +677,6 @@ def fragment_shape(p: ParamSpec, cfg: ParallelConfig, meta: RecordMeta) -> tuple
 class XRunTable:
     """Fused convert+load runs (ucp_xrun) for one ucp_reshard_fused launch."""
 
-    # UCP_FUSED_MIXED=1: all target dtypes in one launch (reshard_fused_mixed).
-    # Measured 0.5-1 % slower than one launch per dtype for bf16 targets
-    # (DESIGN §3 tuning log), so off by default.
-    MIXED = os.environ.get("UCP_FUSED_MIXED", "0") != "0"
-
     def __init__(self):
         self._rows: list = []
         self._aux: list = []
@@ -691,14 +684,16 @@ class XRunTable:
         self.src_bytes = 0
         self.atom_bytes = 0
         self.dst_bytes = 0
-        self.mixed = self.MIXED
 
     def unit(self, param: str, kind: str) -> int:
         self.units.append(Unit(param, kind))
         return len(self.units) - 1
 
     def add(self, *, srcs, atom, dsts, src_pitch, atom_pitch, dst_pitch, rows, cols, dtype, tag,
-            labels=None) -> None:
+            labels=None, vec: bool = True) -> None:
+        """vec: every source, the atomic and every destination share one
+        16-B phase (the vector kernels); otherwise the cell runs on the
+        scalar fused path (coalesced 4-B accesses, reshard_fused_mixed)."""
         if rows == 0 or cols == 0:
             return
         if labels is not None:
@@ -707,7 +702,8 @@ class XRunTable:
         self._aux.extend(srcs[1:])
         self._aux.extend(dsts[1:])
         self._rows.append((srcs[0], atom, dsts[0] if dsts else 0, src_pitch, atom_pitch, dst_pitch,
-                           rows, cols, aux_at, len(srcs), len(dsts), dtype.value, tag, RUN_VEC))
+                           rows, cols, aux_at, len(srcs), len(dsts), dtype.value, tag,
+                           RUN_VEC if vec else 0))
         n = rows * cols
         self.src_bytes += 4 * n * len(srcs)
         self.atom_bytes += 0 if atom == NO_ATOM else 4 * n
@@ -725,11 +721,8 @@ class XRunTable:
         extra = np.where(runs["atom"] == np.uint64(NO_ATOM), 0, 4).astype(np.int64)
         cls = np.select([runs["dtype"] == DType.F32.value, runs["dtype"] == DType.BF16.value],
                         [CLASS_VEC_F32, CLASS_VEC_BF16], CLASS_VEC_F16).astype(np.int64)
-        if self.mixed and len(np.unique(cls)) > 1:
-            # one launch over every target dtype (reshard_fused_mixed): the
-            # read-heavy 2-B-target weight tiles interleave with the f32
-            # moment tiles in table order
-            cls = np.full(len(runs), CLASS_GENERAL, dtype=np.int64)
+        # phase-mismatched cells: the scalar fused path (reshard_fused_scalar)
+        cls = np.where((runs["flags"] & RUN_VEC) != 0, cls, CLASS_GENERAL).astype(np.int64)
         return classed(runs, aux, cls, tile_bytes, extra)
 
 
@@ -772,7 +765,7 @@ def compile_fused(fx: XRunTable, rest_conv: RunTable, rest_load: RunTable, p: Pa
         if op == OP_CHECKZERO:
             extra_conv.append(i)
             continue
-        if op != OP_COPY or not (flags & RUN_VEC) or ns > MAX_SRC:
+        if op != OP_COPY or ns > MAX_SRC:
             ok = False
             break
         srcs = [s0] + conv._aux[aux:aux + ns - 1]
@@ -787,7 +780,7 @@ def compile_fused(fx: XRunTable, rest_conv: RunTable, rest_load: RunTable, p: Pa
             if op == OP_ZERO:
                 extra_load.append(i)
                 continue
-            if op != OP_COPY or not (flags & RUN_VEC) or nd > MAX_DST:
+            if op != OP_COPY or nd > MAX_DST:
                 ok = False
                 break
             dsts = [d0] + load._aux[aux + ns - 1:aux + ns - 1 + nd - 1]
@@ -811,10 +804,13 @@ def compile_fused(fx: XRunTable, rest_conv: RunTable, rest_load: RunTable, p: Pa
                 atom = atom_off + 4 * (r0 * W + c0)
                 ph = {(x // 4) % 4 for x in srcs} | {(atom // 4) % 4} | {(x // esz) % 4 for x in dsts}
                 pit = r1 - r0 == 1 or (aep % 4 == 0 and bep % 4 == 0 and W % 4 == 0)
-                if len(ph) != 1 or not pit or any(x % 4 for x in srcs) or any(x % esz for x in dsts):
+                if any(x % 4 for x in srcs) or any(x % esz for x in dsts):
                     ok = False
                     break
-                cells.append((srcs, atom, dsts, aep, bep, r1 - r0, c1 - c0, ai))
+                # cells whose pieces do not share one 16-B phase (e.g. ZeRO
+                # partitions of dp = 3) take the scalar fused path
+                cells.append((srcs, atom, dsts, aep, bep, r1 - r0, c1 - c0, ai,
+                              len(ph) == 1 and pit))
             if not ok:
                 break
         if ok and sum(c[5] * c[6] for c in cells) != n:
@@ -825,10 +821,10 @@ def compile_fused(fx: XRunTable, rest_conv: RunTable, rest_load: RunTable, p: Pa
         return False
     cmap, lmap = {}, {}
     tag = fx.unit(p.name, frags[0][0].kind)
-    for srcs, atom, dsts, sp, dp, rows, cols, ci in cells:
+    for srcs, atom, dsts, sp, dp, rows, cols, ci, vec in cells:
         fx.add(srcs=srcs, atom=atom if materialize else NO_ATOM, dsts=dsts, src_pitch=sp,
                atom_pitch=W, dst_pitch=dp, rows=rows, cols=cols, dtype=dtype, tag=tag,
-               labels=conv.units[0].labels.get(ci) if conv.units else None)
+               labels=conv.units[0].labels.get(ci) if conv.units else None, vec=vec)
     for i in extra_conv:
         _absorb_row(rest_conv, conv, i, cmap)
     for i in extra_load:

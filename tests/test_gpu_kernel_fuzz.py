@@ -7,8 +7,8 @@ CPU). Every destination byte must agree, and so must the failure report.
 This exercises what the golden cells reach only partly: ROWSPLIT and
 row-block tiles of every size, the per-CTA tile derivation over many runs
 (ABI v2), scalar heads/tails at every phase, phase-mismatched runs on the
-general kernel, MEAN/NOISE/ZERO/CHECKZERO, and the fused kernel with and
-without the atomic write."""
+general kernel, MEAN/NOISE/ZERO/CHECKZERO, and the fused kernels (vector
+and phase-mismatched scalar cells) with and without the atomic write."""
 
 import numpy as np
 import pytest
@@ -138,7 +138,6 @@ def test_move_kernels_match_interpreter(seed):
 def test_fused_kernel_matches_interpreter(seed):
     rng = np.random.default_rng(2000 + seed)
     fx = XRunTable()
-    fx.mixed = bool(seed % 2)  # odd seeds: one mixed-dtype launch (reshard_fused_mixed)
     fx.unit("fuzz", "weight")
     src_a, atom_a, dst_a = _Arena(), _Arena(), _Arena()
     fills = []
@@ -148,22 +147,24 @@ def test_fused_kernel_matches_interpreter(seed):
         rows = int(rng.choice([1, 2, 5, 33]))
         cols = int(rng.choice([1, 4, 7, 512, 777, 4096, 30001]))
         phase = int(rng.integers(0, 4))
-        pad = lambda: int(rng.integers(0, 3)) * 4  # noqa: E731 - pitches keep the phase
+        vec = seed % 2 == 0 or rng.random() < 0.3  # odd seeds: mostly phase-mismatched cells
+        pad = lambda: int(rng.integers(0, 3)) * 4 if vec else int(rng.integers(0, 9))  # noqa: E731
         sp, ap, dp = cols + pad(), cols + pad(), cols + pad()
         if rows == 1:
             sp = ap = dp = cols
+        ph = (lambda: phase) if vec else (lambda: int(rng.integers(0, 4)))  # noqa: E731
         K = int(rng.integers(1, 5))
         vals = _random_bits(rng, rows * cols, finite=False).reshape(rows, cols)
         srcs = []
         for _k in range(K):
-            at = src_a.take(4 * _region(rows, cols, sp), phase, 4)
+            at = src_a.take(4 * _region(rows, cols, sp), ph(), 4)
             srcs.append(at)
             fills.append((at, rows, cols, sp, vals))
-        atom = atom_a.take(4 * _region(rows, cols, ap), phase, 4) if rng.random() < 0.8 else NO_ATOM
-        dsts = [dst_a.take(esz * _region(rows, cols, dp), phase, esz)
+        atom = atom_a.take(4 * _region(rows, cols, ap), ph(), 4) if rng.random() < 0.8 else NO_ATOM
+        dsts = [dst_a.take(esz * _region(rows, cols, dp), ph(), esz)
                 for _d in range(int(rng.integers(0, 4)))]
         fx.add(srcs=srcs, atom=atom, dsts=dsts, src_pitch=sp, atom_pitch=ap, dst_pitch=dp,
-               rows=rows, cols=cols, dtype=dtype, tag=0)
+               rows=rows, cols=cols, dtype=dtype, tag=0, vec=vec)
     src = np.zeros(max(src_a.top, 16), dtype=np.uint8)
     for at, rows, cols, sp, vals in fills:
         _fill(src, at, rows, cols, sp, vals)
