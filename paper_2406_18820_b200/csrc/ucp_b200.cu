@@ -1105,17 +1105,125 @@ __device__ __forceinline__ void fused_tile_scalar(const uint64_t* __restrict__ a
   }
 }
 
-// The GENERAL class of fused tables: phase-mismatched cells, scalar path;
-// each CTA dispatches on its run's target dtype.
+#ifndef UCP_STAGED
+#define UCP_STAGED 1  // phase-mismatched fused cells through shared memory (0: scalar path)
+#endif
+
+// Phase-mismatched fused cells at vector width: each warp stages its row
+// segment through shared memory. Every source replica is read with aligned
+// 16-B loads on its own phase grid into a warp-private buffer; replicas are
+// compared element-wise from shared memory; the atomic and every target are
+// written with aligned 16-B (8-B for 16-bit targets) stores on their own
+// phase grids, reading four shifted elements from shared memory -- the
+// "shared-memory staging" the strided pieces need, with no register
+// pressure added to the aligned kernels.
+constexpr int kStage = kSeg + 8;  // floats per warp buffer: 512 + up to 3 + 3 slop
+
+__device__ __forceinline__ int stage_in(float* buf, const char* p, uint32_t len, uint32_t lane) {
+  // p: address of element 0 (4-B aligned). Returns off: element j sits at buf[j + off].
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const int off = (int)((a >> 2) & 3);
+  const float4* v0 = reinterpret_cast<const float4*>(a - 4 * off);
+  const uint32_t nv = (off + len + 3) >> 2;
+  for (uint32_t i = lane; i < nv; i += 32) {
+    const float4 x = ld_stream4(v0 + i);
+    reinterpret_cast<float4*>(buf)[i] = x;
+  }
+  return off;
+}
+
+template <int DT>
+__device__ __forceinline__ void stage_out(char* p, const float* buf, int off, uint32_t len,
+                                          uint32_t lane) {
+  // p: address of element 0 of the destination (ESZ-aligned)
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t ph = (uint32_t)((a / ESZ) & 3);
+  uint32_t head = (4u - ph) & 3u;
+  if (head > len) head = len;
+  const uint32_t nvec = (len - head) >> 2;
+  const uint32_t tail = len - head - 4 * nvec;
+  for (uint32_t i = lane; i < nvec; i += 32) {
+    const uint32_t j = head + 4 * i + off;
+    const float4 x = make_float4(buf[j], buf[j + 1], buf[j + 2], buf[j + 3]);
+    store4<DT>(p + (uint64_t)ESZ * (head + 4 * i), x);
+  }
+  if (lane < head + tail) {
+    const uint32_t e = lane < head ? lane : head + 4 * nvec + (lane - head);
+    store1<DT>(p + (uint64_t)ESZ * e, buf[e + off]);
+  }
+}
+
+template <int DT>
+__device__ __noinline__ void fused_tile_staged(const uint64_t* __restrict__ aux,
+                                                  const ucp_tile& tile, const ucp_xrun& s_run,
+                                                  uint64_t* s_aux, const char* __restrict__ sb,
+                                                  char* __restrict__ ab, char* __restrict__ db,
+                                                  ucp_status* st, float* sbuf) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  const int ns = s_run.n_src, nd = s_run.n_dst;
+  const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
+  if (n_aux > 0) {
+    for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
+    __syncthreads();
+  }
+  uint32_t nrows, nc;
+  if (s_run.flags & UCP_RUN_ROWSPLIT) { nrows = 1; nc = tile.count; }
+  else { nrows = tile.count; nc = s_run.cols; }
+  const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nrows * spr;
+  const uint64_t s0 = s_run.src, a0 = s_run.atom, d0 = s_run.dst;
+  const bool atom_on = a0 != ~0ull;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* buf = sbuf + warp * 2 * kStage;  // primary | replica
+  float* rep = buf + kStage;
+  for (uint32_t it = warp; it < n_items; it += kWarps) {
+    const uint32_t rr = it / spr;
+    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
+    const uint32_t row = tile.row0 + rr;
+    const uint64_t srow = (uint64_t)row * s_run.src_pitch + cs;
+    const uint64_t arow = (uint64_t)row * s_run.atom_pitch + cs;
+    const uint64_t drow = (uint64_t)row * s_run.dst_pitch + cs;
+    bool bad = false;
+    uint32_t bad_e = 0xffffffffu;
+    __syncwarp();  // the previous segment's readers are done with buf
+    const int off = stage_in(buf, sb + s0 + 4 * srow, len, lane);
+    for (int k = 1; k < ns; ++k) {
+      const int offk = stage_in(rep, sb + s_aux[k - 1] + 4 * srow, len, lane);
+      __syncwarp();
+      for (uint32_t e = lane; e < len; e += 32)
+        if (bits_of(rep[e + offk]) != bits_of(buf[e + off])) { bad = true; bad_e = min(bad_e, e); }
+      __syncwarp();  // rep is refilled by the next replica
+    }
+    __syncwarp();
+    if (atom_on) stage_out<UCP_DT_F32>(ab + a0 + 4 * arow, buf, off, len, lane);
+    for (int d = 0; d < nd; ++d)
+      stage_out<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + (uint64_t)ESZ * drow, buf, off,
+                    len, lane);
+    report(bad, row * s_run.cols + cs + bad_e, tile.run, st);
+  }
+}
+
+// The GENERAL class of fused tables: phase-mismatched cells; each CTA
+// dispatches on its run's target dtype.
 __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_scalar(UCP_FUSED_ARGS) {
   (void)n_tiles;
   __shared__ __align__(16) ucp_xrun s_run;
   __shared__ uint4 s_t;
   __shared__ uint64_t s_aux[kMaxAux];
+#if UCP_STAGED
+  __shared__ __align__(16) float s_stage[kWarps * 2 * kStage];
+#endif
   const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
+#if UCP_STAGED
+  if (s_run.dtype == UCP_DT_F32) fused_tile_staged<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage);
+  else if (s_run.dtype == UCP_DT_BF16) fused_tile_staged<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage);
+  else fused_tile_staged<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage);
+#else
   if (s_run.dtype == UCP_DT_F32) fused_tile_scalar<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st);
   else if (s_run.dtype == UCP_DT_BF16) fused_tile_scalar<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st);
   else fused_tile_scalar<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st);
+#endif
 }
 
 // ---------------------------------------------------------------- entry kernels
