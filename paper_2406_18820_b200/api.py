@@ -44,6 +44,7 @@ from .spec import (
     ParamSpec,
     RecordMeta,
     Tensor,
+    format_config_string,
     make_tensor,
     spec_to_json,
 )
@@ -251,6 +252,7 @@ class _PerThread(threading.local):
     def __init__(self):
         self.stage = _Staging()
         self.status: dict = {}
+        self.plans: dict = {}  # reshard(): the last compiled ReshardPlan
 
 
 _LOCAL = _PerThread()
@@ -272,9 +274,10 @@ def _status(dev) -> Status:
 
 
 def release_staging() -> None:
-    """Drop this thread's pinned / device staging buffers (they are
-    grow-only and reused across calls otherwise)."""
+    """Drop this thread's pinned / device staging buffers and its cached
+    reshard() plan (they are grow-only and reused across calls otherwise)."""
     _LOCAL.stage = _Staging()
+    _LOCAL.plans = {}
 
 
 def _run(prog: Program, gather: bool, src_base: int, dst_base: int, dev) -> None:
@@ -1179,7 +1182,16 @@ def reshard(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: d
     if any(_is_cuda(t) for v in shards.values() for t in v):
         # fragments already in HBM: zero-copy device-to-device reshard
         return reshard_device(spec, src, tgt, shards, dtype=dtype, strict=strict)
-    plan = ReshardPlan(spec, src, tgt, dtype=dtype, strict=strict, device=device, fused=fused)
+    dev = require_device(device)
+    key = (spec_to_json(spec), format_config_string(src), getattr(src, "vocab_multiple", 1),
+           format_config_string(tgt), getattr(tgt, "vocab_multiple", 1), dtype.name, strict,
+           fused, str(dev))
+    cache = _LOCAL.plans  # per thread: a plan's streams and device slots are not shared
+    plan = cache.get(key)
+    if plan is None:
+        plan = ReshardPlan(spec, src, tgt, dtype=dtype, strict=strict, device=dev, fused=fused)
+        cache.clear()  # keep one compiled plan (its device slots) per thread
+        cache[key] = plan
     return plan.run_host(shards)
 
 
