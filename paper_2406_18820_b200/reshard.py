@@ -23,6 +23,7 @@ Modes:
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -39,7 +40,7 @@ from .plan import (
     fragment_elems,
     fragment_shape,
 )
-from .spec import STATE_KINDS, DType, ModelSpec, ParallelConfig
+from .spec import STATE_KINDS, DType, ModelSpec, ParallelConfig, format_config_string
 from .synth import stream_base
 
 
@@ -625,6 +626,68 @@ class ReshardPlan:
 _TORCH_OF = {DType.F32: torch.float32, DType.BF16: torch.bfloat16, DType.F16: torch.float16}
 
 
+_SRC_V, _TGT_V = 1 << 56, 1 << 57  # virtual address spaces of a cached d2d template
+_D2D = threading.local()
+
+
+class _D2DTemplate:
+    """The compiled tables of one device-to-device reshard layout, built on
+    virtual addresses (source fragment (g, i) at _SRC_V + offset, target
+    fragment at _TGT_V + offset, 256-B aligned). Each call patches the
+    caller's and the outputs' real addresses into host copies of the run /
+    aux tables (vectorised) and uploads them; the tile scan and the classing
+    stay. Valid for calls whose source pointers have the template's 16-B
+    phase (fresh torch allocations always do)."""
+
+    def __init__(self, spec, src, tgt, dtype, strict, device, window_bytes, tile_bytes,
+                 src_addr, tgt_addr):
+        frags, targets = {}, {}
+        for (g, i), (m, a, n) in src_addr.items():
+            frags.setdefault((m.param, m.kind), []).append((m, a, n))
+        for (g, i), (m, a) in tgt_addr.items():
+            targets.setdefault((m.param, m.kind), []).append((m, a))
+        wins = make_windows(spec.params, window_bytes)
+        self.scratch = torch.empty(max(max(sum(3 * align_up(4 * p.numel) for p in W.params)
+                                           for W in wins), 256), dtype=torch.uint8, device=device)
+        self.progs = []
+        for W in wins:
+            fx, rc, rl = XRunTable(), RunTable(), RunTable()
+            at = self.scratch.data_ptr()
+            for p in W.params:
+                for k in STATE_KINDS:
+                    dt = dtype if k == "weight" else DType.F32
+                    compile_fused(fx, rc, rl, p, src, frags.get((p.name, k), []), at, tgt,
+                                  targets.get((p.name, k), []), dt, strict, False)
+                    at += align_up(4 * p.numel)
+            progs = (XProgram(fx, device, tile_bytes), Program(rc, device, tile_bytes),
+                     Program(rl, device, tile_bytes))
+            for prog in progs:
+                prog.virt = (prog.runs_host.copy(), prog.aux_host.copy())
+            self.progs.append(progs)
+
+    def patch(self, starts: np.ndarray, real: np.ndarray) -> None:
+        """Rebind every virtual address to real[k] + (v - starts[k])."""
+        def rebind(v: np.ndarray) -> np.ndarray:
+            v = v.astype(np.uint64, copy=True)
+            mask = v >= np.uint64(_SRC_V)
+            if mask.any():
+                k = np.searchsorted(starts, v[mask], side="right") - 1
+                v[mask] = real[k] + (v[mask] - starts[k])
+            return v
+
+        for progs in self.progs:
+            for prog in progs:
+                runs0, aux0 = prog.virt
+                runs = runs0.copy()
+                for f in ("src", "dst"):
+                    runs[f] = rebind(runs0[f])
+                aux = rebind(aux0)
+                prog.runs_host, prog.aux_host = runs, aux
+                if len(runs):
+                    prog._runs.copy_(torch.from_numpy(np.ascontiguousarray(runs).view(np.uint8)))
+                prog._aux.copy_(torch.from_numpy(np.ascontiguousarray(aux).view(np.uint8)))
+
+
 def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: dict,
                    dtype: DType = DType.F32, strict: bool = True, *,
                    window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17) -> dict:
@@ -639,60 +702,81 @@ def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, sh
     one fused launch per window reads each source replica once, checks it
     and writes every target replica. The atomic tensor is not materialised;
     only units that cannot fuse (Partial mean / noise) go through a window
-    scratch buffer. Raises the reference's exceptions
-    (ReplicateMismatchError, PaddingError, ShapeError, ...)."""
+    scratch buffer. The compiled tables are cached per thread and layout and
+    re-bound to each call's addresses (``_D2DTemplate``). Raises the
+    reference's exceptions (ReplicateMismatchError, PaddingError,
+    ShapeError, ...)."""
     from ._errors import ShapeError
     from .engine import describe_failure
+    from .spec import spec_to_json
 
     validate_model_config(spec, src)
     validate_model_config(spec, tgt)
     src_recs, tgt_recs = all_rank_records(spec, src), all_rank_records(spec, tgt)
     first = next((t for v in shards.values() for t in v), None)
     device = require_device(first.device if isinstance(first, torch.Tensor) else None)
-    frags: dict = {}
+    src_real, src_virt, vat = {}, {}, _SRC_V
     for g in range(src.world_size):
         got = shards.get(g, [])
         if len(got) != len(src_recs[g]):
             raise ShapeError(f"rank {g}: {len(got)} fragments, want {len(src_recs[g])}")
-        for m, t in zip(src_recs[g], got):
+        for i, (m, t) in enumerate(zip(src_recs[g], got)):
             n = fragment_elems(spec.param(m.param), src, m)
             if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
                     and t.is_contiguous() and t.numel() == n and t.device == device):
                 raise ShapeError(f"rank {g} {m.param}.{m.kind}: want a contiguous float32 CUDA "
                                  f"tensor of {n} elements on {device}")
-            frags.setdefault((m.param, m.kind), []).append((m, t.data_ptr(), n))
+            src_real[(g, i)] = (m, t.data_ptr(), n)
+            src_virt[(g, i)] = (m, vat, n)
+            vat += align_up(4 * max(n, 1))
     out: dict = {g: [] for g in range(tgt.world_size)}
-    targets: dict = {}
+    tgt_real, tgt_virt, vat = {}, {}, _TGT_V
     for g in range(tgt.world_size):
-        for m in tgt_recs[g]:
+        for i, m in enumerate(tgt_recs[g]):
             p = spec.param(m.param)
             dt = dtype if m.kind == "weight" else DType.F32
             t = torch.empty(fragment_shape(p, tgt, m), dtype=_TORCH_OF[dt], device=device)
             out[g].append(t)
-            targets.setdefault((m.param, m.kind), []).append((m, t.data_ptr()))
+            tgt_real[(g, i)] = (m, t.data_ptr())
+            tgt_virt[(g, i)] = (m, vat)
+            vat += align_up(max(t.numel(), 1) * t.element_size())
+    # a cached template holds when every source keeps the virtual 16-B phase
+    phase_ok = (all((src_real[k][1] - src_virt[k][1]) % 16 == 0 for k in src_real)
+                and all((tgt_real[k][1] - tgt_virt[k][1]) % 16 == 0 for k in tgt_real))
+    key = (spec_to_json(spec), format_config_string(src), getattr(src, "vocab_multiple", 1),
+           format_config_string(tgt), getattr(tgt, "vocab_multiple", 1), dtype.name, strict,
+           window_bytes, tile_bytes, str(device))
+    cache = getattr(_D2D, "cache", None)
+    if cache is None:
+        cache = _D2D.cache = {}
+    tpl = cache.get(key) if phase_ok else None
+    if tpl is None:
+        if phase_ok:
+            tpl = _D2DTemplate(spec, src, tgt, dtype, strict, device, window_bytes, tile_bytes,
+                               src_virt, tgt_virt)
+            cache.clear()  # one template (and its scratch) per thread
+            cache[key] = tpl
+        else:  # odd source alignment: compile on the real addresses, uncached
+            tpl = _D2DTemplate(spec, src, tgt, dtype, strict, device, window_bytes, tile_bytes,
+                               src_real, tgt_real)
+    if phase_ok:
+        keys = sorted(src_virt, key=lambda k: src_virt[k][1])
+        tkeys = sorted(tgt_virt, key=lambda k: tgt_virt[k][1])
+        starts = np.array([src_virt[k][1] for k in keys] + [tgt_virt[k][1] for k in tkeys],
+                          dtype=np.uint64)
+        real = np.array([src_real[k][1] for k in keys] + [tgt_real[k][1] for k in tkeys],
+                        dtype=np.uint64)
+        tpl.patch(starts, real)
     status = Status(device)
     status.reset()
     stream = torch.cuda.current_stream(device)
-    wins = make_windows(spec.params, window_bytes)
-    scratch = torch.empty(max(max(sum(3 * align_up(4 * p.numel) for p in W.params)
-                                  for W in wins), 256), dtype=torch.uint8, device=device)
     launched = []
-    for W in wins:
-        fx, rc, rl = XRunTable(), RunTable(), RunTable()
-        at = scratch.data_ptr()
-        for p in W.params:
-            for k in STATE_KINDS:
-                dt = dtype if k == "weight" else DType.F32
-                compile_fused(fx, rc, rl, p, src, frags.get((p.name, k), []), at, tgt,
-                              targets.get((p.name, k), []), dt, strict, False)
-                at += align_up(4 * p.numel)
-        progs = (XProgram(fx, device, tile_bytes), Program(rc, device, tile_bytes),
-                 Program(rl, device, tile_bytes))
+    for progs in tpl.progs:
         progs[0].launch(0, 0, 0, status, stream)
         progs[1].launch(True, 0, 0, status, stream)
         progs[2].launch(False, 0, 0, status, stream)
         launched.append(progs)
-        if len(wins) > 1:
+        if len(tpl.progs) > 1:
             # the next window reuses the scratch: keep failures attributable
             torch.cuda.synchronize(device)
             if status.read()[0] != (1 << 64) - 1:

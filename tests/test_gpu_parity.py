@@ -734,3 +734,30 @@ def test_reshard_device_errors():
     dev[3][i] = dev[3][i][:-1].clone()
     with pytest.raises(U.ShapeError):
         U.reshard(spec, src_cfg, tgt_cfg, dev)
+
+
+def test_reshard_device_template_rebinding(golden):
+    """The cached device-to-device template is re-bound to each call's
+    addresses: repeated calls with fresh source tensors (and a deliberately
+    misaligned one, which compiles uncached) all give the golden world."""
+    import sys
+
+    R = sys.modules["paper_2406_18820_b200.reshard"]
+    row = next(r for r in golden["pipelines"] if r["name"] == "gqa")
+    spec = cell_spec(golden, row)
+    src_cfg, tgt_cfg = cell_cfgs(row)
+    shards = O.partition_mem(spec, O.init_state(spec, 7), src_cfg)
+    recs = {g: U.enumerate_rank_records(spec, tgt_cfg, g) for g in range(tgt_cfg.world_size)}
+    for trial in range(3):
+        dev = {g: [torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).cuda() for _, a in v]
+               for g, v in shards.items()}
+        if trial == 2:  # a 4-B-offset view: phase differs from the template
+            t = dev[0][0]
+            big = torch.empty(t.numel() + 1, dtype=torch.float32, device="cuda")
+            big[1:].copy_(t)
+            dev[0][0] = big[1:]
+        out = U.reshard(spec, src_cfg, tgt_cfg, dev)
+        wd = {g: list(zip(recs[g], [_host_bits(t) for t in out[g]])) for g in out}
+        assert O.world_digest(wd) == row["world_F32"], trial
+        if trial < 2:
+            assert len(R._D2D.cache) == 1
