@@ -770,20 +770,15 @@ def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, sh
     status = Status(device)
     status.reset()
     stream = torch.cuda.current_stream(device)
-    launched = []
+    # stream-ordered: windows reuse the scratch in order; a failure anywhere
+    # is localised afterwards by re-running the source-reading launches
     for progs in tpl.progs:
         progs[0].launch(0, 0, 0, status, stream)
         progs[1].launch(True, 0, 0, status, stream)
         progs[2].launch(False, 0, 0, status, stream)
-        launched.append(progs)
-        if len(tpl.progs) > 1:
-            # the next window reuses the scratch: keep failures attributable
-            torch.cuda.synchronize(device)
-            if status.read()[0] != (1 << 64) - 1:
-                break
     torch.cuda.synchronize(device)
     if status.read()[0] != (1 << 64) - 1:
-        for fused, conv, _ in launched:  # localise: re-run the source-reading launches
+        for fused, conv, _ in tpl.progs:  # localise: re-run the source-reading launches
             for prog in (fused, conv):
                 status.reset()
                 if prog is fused:
