@@ -630,6 +630,18 @@ _SRC_V, _TGT_V = 1 << 56, 1 << 57  # virtual address spaces of a cached d2d temp
 _D2D = threading.local()
 
 
+def _rebind(v: np.ndarray, starts: np.ndarray, real: np.ndarray) -> np.ndarray:
+    """Map virtual addresses (>= _SRC_V) inside fragment k, which starts at
+    starts[k] (sorted), to real[k] + offset; other values (real scratch
+    addresses, zeros) pass through."""
+    v = v.astype(np.uint64, copy=True)
+    mask = v >= np.uint64(_SRC_V)
+    if mask.any():
+        k = np.searchsorted(starts, v[mask], side="right") - 1
+        v[mask] = real[k] + (v[mask] - starts[k])
+    return v
+
+
 class _D2DTemplate:
     """The compiled tables of one device-to-device reshard layout, built on
     virtual addresses (source fragment (g, i) at _SRC_V + offset, target
@@ -668,12 +680,7 @@ class _D2DTemplate:
     def patch(self, starts: np.ndarray, real: np.ndarray) -> None:
         """Rebind every virtual address to real[k] + (v - starts[k])."""
         def rebind(v: np.ndarray) -> np.ndarray:
-            v = v.astype(np.uint64, copy=True)
-            mask = v >= np.uint64(_SRC_V)
-            if mask.any():
-                k = np.searchsorted(starts, v[mask], side="right") - 1
-                v[mask] = real[k] + (v[mask] - starts[k])
-            return v
+            return _rebind(v, starts, real)
 
         for progs in self.progs:
             for prog in progs:

@@ -160,3 +160,25 @@ def test_public_names_are_the_api_functions():
                  "init_state", "ucp_info", "cast", "load_atomic", "consolidate_world"):
         assert inspect.isfunction(getattr(U, name)), name
     assert inspect.isclass(U.ReshardPlan)
+
+
+def test_d2d_template_rebind():
+    """reshard_device's template patch: virtual source / target addresses
+    map to the caller's real ones with offsets kept; real scratch addresses
+    and zeros are untouched."""
+    import sys
+
+    import numpy as np
+
+    R = sys.modules["paper_2406_18820_b200.reshard"]
+    S, T = R._SRC_V, R._TGT_V
+    starts = np.array([S, S + 256, S + 1024, T, T + 512], dtype=np.uint64)
+    real = np.array([0x7000_0000, 0x7100_0100, 0x7200_0000, 0x7300_0000, 0x7400_0000],
+                    dtype=np.uint64)
+    v = np.array([S, S + 4, S + 256 + 12, S + 1024 + 1000, T + 8, T + 512 + 4, 0, 0x7f00_0000],
+                 dtype=np.uint64)
+    got = R._rebind(v, starts, real)
+    want = [0x7000_0000, 0x7000_0004, 0x7100_010C, 0x7200_03E8, 0x7300_0008, 0x7400_0004, 0,
+            0x7f00_0000]
+    assert [int(x) for x in got] == want
+    assert [int(x) for x in v][:1] == [S]  # input untouched
