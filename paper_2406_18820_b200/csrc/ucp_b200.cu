@@ -712,10 +712,98 @@ __device__ __forceinline__ void vec_body(const ucp_run* __restrict__ runs,
   }
 }
 
+#ifndef UCP_STAGED
+#define UCP_STAGED 1  // phase-mismatched fused cells through shared memory (0: scalar path)
+#endif
+
+// Phase-mismatched fused cells at vector width: each warp stages its row
+// segment through shared memory. Every source replica is read with aligned
+// 16-B loads on its own phase grid into a warp-private buffer; replicas are
+// compared element-wise from shared memory; the atomic and every target are
+// written with aligned 16-B (8-B for 16-bit targets) stores on their own
+// phase grids, reading four shifted elements from shared memory -- the
+// "shared-memory staging" the strided pieces need, with no register
+// pressure added to the aligned kernels.
+constexpr int kStage = kSeg + 8;  // floats per warp buffer: 512 + up to 3 + 3 slop
+
+__device__ __forceinline__ int stage_in(float* buf, const char* p, uint32_t len, uint32_t lane) {
+  // p: address of element 0 (4-B aligned). Returns off: element j sits at buf[j + off].
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const int off = (int)((a >> 2) & 3);
+  const float4* v0 = reinterpret_cast<const float4*>(a - 4 * off);
+  const uint32_t nv = (off + len + 3) >> 2;
+  for (uint32_t i = lane; i < nv; i += 32) {
+    const float4 x = ld_stream4(v0 + i);
+    reinterpret_cast<float4*>(buf)[i] = x;
+  }
+  return off;
+}
+
+template <int DT>
+__device__ __forceinline__ void stage_out(char* p, const float* buf, int off, uint32_t len,
+                                          uint32_t lane) {
+  // p: address of element 0 of the destination (ESZ-aligned)
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t ph = (uint32_t)((a / ESZ) & 3);
+  uint32_t head = (4u - ph) & 3u;
+  if (head > len) head = len;
+  const uint32_t nvec = (len - head) >> 2;
+  const uint32_t tail = len - head - 4 * nvec;
+  for (uint32_t i = lane; i < nvec; i += 32) {
+    const uint32_t j = head + 4 * i + off;
+    const float4 x = make_float4(buf[j], buf[j + 1], buf[j + 2], buf[j + 3]);
+    store4<DT>(p + (uint64_t)ESZ * (head + 4 * i), x);
+  }
+  if (lane < head + tail) {
+    const uint32_t e = lane < head ? lane : head + 4 * nvec + (lane - head);
+    store1<DT>(p + (uint64_t)ESZ * e, buf[e + off]);
+  }
+}
+
 // ---------------------------------------------------------------- general kernel
 //
 // Everything else: MEAN / NOISE / ZERO / CHECKZERO runs and phase-mismatched
 // runs (scalar path). Tiny by bytes (Partial vectors, pads, dp=3 cells).
+
+// Phase-mismatched COPY runs of the unfused path, staged through shared
+// memory like the fused cells (fused_tile_staged): aligned 16-B loads on
+// each replica's phase grid, aligned stores on each destination's.
+template <int DT>
+__device__ __noinline__ void move_tile_staged(const TileGeom& g, const ucp_run& r,
+                                              const uint64_t* s_aux, const char* __restrict__ sb,
+                                              char* __restrict__ db, uint32_t run_idx,
+                                              ucp_status* st, float* sbuf) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  const int ns = r.n_src, nd = r.n_dst;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* buf = sbuf + warp * 2 * kStage;
+  float* rep = buf + kStage;
+  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
+    const uint32_t rr = it / g.spr;
+    const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, g.col0 + g.nc) - cs;
+    const uint32_t row = g.row0 + rr;
+    const uint64_t srow = (uint64_t)row * r.src_pitch + cs;
+    const uint64_t drow = (uint64_t)row * r.dst_pitch + cs;
+    bool bad = false;
+    uint32_t bad_e = 0xffffffffu;
+    __syncwarp();
+    const int off = stage_in(buf, sb + r.src + 4 * srow, len, lane);
+    for (int k = 1; k < ns; ++k) {
+      const int offk = stage_in(rep, sb + s_aux[k - 1] + 4 * srow, len, lane);
+      __syncwarp();
+      for (uint32_t e = lane; e < len; e += 32)
+        if (bits_of(rep[e + offk]) != bits_of(buf[e + off])) { bad = true; bad_e = min(bad_e, e); }
+      __syncwarp();
+    }
+    __syncwarp();
+    for (int d = 0; d < nd; ++d)
+      stage_out<DT>(db + (d == 0 ? r.dst : s_aux[ns - 1 + d - 1]) + (uint64_t)ESZ * drow, buf, off,
+                    len, lane);
+    report(bad, row * r.cols + cs + bad_e, run_idx, st);
+  }
+}
 
 __device__ __forceinline__ void general_body(const ucp_run* __restrict__ runs,
                                              const uint64_t* __restrict__ aux,
@@ -727,6 +815,16 @@ __device__ __forceinline__ void general_body(const ucp_run* __restrict__ runs,
   __shared__ uint64_t s_aux[kMaxAux];
   const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
   const TileGeom g = tile_prologue(aux, tile, s_run, s_aux);
+#if UCP_STAGED
+  __shared__ __align__(16) float s_stage[kWarps * 2 * kStage];
+  if (s_run.op == UCP_OP_COPY && !(s_run.flags & UCP_RUN_VEC) && s_run.n_src >= 1 &&
+      s_run.n_src + s_run.n_dst - 2 < kMaxAux) {
+    if (s_run.dtype == UCP_DT_F32) move_tile_staged<UCP_DT_F32>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
+    else if (s_run.dtype == UCP_DT_BF16) move_tile_staged<UCP_DT_BF16>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
+    else move_tile_staged<UCP_DT_F16>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
+    return;
+  }
+#endif
   const Ctx c{&s_run, s_aux, sb, db, tile.run};
   const uint32_t warp = threadIdx.x >> 5;
   for (uint32_t it = warp; it < g.n_items; it += kWarps) {
@@ -1102,55 +1200,6 @@ __device__ __forceinline__ void fused_tile_scalar(const uint64_t* __restrict__ a
       }
     }
     report(bad, row * s_run.cols + cs + bad_e, tile.run, st);
-  }
-}
-
-#ifndef UCP_STAGED
-#define UCP_STAGED 1  // phase-mismatched fused cells through shared memory (0: scalar path)
-#endif
-
-// Phase-mismatched fused cells at vector width: each warp stages its row
-// segment through shared memory. Every source replica is read with aligned
-// 16-B loads on its own phase grid into a warp-private buffer; replicas are
-// compared element-wise from shared memory; the atomic and every target are
-// written with aligned 16-B (8-B for 16-bit targets) stores on their own
-// phase grids, reading four shifted elements from shared memory -- the
-// "shared-memory staging" the strided pieces need, with no register
-// pressure added to the aligned kernels.
-constexpr int kStage = kSeg + 8;  // floats per warp buffer: 512 + up to 3 + 3 slop
-
-__device__ __forceinline__ int stage_in(float* buf, const char* p, uint32_t len, uint32_t lane) {
-  // p: address of element 0 (4-B aligned). Returns off: element j sits at buf[j + off].
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const int off = (int)((a >> 2) & 3);
-  const float4* v0 = reinterpret_cast<const float4*>(a - 4 * off);
-  const uint32_t nv = (off + len + 3) >> 2;
-  for (uint32_t i = lane; i < nv; i += 32) {
-    const float4 x = ld_stream4(v0 + i);
-    reinterpret_cast<float4*>(buf)[i] = x;
-  }
-  return off;
-}
-
-template <int DT>
-__device__ __forceinline__ void stage_out(char* p, const float* buf, int off, uint32_t len,
-                                          uint32_t lane) {
-  // p: address of element 0 of the destination (ESZ-aligned)
-  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const uint32_t ph = (uint32_t)((a / ESZ) & 3);
-  uint32_t head = (4u - ph) & 3u;
-  if (head > len) head = len;
-  const uint32_t nvec = (len - head) >> 2;
-  const uint32_t tail = len - head - 4 * nvec;
-  for (uint32_t i = lane; i < nvec; i += 32) {
-    const uint32_t j = head + 4 * i + off;
-    const float4 x = make_float4(buf[j], buf[j + 1], buf[j + 2], buf[j + 3]);
-    store4<DT>(p + (uint64_t)ESZ * (head + 4 * i), x);
-  }
-  if (lane < head + tail) {
-    const uint32_t e = lane < head ? lane : head + 4 * nvec + (lane - head);
-    store1<DT>(p + (uint64_t)ESZ * e, buf[e + off]);
   }
 }
 

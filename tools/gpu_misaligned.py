@@ -16,9 +16,10 @@ from paper_2406_18820_b200.plan import CLASS_GENERAL  # noqa: E402
 spec = U.llama_spec("7b", 4)
 tgt = U.ParallelConfig(dp=2, tp=4, zero_stage=U.ZeroStage.Z1)
 peak = 6536.4
+fused = "unfused" not in sys.argv[1:]
 for dp in (2, 3, 4, 5):
     src = U.ParallelConfig(dp=dp, tp=2, zero_stage=U.ZeroStage.Z1)
-    plan = ReshardPlan(spec, src, tgt, fused=True)
+    plan = ReshardPlan(spec, src, tgt, fused=fused)
     plan.synthesize(7)
     res = plan.verify(7)
     gen = sum(int(W.conv.class_info[CLASS_GENERAL]) + int(W.load.class_info[CLASS_GENERAL])
