@@ -1255,7 +1255,10 @@ __device__ __noinline__ void fused_tile_staged(const uint64_t* __restrict__ aux,
 
 // The GENERAL class of fused tables: phase-mismatched cells; each CTA
 // dispatches on its run's target dtype.
-__global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_scalar(UCP_FUSED_ARGS) {
+#ifndef UCP_SCALAR_MINB
+#define UCP_SCALAR_MINB 4  // CTAs per SM of the staged kernel (2 / 3 / 4 measured equal within 2 %)
+#endif
+__global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) reshard_fused_scalar(UCP_FUSED_ARGS) {
   (void)n_tiles;
   __shared__ __align__(16) ucp_xrun s_run;
   __shared__ uint4 s_t;
