@@ -150,6 +150,12 @@ typedef struct ucp_status {
 /* Version of this ABI (UCP_ABI_VERSION). */
 int ucp_version(void);
 
+/* Build provenance: "UCP_BUILD_ID:" + the first 32 hex digits of
+ * sha256(csrc/ucp_b200.cu || include/ucp_b200.h), baked in by the build
+ * (paper_2406_18820_b200/_build.py); the loader refuses a library whose id
+ * differs from the sources next to it. */
+const char* ucp_build_id(void);
+
 /* Reset a device status word to "no failure" (stream-ordered). */
 int ucp_status_reset(ucp_status* status, void* stream);
 

@@ -28,6 +28,8 @@ typedef struct ucp_comm_id {
 } ucp_comm_id;
 
 int ucp_comm_version(void);
+/* "UCP_BUILD_ID:" + sha256(csrc/ucp_comm.cpp || this header)[:32 hex] */
+const char* ucp_comm_build_id(void);
 int ucp_comm_unique_id(ucp_comm_id* out);
 int ucp_comm_init(int nranks, int rank, const ucp_comm_id* id, void** comm);
 int ucp_alltoallv(void* comm, const void* send, const uint64_t* send_counts, void* recv,

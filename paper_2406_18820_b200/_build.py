@@ -5,24 +5,34 @@
 Flags: -gencode arch=compute_100a,code=sm_100a, -O3, -lineinfo, and no fast
 math (the partial-noise and mean epilogues rely on IEEE f64/f32 with
 denormals; nvcc defaults keep -ftz=false -prec-div=true).
+
+Provenance: each library embeds ``UCP_BUILD_ID:<id>``, where id is the first
+32 hex digits of sha256 over its source and header. ``build()`` recompiles
+whenever the embedded id differs from the sources (not on mtime), and
+``_native.load_library`` refuses a library whose id does not match.
 """
 
 from __future__ import annotations
 
+import hashlib
 import os
+import re
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "ucp_b200.cu")
+HDR = os.path.join(ROOT, "include", "ucp_b200.h")
 OUT = os.path.join(HERE, "libucp_b200.so")
 COMM_SRC = os.path.join(HERE, "csrc", "ucp_comm.cpp")
+COMM_HDR = os.path.join(ROOT, "include", "ucp_b200_comm.h")
 COMM_OUT = os.path.join(HERE, "libucp_b200_comm.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC,-O2", "-ftz=false",
               "-prec-div=true", "-prec-sqrt=true", "-fmad=false"]
+_ID_RE = re.compile(rb"UCP_BUILD_ID:([0-9a-f]{32}|unknown)")
 
 
 def nvcc() -> str:
@@ -32,43 +42,69 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def _fresh(out: str, srcs: list) -> bool:
-    return os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(s) for s in srcs)
+def source_id(srcs) -> str | None:
+    """sha256 of the sources, first 32 hex digits (None if any is absent)."""
+    h = hashlib.sha256()
+    for s in srcs:
+        if not os.path.exists(s):
+            return None
+        with open(s, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:32]
 
 
-def build_comm(verbose: bool = False) -> str:
-    """libucp_b200_comm.so: host-only NCCL wrapper (links libnccl.so.2 by
-    soname, so a process that already loaded torch's NCCL reuses it)."""
-    srcs = [COMM_SRC, os.path.join(ROOT, "include", "ucp_b200_comm.h")]
-    if _fresh(COMM_OUT, srcs):
-        return COMM_OUT
-    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", os.path.join(ROOT, "include"),
-           "-I", os.path.join(CUDA_HOME, "include"), COMM_SRC, "-o", COMM_OUT + ".tmp",
-           "-L", os.path.join(CUDA_HOME, "lib64"), "-lnccl", "-lcudart"]
+def embedded_id(lib_path: str) -> str | None:
+    """The UCP_BUILD_ID baked into a built library (read from its bytes, so
+    the library is not loaded into this process)."""
+    if not os.path.exists(lib_path):
+        return None
+    with open(lib_path, "rb") as f:
+        m = _ID_RE.search(f.read())
+    return m.group(1).decode() if m else None
+
+
+def kernel_id() -> str | None:
+    return source_id([SRC, HDR])
+
+
+def comm_id() -> str | None:
+    return source_id([COMM_SRC, COMM_HDR])
+
+
+def _run(cmd: list, out: str, verbose: bool) -> None:
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode:
         sys.stderr.write(res.stdout + res.stderr)
     if res.returncode:
-        raise RuntimeError(f"g++ failed ({res.returncode}): {' '.join(cmd)}")
-    os.replace(COMM_OUT + ".tmp", COMM_OUT)
+        raise RuntimeError(f"build failed ({res.returncode}): {' '.join(cmd)}")
+    os.replace(out + ".tmp", out)
+
+
+def build_comm(verbose: bool = False, force: bool = False) -> str:
+    """libucp_b200_comm.so: host-only NCCL wrapper (links libnccl.so.2 by
+    soname, so a process that already loaded torch's NCCL reuses it)."""
+    sid = comm_id()
+    if not force and embedded_id(COMM_OUT) == sid:
+        return COMM_OUT
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", f'-DUCP_BUILD_ID="{sid}"',
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(CUDA_HOME, "include"),
+           COMM_SRC, "-o", COMM_OUT + ".tmp", "-L", os.path.join(CUDA_HOME, "lib64"), "-lnccl",
+           "-lcudart"]
+    _run(cmd, COMM_OUT, verbose)
     return COMM_OUT
 
 
-def build(verbose: bool = False) -> str:
-    """Compile if a .so is missing or older than its sources."""
-    build_comm(verbose)
-    srcs = [SRC, os.path.join(ROOT, "include", "ucp_b200.h")]
-    if _fresh(OUT, srcs):
+def build(verbose: bool = False, force: bool = False) -> str:
+    """Compile unless the library's embedded build id equals the sources'."""
+    build_comm(verbose, force)
+    sid = kernel_id()
+    if not force and embedded_id(OUT) == sid:
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), SRC, "-o", OUT + ".tmp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if verbose or res.returncode:
-        sys.stderr.write(res.stdout + res.stderr)
-    if res.returncode:
-        raise RuntimeError(f"nvcc failed ({res.returncode}): {' '.join(cmd)}")
-    os.replace(OUT + ".tmp", OUT)
+    cmd = [nvcc(), *NVCC_FLAGS, f'-DUCP_BUILD_ID="{sid}"', "-I", os.path.join(ROOT, "include"),
+           SRC, "-o", OUT + ".tmp"]
+    _run(cmd, OUT, verbose)
     return OUT
 
 
 if __name__ == "__main__":
-    print(build(verbose=True))
+    print(build(verbose=True, force="--force" in sys.argv))

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes
 import os
 
+from . import _build
 from ._errors import NativeUnavailableError
 
 LIB_NAME = "libucp_b200.so"
@@ -18,7 +19,7 @@ LIB_PATH = os.environ.get("UCP_B200_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), LIB_NAME)  # env override: kernel A/B experiments
 
 # exported symbols declared in include/ucp_b200.h
-EXPORTS = ("ucp_version", "ucp_status_reset", "ucp_runtile_scan", "ucp_convert_gather",
+EXPORTS = ("ucp_version", "ucp_build_id", "ucp_status_reset", "ucp_runtile_scan", "ucp_convert_gather",
            "ucp_load_scatter",
            "ucp_reshard_fused", "ucp_gen_state", "ucp_adam_step", "ucp_compare", "ucp_peek",
            "ucp_dev_alloc", "ucp_dev_free", "ucp_ipc_export", "ucp_ipc_open", "ucp_ipc_close")
@@ -30,6 +31,7 @@ _c = ctypes
 _P = _c.c_void_p
 _SIGS = {
     "ucp_version": (_c.c_int, []),
+    "ucp_build_id": (_c.c_char_p, []),
     "ucp_status_reset": (_c.c_int, [_P, _P]),
     "ucp_runtile_scan": (_c.c_int, [_P, _P, _P]),
     "ucp_convert_gather": (_c.c_int, [_P, _c.c_int64, _P, _P, _P, _P, _P, _P, _P]),
@@ -63,9 +65,26 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         fn.argtypes = args
     if lib.ucp_version() != ABI_VERSION:
         raise NativeUnavailableError(f"{path}: ABI {lib.ucp_version()} != {ABI_VERSION}")
+    _check_build_id(path, lib.ucp_build_id(), _build.kernel_id())
     if path == LIB_PATH:
         _lib = lib
     return lib
+
+
+def build_id(lib_handle=None) -> str:
+    """The build id baked into the loaded libucp_b200.so."""
+    raw = (lib_handle or lib()).ucp_build_id().decode()
+    return raw.split(":", 1)[1]
+
+
+def _check_build_id(path: str, raw: bytes, want: str | None) -> None:
+    """Refuse a library not built from the sources next to it (a stale or
+    foreign .so). Sources absent (an installed copy): nothing to check."""
+    got = raw.decode().split(":", 1)[-1]
+    if want is not None and got != want:
+        raise NativeUnavailableError(
+            f"{path} was built from other sources (build id {got}, sources {want}); "
+            "rebuild with __graft_entry__.build()")
 
 
 def lib() -> ctypes.CDLL:
@@ -75,11 +94,12 @@ def lib() -> ctypes.CDLL:
 # --------------------------------------------------------------------------- comm library
 
 COMM_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libucp_b200_comm.so")
-COMM_EXPORTS = ("ucp_comm_version", "ucp_comm_unique_id", "ucp_comm_init", "ucp_alltoallv",
+COMM_EXPORTS = ("ucp_comm_version", "ucp_comm_build_id", "ucp_comm_unique_id", "ucp_comm_init", "ucp_alltoallv",
                 "ucp_comm_destroy")
 _comm = None
 _COMM_SIGS = {
     "ucp_comm_version": (_c.c_int, []),
+    "ucp_comm_build_id": (_c.c_char_p, []),
     "ucp_comm_unique_id": (_c.c_int, [_P]),
     "ucp_comm_init": (_c.c_int, [_c.c_int, _c.c_int, _P, _P]),
     "ucp_alltoallv": (_c.c_int, [_P, _P, _P, _P, _P, _P]),
@@ -98,5 +118,6 @@ def comm_lib() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        _check_build_id(COMM_PATH, lib.ucp_comm_build_id(), _build.comm_id())
         _comm = lib
     return _comm

@@ -276,8 +276,11 @@ def _status(dev) -> Status:
 def release_staging() -> None:
     """Drop this thread's pinned / device staging buffers and its cached
     reshard() plan (they are grow-only and reused across calls otherwise)."""
+    from . import reshard as _reshard
+
     _LOCAL.stage = _Staging()
     _LOCAL.plans = {}
+    getattr(_reshard._D2D, "cache", {}).clear()  # reshard_device templates + their scratch
 
 
 def _run(prog: Program, gather: bool, src_base: int, dst_base: int, dev) -> None:
@@ -502,7 +505,7 @@ class _FusedStep:
             stream.synchronize()
             f, _ = st.read()
             if f != (1 << 64) - 1:
-                raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, src)
+                raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, src, (self.cprog,))
         raise RuntimeError("fused resume reported a failure that did not reproduce")
 
 

@@ -1441,6 +1441,11 @@ extern "C" {
 
 int ucp_version(void) { return UCP_ABI_VERSION; }
 
+#ifndef UCP_BUILD_ID
+#define UCP_BUILD_ID "unknown"
+#endif
+const char* ucp_build_id(void) { return "UCP_BUILD_ID:" UCP_BUILD_ID; }
+
 int ucp_status_reset(ucp_status* status, void* stream) {
   if (!status) return UCP_EINVAL;
   static_assert(sizeof(ucp_status) == 16, "ucp_status layout");

@@ -21,6 +21,11 @@ extern "C" {
 
 int ucp_comm_version(void) { return UCP_COMM_ABI_VERSION; }
 
+#ifndef UCP_BUILD_ID
+#define UCP_BUILD_ID "unknown"
+#endif
+const char* ucp_comm_build_id(void) { return "UCP_BUILD_ID:" UCP_BUILD_ID; }
+
 int ucp_comm_unique_id(ucp_comm_id* out) {
   if (!out) return UCP_COMM_EINVAL;
   ncclUniqueId id;

@@ -65,6 +65,15 @@ class _Table:
                                                       self.class_info.ctypes.data,
                                                       stream_ptr(None)), "runtile_scan")
 
+    def set_tables(self, runs: np.ndarray, aux: np.ndarray) -> None:
+        """Replace the run / aux contents in place (same shapes and class
+        order, e.g. addresses re-bound); the tile scan stays valid."""
+        self.runs_host, self.aux_host = runs, aux
+        if len(runs):
+            self._runs.copy_(torch.from_numpy(np.ascontiguousarray(runs).view(np.uint8)),
+                             non_blocking=False)
+        self._aux.copy_(torch.from_numpy(np.ascontiguousarray(aux).view(np.uint8)))
+
     @property
     def tiles_host(self) -> np.ndarray:
         """Every tile as the kernels derive it (tests / diagnostics)."""
@@ -129,7 +138,9 @@ class Status:
     """Device status word (ucp_status) + host readback."""
 
     def __init__(self, device: torch.device):
-        self.t = torch.zeros(2, dtype=torch.int64, device=device)
+        # constructed in the "ok" state (first = ~0, n_bad = 0): a word of
+        # zeros would decode as "failure at run 0, element 0"
+        self.t = torch.tensor([-1, 0], dtype=torch.int64, device=device)
         self.ptr = self.t.data_ptr()
 
     def reset(self, stream=None) -> None:
@@ -153,15 +164,48 @@ def _peek_f32(addr: int) -> int:
     return int(out[0]) if rc == 0 else 0xFFFFFFFF
 
 
-def describe_failure(prog: Program, run_idx: int, elem: int, src_base: int) -> Exception:
+def _unit_pad_error(progs, param: str, kind: str, src_base: int) -> Exception | None:
+    """PaddingError if any pad-check (CHECKZERO) run of unit (param, kind)
+    in ``progs`` sees a nonzero bit pattern, else None. The reference strips
+    pads inside _collapse_dp, before it compares tp replicas
+    (ucp/convert.py:192, :262-278), so a bad pad outranks a replica mismatch
+    of the same unit; the status word orders runs by kernel class instead.
+    Pads are < dp elements per tp rank, so this is a few tiny peeks."""
+    for prog in progs:
+        runs = prog.runs_host
+        if "op" not in runs.dtype.names:
+            continue
+        for j in np.nonzero(runs["op"] == OP_CHECKZERO)[0]:
+            r = runs[j]
+            u = prog.units[int(r["tag"])]
+            if (u.param, u.kind) != (param, kind):
+                continue
+            n = int(r["rows"]) * int(r["cols"])
+            buf = np.zeros(n, dtype=np.uint32)
+            if _native.lib().ucp_peek(ctypes.c_void_p(src_base + int(r["src"])), buf.ctypes.data,
+                                      4 * n) != 0:
+                continue
+            bad = np.nonzero(buf)[0]
+            if len(bad):
+                return PaddingError(f"{param}.{kind}: nonzero pad tail (first bad element "
+                                    f"{int(bad[0])})")
+    return None
+
+
+def describe_failure(prog: Program, run_idx: int, elem: int, src_base: int,
+                     pad_progs=()) -> Exception:
     """Reference-style exception for a failing run (ucp/convert.py:165-171,
-    :272-277, :127-128)."""
+    :272-277, :127-128). ``pad_progs``: other tables of the same window
+    that hold the unit's pad checks (the unfused rest of a fused window)."""
     r = prog.runs_host[run_idx]
     unit = prog.units[int(r["tag"])]
     where = f"{unit.param}.{unit.kind}"
     fused = "atom" in r.dtype.names
     if not fused and int(r["op"]) == OP_CHECKZERO:
         return PaddingError(f"{where}: nonzero pad tail (first bad element {elem})")
+    pad = _unit_pad_error((prog, *pad_progs), unit.param, unit.kind, src_base)
+    if pad is not None:
+        return pad
     labels = unit.labels.get(int(prog.run_order[run_idx]))  # keyed by table index
     row, col = divmod(elem, int(r["cols"]))
     n_src, groups = int(r["n_src"]), 1 if fused else max(int(r["groups"]), 1)

@@ -467,14 +467,16 @@ def _mode_shape(p, mode, cfg):
 
 def _emit_group(tab, p, groups, corrs, fn, dst_off, op, tag, G):
     """Runs writing atomic regions from `groups` (list over G of replica
-    source maps) through `corrs`."""
+    source maps) through `corrs`. dst_off None: verify-only runs (replica
+    checks with no destination)."""
     maps = [m for grp in groups for m in grp]
     labels = [m.label for m in maps]
     cuts = _cuts(maps, 0, fn)
     for a, b in zip(cuts[:-1], cuts[1:]):
         for corr in corrs:
             for fs, xs, xp, rows, cols in split_rows(corr, a, b):
-                tab.add(srcs=[m.offset(fs) for m in maps], dsts=[dst_off + 4 * xs],
+                tab.add(srcs=[m.offset(fs) for m in maps],
+                        dsts=[] if dst_off is None else [dst_off + 4 * xs],
                         src_pitch=corr[4], dst_pitch=xp, rows=rows, cols=cols, op=op,
                         groups=G, tag=tag, labels=labels)
 
@@ -536,8 +538,17 @@ def compile_union(tab: RunTable, p: ParamSpec, cfg: ParallelConfig, frags: list,
                     OP_COPY, tag, 1)
     elif mode == PARTIAL:
         groups = [per_tp[t] for t in range(cfg.tp)]
-        _emit_group(tab, p, groups, tp_correspondences(p, mode, cfg.tp, 0), fn, dst_off,
-                    OP_MEAN, tag, cfg.tp)
+        corrs = tp_correspondences(p, mode, cfg.tp, 0)
+        if sum(len(g) for g in groups) - 1 > MAX_AUX:
+            # too many sources for one averaged run (tp x dp replicas): each
+            # tp rank's dp replicas are checked by verify-only COPY runs
+            # (split further by RunTable.add), then the MEAN reads one
+            # replica per tp rank -- the same bytes, in _collapse_dp order
+            for grp in groups:
+                if len(grp) > 1:
+                    _emit_group(tab, p, [grp], corrs, fn, None, OP_COPY, tag, 1)
+            groups = [grp[:1] for grp in groups]
+        _emit_group(tab, p, groups, corrs, fn, dst_off, OP_MEAN, tag, cfg.tp)
     else:
         for t in range(cfg.tp):
             _emit_group(tab, p, [per_tp[t]], tp_correspondences(p, mode, cfg.tp, t, vrows), fn,
@@ -762,7 +773,10 @@ def compile_fused(fx: XRunTable, rest_conv: RunTable, rest_load: RunTable, p: Pa
     ok = n > 0
     for i, r in enumerate(conv._rows):
         (s0, d0, sp, dp, rows, cols, aux, ns, nd, groups, op, dt, tpr, tp, tag, flags) = r
-        if op == OP_CHECKZERO:
+        if op == OP_CHECKZERO or (op == OP_COPY and nd == 0):
+            # pad checks and the verify-only continuation runs of units with
+            # more than MAX_SRC replicas (RunTable.add) have no atomic
+            # destination: they run unfused, reading only their sources
             extra_conv.append(i)
             continue
         if op != OP_COPY or ns > MAX_SRC:

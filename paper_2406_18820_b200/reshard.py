@@ -403,7 +403,7 @@ class ReshardPlan:
             torch.cuda.synchronize(self.device)
             f, _ = self.status.read()
             if f != (1 << 64) - 1:
-                raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, src_ptr)
+                raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, src_ptr, (W.conv,))
 
     # ------------------------------------------------------------------ host-streamed
 
@@ -626,16 +626,16 @@ class ReshardPlan:
 _TORCH_OF = {DType.F32: torch.float32, DType.BF16: torch.bfloat16, DType.F16: torch.float16}
 
 
-_SRC_V, _TGT_V = 1 << 56, 1 << 57  # virtual address spaces of a cached d2d template
+_SRC_V, _TGT_V, _ATOM_V = 1 << 56, 1 << 57, 1 << 58  # virtual spaces of a d2d template
 _D2D = threading.local()
 
 
-def _rebind(v: np.ndarray, starts: np.ndarray, real: np.ndarray) -> np.ndarray:
-    """Map virtual addresses (>= _SRC_V) inside fragment k, which starts at
+def _rebind(v: np.ndarray, starts: np.ndarray, real: np.ndarray, lo: int = _SRC_V) -> np.ndarray:
+    """Map virtual addresses (>= lo) inside fragment k, which starts at
     starts[k] (sorted), to real[k] + offset; other values (real scratch
     addresses, zeros) pass through."""
     v = v.astype(np.uint64, copy=True)
-    mask = v >= np.uint64(_SRC_V)
+    mask = v >= np.uint64(lo)
     if mask.any():
         k = np.searchsorted(starts, v[mask], side="right") - 1
         v[mask] = real[k] + (v[mask] - starts[k])
@@ -659,20 +659,40 @@ class _D2DTemplate:
         for (g, i), (m, a) in tgt_addr.items():
             targets.setdefault((m.param, m.kind), []).append((m, a))
         wins = make_windows(spec.params, window_bytes)
-        self.scratch = torch.empty(max(max(sum(3 * align_up(4 * p.numel) for p in W.params)
-                                           for W in wins), 256), dtype=torch.uint8, device=device)
-        self.progs = []
+        # the atomic of a unit is compiled at a virtual address; only units
+        # that do not fuse (Partial mean / noise) need real scratch, packed
+        # per window and bound once the largest window's need is known
+        built, need = [], 0
         for W in wins:
             fx, rc, rl = XRunTable(), RunTable(), RunTable()
-            at = self.scratch.data_ptr()
+            vstarts, offs, at = [], [], 0
             for p in W.params:
                 for k in STATE_KINDS:
                     dt = dtype if k == "weight" else DType.F32
-                    compile_fused(fx, rc, rl, p, src, frags.get((p.name, k), []), at, tgt,
-                                  targets.get((p.name, k), []), dt, strict, False)
-                    at += align_up(4 * p.numel)
+                    v = _ATOM_V + len(vstarts) * (1 << 40)
+                    if not compile_fused(fx, rc, rl, p, src, frags.get((p.name, k), []), v, tgt,
+                                         targets.get((p.name, k), []), dt, strict, False):
+                        vstarts.append(v)
+                        offs.append(at)
+                        at += align_up(4 * p.numel)
+                    else:
+                        vstarts.append(v)
+                        offs.append(-1)
+            need = max(need, at)
+            built.append((fx, rc, rl, vstarts, offs))
+        self.scratch = (torch.empty(need, dtype=torch.uint8, device=device) if need else None)
+        base = self.scratch.data_ptr() if need else 0
+        self.progs = []
+        for fx, rc, rl, vstarts, offs in built:
+            starts = np.array(vstarts, dtype=np.uint64)
+            real = np.array([base + max(o, 0) for o in offs], dtype=np.uint64)
             progs = (XProgram(fx, device, tile_bytes), Program(rc, device, tile_bytes),
                      Program(rl, device, tile_bytes))
+            for prog in progs[1:]:  # rest tables address the scratch atomics
+                runs = prog.runs_host.copy()
+                for f in ("src", "dst"):
+                    runs[f] = _rebind(runs[f], starts, real, _ATOM_V)
+                prog.set_tables(runs, _rebind(prog.aux_host, starts, real, _ATOM_V))
             for prog in progs:
                 prog.virt = (prog.runs_host.copy(), prog.aux_host.copy())
             self.progs.append(progs)
@@ -795,6 +815,6 @@ def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, sh
                 torch.cuda.synchronize(device)
                 f, _ = status.read()
                 if f != (1 << 64) - 1:
-                    raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, 0)
+                    raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, 0, (conv,))
         raise RuntimeError("reshard reported a failure that did not reproduce")
     return out

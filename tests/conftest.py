@@ -16,6 +16,24 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libucp_b200.so")
 
 
+def pytest_collection_modifyitems(config, items):
+    """Tests marked gpu skip on a machine without a CUDA device (a plain
+    ``pytest`` there stays green). With a device they always run: a missing
+    libucp_b200.so then fails them loudly (there is no CPU fallback)."""
+    try:
+        import torch
+
+        has_cuda = torch.cuda.is_available()
+    except Exception:  # noqa: BLE001
+        has_cuda = False
+    if has_cuda:
+        return
+    skip = pytest.mark.skip(reason="no CUDA device")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
+
+
 @pytest.fixture(scope="session")
 def golden():
     with open(os.path.join(GOLDEN_DIR, "golden.json")) as f:

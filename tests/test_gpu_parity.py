@@ -761,3 +761,49 @@ def test_reshard_device_template_rebinding(golden):
         assert O.world_digest(wd) == row["world_F32"], trial
         if trial < 2:
             assert len(R._D2D.cache) == 1
+
+
+@pytest.mark.parametrize("path", ["union", "host", "device", "unfused"])
+def test_pad_error_outranks_tp_mismatch(path):
+    # Z1 m of a tp-replicated LayerNorm bias with BOTH a nonzero pad and a
+    # tp-replica mismatch: the reference strips pads inside _collapse_dp,
+    # before it compares tp replicas (ucp/convert.py:192, :262-278), so it
+    # raises PaddingError; the GPU path must name the same fault
+    spec = U.make_model("DenseGPT", {"n_layers": 1, "hidden": 1024})
+    src, tgt = cfg(dp=3, tp=2, zero="z1"), cfg(dp=2, zero="z1")
+    shards = O.partition_mem(spec, O.init_state(spec, 7), src)
+    recs = U.enumerate_rank_records(spec, src, 0)
+    for g in range(src.world_size):
+        for i, (m, a) in enumerate(shards[g]):
+            if (m.param, m.kind) != ("layers.0.ln_b", "m") or m.placement[1] != 1:
+                continue
+            a = a.copy()
+            if m.pad_elems:
+                a[-1] = np.float32(1.0)  # nonzero pad on the last dp rank of tp 1
+            else:
+                a[3] = np.float32(0.25)  # tp 1 differs from tp 0
+            shards[g][i] = (m, a)
+    assert recs
+    with pytest.raises(O.OracleError, match="PaddingError"):
+        O.convert_mem(spec, src, shards)
+    with pytest.raises(U.PaddingError):
+        if path == "union":
+            p = spec.param("layers.0.ln_b")
+            U.union(p, src, [U.FragmentMsg(m, a) for g in range(src.world_size)
+                             for m, a in shards[g] if (m.param, m.kind) == (p.name, "m")])
+        elif path == "device":
+            U.reshard(spec, src, tgt, {g: [torch.from_numpy(a).cuda() for _, a in v]
+                                       for g, v in shards.items()})
+        else:
+            U.reshard(spec, src, tgt, {g: [a for _, a in v] for g, v in shards.items()},
+                      fused=path == "host")
+
+
+def test_fresh_plan_check_is_clean():
+    # a plan's status word starts "ok": check() before any reset is silent
+    spec = U.make_model("DenseGPT", {"n_layers": 1, "hidden": 32})
+    plan = ReshardPlan(spec, cfg(dp=2, zero="z1"), cfg(tp=2), fused=True)
+    plan.synthesize()
+    plan.step_device()
+    torch.cuda.synchronize()
+    plan.check()

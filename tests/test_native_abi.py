@@ -16,7 +16,7 @@ HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 
 def _declared():
     text = open(HDR).read()
-    return sorted(set(re.findall(r"^int\s+(ucp_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(ucp_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -67,7 +67,8 @@ def test_argument_errors_without_device():
 
 def test_comm_library_exports():
     hdr = HDR.replace("ucp_b200.h", "ucp_b200_comm.h")
-    names = sorted(set(re.findall(r"^int\s+(ucp_\w+)\s*\(", open(hdr).read(), flags=re.M)))
+    names = sorted(set(re.findall(r"^(?:int|const char\*)\s+(ucp_\w+)\s*\(", open(hdr).read(),
+                                  flags=re.M)))
     assert names == sorted(_native.COMM_EXPORTS)
     lib = _native.comm_lib()
     for n in names:
@@ -109,3 +110,23 @@ def test_no_cpu_fallback_without_a_device(tmp_path):
         U.ReshardPlan(spec, U.ParallelConfig(dp=2, zero_stage=U.ZeroStage.Z1), U.ParallelConfig())
     with pytest.raises(U.NativeUnavailableError):
         _native.load_library(str(tmp_path / "missing.so"))
+
+
+def test_build_id_matches_sources():
+    # provenance: the loaded library was built from the committed sources
+    from paper_2406_18820_b200 import _build
+
+    lib = _native.load_library()
+    assert _native.build_id(lib) == _build.kernel_id()
+    assert _build.embedded_id(_native.LIB_PATH) == _build.kernel_id()
+    assert _build.embedded_id(_native.COMM_PATH) == _build.comm_id()
+
+
+def test_stale_library_is_refused():
+    import pytest
+
+    from paper_2406_18820_b200._errors import NativeUnavailableError
+
+    with pytest.raises(NativeUnavailableError, match="other sources"):
+        _native._check_build_id("x.so", b"UCP_BUILD_ID:" + b"0" * 32, "f" * 32)
+    _native._check_build_id("x.so", b"UCP_BUILD_ID:" + b"0" * 32, None)

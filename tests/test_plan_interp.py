@@ -310,7 +310,10 @@ def test_device_tile_derivation_matches_expansion(tb):
     assert got == [tuple(int(x) for x in t) for t in want]
 
 
-def _fused_world(spec, src_cfg, tgt_cfg, shards, dtype, tile_bytes=4096, materialize=True):
+def _fused_world(spec, src_cfg, tgt_cfg, shards, dtype, tile_bytes=4096, materialize=True,
+                 fails=None):
+    """Fused tables of every unit through the interpreter. ``fails``: a
+    list collecting (table, run, elem) failures instead of asserting none."""
     from descr_interp import execute_fused
     from paper_2406_18820_b200.plan import XRunTable, compile_fused
 
@@ -345,11 +348,15 @@ def _fused_world(spec, src_cfg, tgt_cfg, shards, dtype, tile_bytes=4096, materia
     atom = np.zeros(max(aat, 16), dtype=np.uint8)
     dst = np.full(max(tat, 16), 0xCD, dtype=np.uint8)
     xr, xa, xrt, _, _ = fx.finish_classed(tile_bytes)
-    assert execute_fused(xr, xa, expand_tiles(xr, xrt), src, atom, dst) == []
+    got = [("fused",) + f for f in execute_fused(xr, xa, expand_tiles(xr, xrt), src, atom, dst)]
     r1, a1, t1 = rc.finish(tile_bytes)
-    assert execute(r1, a1, t1, src, atom) == []
+    got += [("conv",) + f for f in execute(r1, a1, t1, src, atom)]
     r2, a2, t2 = rl.finish(tile_bytes)
-    assert execute(r2, a2, t2, atom, dst) == []
+    got += [("load",) + f for f in execute(r2, a2, t2, atom, dst)]
+    if fails is None:
+        assert got == []
+    else:
+        fails.extend(got)
     world = {}
     for g, m, o, n, odt in outs:
         shape = U.plan.fragment_shape(spec.param(m.param), tgt_cfg, m)
@@ -443,3 +450,80 @@ def test_fused_remainder_keeps_unit_provenance():
             unit = table.units[row[14]]
             lo, hi = aoff[(unit.param, unit.kind)]
             assert lo <= row[field] < hi, (unit.param, unit.kind)
+
+
+def _ln_spec():
+    return U.make_model("DenseGPT", {"n_layers": 1, "hidden": 32})
+
+
+@pytest.mark.parametrize("bad_dp", [None, 3, 70, 79])
+def test_fused_checks_every_replica_beyond_64(bad_dp):
+    # dp = 80 Z0: every weight has 80 replicas, more than one run holds
+    # (MAX_SRC); the verify-only continuation runs must still run when the
+    # unit fuses, so a flipped late replica is reported like the reference
+    # does (ucp/convert.py:163-172)
+    spec = _ln_spec()
+    src_cfg = ParallelConfig(dp=80, zero_stage=ZeroStage.Z0)
+    tgt_cfg = ParallelConfig(dp=2, zero_stage=ZeroStage.Z1)
+    state = O.init_state(spec, 7)
+    shards = O.partition_mem(spec, state, src_cfg)
+    target = "layers.0.ln_w"
+    if bad_dp is not None:
+        recs = all_rank_records(spec, src_cfg)
+        g = next(g for g in range(src_cfg.world_size) if recs[g][0].placement[2] == bad_dp)
+        i = next(i for i, m in enumerate(recs[g]) if (m.param, m.kind) == (target, "weight"))
+        m, a = shards[g][i]
+        a = a.copy()
+        a.reshape(-1).view(np.uint32)[5] ^= 1
+        shards[g][i] = (m, a)
+    fails = []
+    world, _, fused, _ = _fused_world(spec, src_cfg, tgt_cfg, shards, DType.F32, fails=fails)
+    assert fused > 0
+    if bad_dp is None:
+        assert fails == []
+        want = O.load_mem(spec, O.convert_mem(spec, src_cfg, shards), tgt_cfg, "F32")
+        assert O.world_digest(world) == O.world_digest(want)
+    else:
+        assert fails, "a corrupted replica beyond the first run went unchecked"
+        assert all(f[2] == 5 for f in fails)
+
+
+@pytest.mark.parametrize("bad", [False, True])
+def test_partial_mean_with_more_replicas_than_one_run(bad):
+    # tp = 8, dp = 40 Z0: 320 sources for the averaged pos.alibi vector, more
+    # than one averaged run can carry; the dp replicas are verified by
+    # verify-only runs and the f64 mean reads one replica per tp rank
+    spec = _ln_spec()
+    src_cfg = ParallelConfig(dp=40, tp=8, zero_stage=ZeroStage.Z0)
+    state = O.init_state(spec, 7)
+    shards = O.partition_mem(spec, state, src_cfg)
+    alibi = next(p for p in spec.params if p.kind == ParamKind.ASYNC_PARTIAL)
+    if bad:
+        recs = all_rank_records(spec, src_cfg)
+        g = next(g for g in range(src_cfg.world_size) if recs[g][0].placement[1:] == (3, 33))
+        i = next(i for i, m in enumerate(recs[g]) if (m.param, m.kind) == (alibi.name, "v"))
+        m, a = shards[g][i]
+        a = a.copy()
+        a.reshape(-1).view(np.uint32)[2] ^= 1
+        shards[g][i] = (m, a)
+        with pytest.raises(O.OracleError, match="ReplicateMismatchError"):
+            O.convert_mem(spec, src_cfg, shards)
+    got, fails, _ = _arena_union(spec, src_cfg, shards)
+    if bad:
+        assert fails and all(e == 2 for _, e in fails)
+        return
+    assert fails == []
+    want = O.convert_mem(spec, src_cfg, shards)
+    for p in spec.params:
+        for k in STATE_KINDS:
+            assert np.array_equal(got[(p.name, k)].view(np.uint32),
+                                  want[p.name][k].view(np.uint32)), (p.name, k)
+
+
+def test_status_word_starts_ok():
+    # a fresh status word decodes as "no failure" (first = ~0, n_bad = 0)
+    import torch
+
+    from paper_2406_18820_b200.engine import Status
+
+    assert Status(torch.device("cpu")).read() == ((1 << 64) - 1, 0)
