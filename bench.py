@@ -72,6 +72,9 @@ def parse():
                          "GPU's CUDA-IPC-mapped buffer over NVLink; nccl = all-to-all-v per "
                          "window through libucp_b200_comm.so; torch = the same through "
                          "torch.distributed")
+    ap.add_argument("--no-exchange", action="store_true",
+                    help="N>1: skip the rank-homed NCCL leg that times the exchange stage")
+    ap.add_argument("--exchange-steps", type=int, default=5)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to smoke-test the multi-rank logic with >1 rank per GPU")
     ap.add_argument("--no-atomic", action="store_true",
@@ -82,6 +85,10 @@ def parse():
     ap.add_argument("--unfused", action="store_true",
                     help="separate convert and load launches (atomic re-read from HBM)")
     ap.add_argument("--cpu-threads", type=int, default=os.cpu_count())
+    ap.add_argument("--no-file-leg", action="store_true",
+                    help="skip the cfg1 file-pipeline leg (reference vs ours on tmpfs)")
+    ap.add_argument("--no-public-e2e", action="store_true",
+                    help="skip timing the e2e sample through the public numpy reshard()")
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16"],
                     help="target weight dtype of load (moments stay f32), ucp/load.py:204-205")
     return ap.parse_args()
@@ -91,21 +98,76 @@ def parse():
 
 
 class ClockSampler:
+    """SM clock and clock-event (throttle) reasons of one GPU during the timed
+    region: an NVML thread samples every 5 ms (so even a region of a few ms
+    gets samples), plus one sample at start and one at stop. Falls back to
+    ``nvidia-smi -lms 100`` when NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80))
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.path = tempfile.mktemp(suffix=".csv")
+    def __init__(self, index: int, period: float = 0.005):
+        import threading
+
+        self.index, self.period, self.rows = index, period, []
+        self.proc = self.h = None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            try:
+                pr = torch.cuda.get_device_properties(index)
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(
+                    f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+            except Exception:  # noqa: BLE001
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - no NVML: nvidia-smi polling
+            self.h = None
+        if self.h is None:
+            self.path = tempfile.mktemp(suffix=".csv")
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            except OSError:
+                self.proc = None
+            return
+        self._stop = threading.Event()
+        self.sample()
+        self.thread = threading.Thread(target=self._loop, daemon=True)
+        self.thread.start()
+
+    def sample(self) -> None:
+        nv = self.nv
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:  # noqa: BLE001
+            return
+        self.rows.append((sm, rs))
+
+    def _loop(self) -> None:
+        while not self._stop.wait(self.period):
+            self.sample()
 
     def stop(self) -> dict:
+        if self.h is not None:
+            self._stop.set()
+            self.thread.join(timeout=5)
+            self.sample()
+            sm = [r[0] for r in self.rows]
+            reasons = sorted({n for _, rs in self.rows for n, bit in self.REASONS if rs & bit})
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_sm,
+                    "reasons": reasons, "samples": len(sm), "gpu": self.index,
+                    "how": "NVML every 5 ms in a thread + one sample at start and stop"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -125,7 +187,82 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "gpu": self.index, "how": "nvidia-smi -lms 100"}
+
+
+def merge_clocks(per_gpu: list) -> dict:
+    """Job-level clocks line from every rank's sampler: median of the
+    per-GPU medians, max of the max clocks, the union of the reasons; the
+    per-GPU lines are kept."""
+    sm = [c["sm_mhz"] for c in per_gpu if c.get("sm_mhz") is not None]
+    mx = [c["sm_max_mhz"] for c in per_gpu if c.get("sm_max_mhz") is not None]
+    out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+           "reasons": sorted({r for c in per_gpu for r in c.get("reasons", [])}),
+           "samples": sum(c.get("samples", 0) for c in per_gpu)}
+    if len(per_gpu) > 1:
+        out["per_gpu"] = per_gpu
+    else:
+        out.update({k: v for k, v in per_gpu[0].items() if k not in out})
+    return out
+
+
+NVLINK_GBPS = 900.0  # NVLink 5 per direction per B200 (SURVEY 8d: the all-to-all roofline)
+
+
+def gather_stats(local: dict, world: int) -> list:
+    """Every rank's local stats on every rank (all_gather_object over the
+    default group: NCCL on the box, gloo in the CPU tests)."""
+    if world == 1:
+        return [local]
+    import torch.distributed as dist
+
+    out = [None] * world
+    dist.all_gather_object(out, local)
+    return out
+
+
+def aggregate_ranks(stats: list, peak: float) -> dict:
+    """Whole-job figures from every rank's local stats (rank 0 emits them):
+    value = sum of state bytes / max-over-ranks step time; the aggregate HBM
+    roofline = sum of algorithmic bytes / max step time vs N x peak; the
+    exchange stage (rank-homed all-to-all-v) vs NVLink; merged clocks."""
+    N = len(stats)
+    ms = max(s["ms"] for s in stats)
+    S = sum(s["S"] for s in stats)
+    hbm = sum(s["hbm_bytes"] for s in stats)
+    per_rank = [{"rank": i, "ms": s["ms"], "state_bytes": s["S"], "hbm_bytes": s["hbm_bytes"],
+                 "frac": s["hbm_bytes"] / (s["ms"] / 1e3) / GB / peak if s["ms"] else 0}
+                for i, s in enumerate(stats)]
+    agg = {"bound": "hbm", "achieved": hbm / (ms / 1e3) / GB, "peak": N * peak, "unit": "GB/s",
+           "frac": hbm / (ms / 1e3) / GB / (N * peak), "n_gpus": N, "hbm_bytes_per_step": hbm,
+           "what": "sum of every rank's algorithmic HBM bytes per step / max-over-ranks step "
+                   "time, vs N x MEASURED_PEAKS.json hbm_gbs",
+           "load_balance": min(s["ms"] for s in stats) / ms if ms else None,
+           "per_rank": per_rank}
+    out = {"value": S / (ms / 1e3) / GB, "ms": ms, "S": S, "aggregate": agg,
+           "clocks": merge_clocks([s["clocks"] for s in stats])}
+    xs = [s.get("exchange") for s in stats]
+    if any(xs):
+        xs = [x for x in xs if x]
+        t = max(x["exchange_ms"] for x in xs)
+        sent = max(x["bytes_sent"] for x in xs)
+        per = [x["bytes_sent"] / (x["exchange_ms"] / 1e3) / GB if x["exchange_ms"] else 0
+               for x in xs]
+        step = max(x["step_ms"] for x in xs)
+        out["exchange"] = {
+            "transport": xs[0]["transport"], "bytes_sent_per_gpu_max": sent,
+            "bytes_sent_total": sum(x["bytes_sent"] for x in xs), "exchange_ms_max": t,
+            "GBps_per_gpu": sent / (t / 1e3) / GB if t else None,
+            "nvlink_frac": sent / (t / 1e3) / GB / NVLINK_GBPS if t else None,
+            "nvlink_peak_GBps": NVLINK_GBPS, "per_rank_GBps": per,
+            "step_ms": step, "value": S / (step / 1e3) / GB if step else None,
+            "what": "rank-homed reshard (target rank g on GPU g mod N): per window one "
+                    "all-to-all-v of the target fragments whose param owner is another GPU, "
+                    "on a comm stream overlapped with the next window's kernels. exchange_ms = "
+                    "CUDA events around the all-to-all-v calls on the comm stream; "
+                    "nvlink_frac = bytes sent by the busiest GPU / exchange_ms / 900 GB/s; "
+                    "value = state GB/s of the whole rank-homed step"}
+    return out
 
 
 # --------------------------------------------------------------------------- helpers
@@ -189,7 +326,8 @@ class CpuArm:
             from oracle import ucp_oracle as O
 
             self.kind = "port"
-            self.union, self.extract = (lambda p, c, fs: O.union(p, c, fs, True)), O.extract
+            self.union_s, self.extract = (lambda p, c, fs, st=True: O.union(p, c, fs, st)), O.extract
+            self.union = self.union_s
             self.spec, self.src, self.tgt, self.frags, self.by_unit = spec, src, tgt, frags, by_unit
             return
         from paper_2406_18820_b200.spec import format_config_string, spec_to_dict
@@ -206,15 +344,17 @@ class CpuArm:
                             m.segments, m.flat_range, m.pad_elems)
         self.frags = {k: [FM(meta(m), a) for m, a in v] for k, v in frags.items()}
         self.by_unit = {k: [(g, meta(m)) for g, m in v] for k, v in by_unit.items()}
-        self.union = lambda p, c, fs: sys.modules["ucp.convert"].union(p, c, fs, True)
+        self.union_s = lambda p, c, fs, st=True: sys.modules["ucp.convert"].union(p, c, fs, st)
+        self.union = self.union_s
         self.extract = u.parallel.extract_fragment
 
-    def run(self, threads: int, collect: dict | None = None) -> float:
+    def run(self, threads: int, collect: dict | None = None, strict: bool = True) -> float:
         """Seconds for one pass over the sample. ``collect`` (optional)
-        receives every target fragment as {(g, param, kind): array}."""
+        receives every target fragment as {(g, param, kind): array};
+        ``strict`` is union's strict_replicate (False: one replica read)."""
         def unit(key):
             p = self.spec.param(key[0])
-            full = self.union(p, self.src, self.frags[key])
+            full = self.union_s(p, self.src, self.frags[key], strict)
             for g, m in self.by_unit.get(key, ()):
                 out = np_copy(self.extract(p, self.tgt, m, full))
                 if collect is not None:
@@ -368,19 +508,125 @@ def link_roofline(link: dict, h2d: int, d2h: int, ms: float) -> dict:
     return out
 
 
+def public_e2e(spec, src, tgt, names, eplan, host_src, wdt, steps: int) -> dict:
+    """The e2e sample again through the public in-memory API, numpy in and
+    numpy out: ``reshard(spec', src, tgt, {g: [ndarray]})`` over a model
+    spec restricted to the sample's params, so packing the caller's arrays
+    into pinned memory, H2D, the fused reshard, D2H and handing back numpy
+    target arrays are all inside the wall-clock timed call. One warm-up call
+    (plan compile + first pinned allocations) first; each result is dropped
+    before the next call, as a caller consuming it would (its pinned arena is
+    then reused)."""
+    import paper_2406_18820_b200 as U
+    from paper_2406_18820_b200.spec import ModelSpec
+
+    keep = set(names)
+    sub = ModelSpec(spec.name, spec.n_layers,
+                    tuple(tp for tp in spec.tied_pairs if tp[0] in keep and tp[1] in keep),
+                    tuple(p for p in spec.params if p.name in keep))
+    hv = host_src.numpy()
+    per: dict = {}
+    for W in eplan.windows:
+        for g, i, m, off, n in W.src_frags:
+            at = W.src_base + off
+            per.setdefault(g, []).append((i, hv[at:at + 4 * n].view("<f4").copy()))
+    shards = {g: [a for _, a in sorted(v, key=lambda t: t[0])] for g, v in per.items()}
+    S = 12 * sum(p.numel for p in sub.params)
+    in_bytes = sum(a.nbytes for v in shards.values() for a in v)
+    out = U.reshard(sub, src, tgt, shards, dtype=wdt)
+    out_bytes = sum(np.asarray(a).nbytes for v in out.values() for a in v)
+    del out
+    ts = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        out = U.reshard(sub, src, tgt, shards, dtype=wdt)
+        ts.append(time.perf_counter() - t0)
+        del out
+    t = statistics.median(ts)
+    return {"value": S / t / GB, "unit": "GB/s", "s_per_call": t, "calls": len(ts),
+            "state_bytes": S, "in_bytes": in_bytes, "out_bytes": out_bytes,
+            "api": "paper_2406_18820_b200.reshard(spec, src, tgt, {g: [np.ndarray]}) -> "
+                   "{g: [np.ndarray]} (the in-memory resume(): pack into pinned memory, H2D, "
+                   "fused reshard, D2H, numpy views), wall clock, median; rank 0"}
+
+
+def cpu_model() -> str:
+    """The host CPU model (lscpu), for the cpu_baseline line."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+def file_leg(threads: int, root: str = "/dev/shm/ucp_bench_file") -> dict:
+    """the reference's own file pipeline, convert(n_workers =
+    cores) + load, on tmpfs for cfg1 (GPT-2-small), next to this engine's
+    drop-in convert() / load() on the same source tree (written by the
+    product's partition(), byte-identical to the reference's). GB/s of state;
+    best of 2 runs each."""
+    import shutil
+
+    import paper_2406_18820_b200 as U
+
+    ucp = reference_ucp()
+    spec, src, tgt, desc = U.bench_config("cfg1")
+    S = 12 * spec.total_numel
+    shutil.rmtree(root, ignore_errors=True)
+    os.makedirs(root)
+    try:
+        src_dir = os.path.join(root, "src")
+        U.partition(U.init_state(spec, 7), src, src_dir)
+        out = {"workload": desc, "state_bytes": S, "fs": "tmpfs (/dev/shm)", "workers": threads}
+
+        def best(fn, reps=2):
+            ts = []
+            for r in range(reps):
+                d = os.path.join(root, f"out{r}")
+                t = time.perf_counter()
+                fn(d)
+                ts.append(time.perf_counter() - t)
+                shutil.rmtree(d, ignore_errors=True)
+            return min(ts)
+
+        atom = os.path.join(root, "atom_ours")
+        U.convert(src_dir, atom, n_workers=threads)
+        c = best(lambda d: U.convert(src_dir, d, n_workers=threads))
+        lo = best(lambda d: U.load(atom, tgt))
+        out["ours"] = {"convert_GBps": S / c / GB, "load_GBps": S / lo / GB,
+                       "convert_plus_load_GBps": S / (c + lo) / GB}
+        if ucp is not None:
+            rtgt = ucp.parse_config_string(U.format_config_string(tgt))
+            ratom = os.path.join(root, "atom_ref")
+            ucp.convert(src_dir, ratom, n_workers=threads)
+            c = best(lambda d: ucp.convert(src_dir, d, n_workers=threads))
+            lo = best(lambda d: ucp.load(ratom, rtgt))
+            out["reference"] = {"convert_GBps": S / c / GB, "load_GBps": S / lo / GB,
+                                "convert_plus_load_GBps": S / (c + lo) / GB,
+                                "what": "ucp.convert(n_workers=cores) + ucp.load from baseline/_ref"}
+        return out
+    finally:
+        shutil.rmtree(root, ignore_errors=True)
+
+
 def cpu_leg(args, spec, src, tgt, host_cpu_frags, cpu_names, gpu_index, host_tgt) -> dict:
     """cpu_baseline: the reference's union + extract_fragment on the host's
-    cores over a bounded sample (the last e2e window's params when the e2e
-    leg ran, else the first layers), plus the bit-exact comparison of its
-    outputs with the GPU e2e leg's D2H bytes for the same params."""
+    cores over the bounded sample ``cpu_names`` (the same params the
+    reference arm times: the first layers, sample_params), strict and
+    non-strict, 1 thread and all threads; plus the bit-exact comparison of
+    its outputs with the GPU e2e leg's D2H bytes for the same params, and
+    the reference's file pipeline on tmpfs (file_leg)."""
     if host_cpu_frags is None:
-        cpu_names = sample_params(spec, 3e9)
         host_cpu_frags = oracle_frags(spec, src, cpu_names, args.cpu_threads)
     S_cpu = sum(12 * spec.param(n).numel for n in cpu_names)
     arm = CpuArm(spec, src, tgt, host_cpu_frags)
     ref_out: dict = {}
     t_cpu = arm.run(args.cpu_threads, ref_out)
     t_cpu1 = arm.run(1)
+    t_ns = arm.run(args.cpu_threads, strict=False)
     parity_cpu = None
     if gpu_index:
         hv = host_tgt.numpy()
@@ -401,15 +647,96 @@ def cpu_leg(args, spec, src, tgt, host_cpu_frags, cpu_names, gpu_index, host_tgt
     what = ("ucp.union + ucp.parallel.extract_fragment from baseline/_ref (unmodified "
             "reference)" if arm.kind == "reference" else "oracle union + extract_fragment")
     cpu = {"value": S_cpu / t_cpu / GB, "unit": "GB/s", "cores": args.cpu_threads,
-           "value_1_thread": S_cpu / t_cpu1 / GB, "kind": arm.kind,
-           "sample": f"{len(cpu_names)} params ({cpu_names[0]} .. {cpu_names[-1]}), "
-                     f"{S_cpu / GB:.2f} GB state: {what} "
-                     f"(materialised), {args.cpu_threads} threads, one pass",
+           "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count(),
+           "value_1_thread": S_cpu / t_cpu1 / GB, "value_non_strict": S_cpu / t_ns / GB,
+           "kind": arm.kind, "sample": sample_desc(cpu_names, S_cpu, what, args.cpu_threads),
            "parity_vs_gpu": parity_cpu}
     if arm.kind == "reference":
         cpu["port_value"] = S_cpu / CpuArm(spec, src, tgt, host_cpu_frags, False).run(
             args.cpu_threads) / GB
+    if not args.no_file_leg:
+        try:
+            cpu["file_pipeline_cfg1"] = file_leg(args.cpu_threads)
+        except Exception as exc:  # noqa: BLE001 - e.g. no tmpfs room
+            cpu["file_pipeline_cfg1"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     return cpu
+
+
+def sample_desc(names, S, what, threads) -> str:
+    """The bounded CPU sample, named identically in the reference arm's
+    config and in cpu_baseline."""
+    return (f"{len(names)} params ({names[0]} .. {names[-1]}), {S / GB:.2f} GB state: {what} "
+            f"(materialised), {threads} threads")
+
+
+def exchange_stats(exch, xevs, rank: int, step_ms: float, transport: str) -> dict:
+    """This rank's side of the rank-homed exchange: bytes it sends to other
+    GPUs per step and the all-to-all-v time per step (CUDA events on the
+    comm stream, summed over windows)."""
+    sent = sum(nb for w in range(exch.n_windows) for h, (_, nb) in enumerate(exch.send[w])
+               if h != rank)
+    total = sum(nb for w in range(exch.n_windows) for _, nb in exch.send[w])
+    xms = sum(e[0].elapsed_time(e[1]) for st in xevs for e in st) / max(len(xevs), 1)
+    return {"transport": transport, "bytes_sent": sent, "bytes_total": total, "exchange_ms": xms,
+            "step_ms": step_ms}
+
+
+def exchange_leg(args, spec, src, tgt, mine, plan, dev, wdt, world: int, rank: int, red_dev):
+    """The rank-homed reshard over NCCL next to the param-homed main leg:
+    same params per rank and the same resident source arena (the source
+    layout does not depend on target homes), target rank g homed on GPU
+    g mod N, one all-to-all-v per window through libucp_b200_comm.so.
+    Returns exchange_stats, or None on every rank if any rank could not
+    prepare it (no rank may skip a collective the others enter)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_18820_b200.dist import NcclComm, build_exchange
+    from paper_2406_18820_b200.reshard import ReshardPlan
+
+    hplan = err = None
+    try:
+        exch = build_exchange(spec, src, tgt, world, rank, int(args.window_gb * GB), wdt)
+        hplan = ReshardPlan(spec, src, tgt, params=mine, device=dev, dtype=wdt,
+                            window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024,
+                            fused=not args.unfused, strict=not args.non_strict,
+                            materialize_atomic=not args.no_atomic,
+                            home_of=[g % world for g in range(tgt.world_size)], n_homes=world)
+        if hplan.src_total != plan.src_total:
+            raise RuntimeError("rank-homed source layout differs from the main leg's")
+        hplan._bufs["src_arena"] = plan._bufs["src_arena"]
+        hplan.buf("atom", hplan.max_atom)  # allocate before agreeing to run
+    except Exception as exc:  # noqa: BLE001 - e.g. HBM short at this N
+        err = f"{type(exc).__name__}: {exc}"[:200]
+    ok = torch.tensor([float(err is None)], device=red_dev, dtype=torch.float64)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() < 1:
+        if err:
+            print(f"rank {rank}: exchange leg skipped: {err}", file=sys.stderr)
+        return None
+    comm = NcclComm()
+    stream, cs = torch.cuda.current_stream(dev), torch.cuda.Stream(dev)
+    hplan.status.reset()
+    hplan.step_device_homed(exch, None, stream, cs, None, comm)  # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    steps = max(1, min(args.steps, args.exchange_steps))
+    xevs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)]
+             for _ in range(exch.n_windows)] for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(steps):
+        hplan.step_device_homed(exch, None, stream, cs, None, comm, xevs[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    hplan.check()
+    out = exchange_stats(exch, xevs, rank, t0.elapsed_time(t1) / steps,
+                         "NCCL all-to-all-v (libucp_b200_comm.so: grouped ncclSend/ncclRecv)")
+    comm.close()
+    hplan._bufs.pop("src_arena", None)
+    hplan.free()
+    return out
 
 
 def emit(obj, rank):
@@ -438,8 +765,7 @@ def run_reference(args):
     v = S / t / GB
     what = ("ucp.union + ucp.parallel.extract_fragment from baseline/_ref (unmodified reference)"
             if arm.kind == "reference" else "oracle port of union + extract_fragment")
-    sample = (f"{len(names)} params ({names[0]} .. {names[-1]}), {S / GB:.2f} GB state: {what}, "
-              f"materialised, {args.cpu_threads} threads")
+    sample = sample_desc(names, S, what, args.cpu_threads)
     emit({"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -459,6 +785,12 @@ def run_ours(args):
     from paper_2406_18820_b200.dist import init_process_group, owned_params
     from paper_2406_18820_b200.reshard import ReshardPlan
 
+    if int(os.environ.get("WORLD_SIZE", 1)) > 1 and args.dist_backend == "nccl":
+        # NCCL's communicator log (ranks, transports, NVLS) on stderr: stdout
+        # carries only the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     rank, world, local = init_process_group(args.dist_backend,
                                             force=args.home == "rank" or args.src_home == "rank")
     local = local % torch.cuda.device_count()  # >1 rank per GPU only for gloo smoke tests
@@ -529,8 +861,16 @@ def run_ours(args):
         from paper_2406_18820_b200.dist import NcclComm
 
         ncomm = NcclComm()
+    xevs = None
     if homed and peer is None:
-        step = lambda ev=None: plan.step_device_homed(exch, None, stream, comm_stream, ev, ncomm)
+        xevs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                 for _ in range(exch.n_windows)] for _ in range(args.steps)]
+        xk = iter(range(1 << 30))
+
+        def step(ev=None):
+            # exchange events only on the timed steps (those pass ``ev``)
+            xe = xevs[next(xk)] if ev is not None else None
+            plan.step_device_homed(exch, None, stream, comm_stream, ev, ncomm, xe)
     elif windowed:
         step = lambda ev=None: plan.step_windowed(7, stream, ev)
     else:
@@ -571,16 +911,6 @@ def run_ours(args):
     fused_bytes = sum(plan.fused_bytes.values())
     conv_bytes = plan.bytes["R_c"] + plan.bytes["W_c"]
     load_bytes = plan.bytes["R_l"] + plan.bytes["W_l"]
-    if world > 1:
-        t = torch.tensor([ms_local, float(S_local)], device=red_dev, dtype=torch.float64)
-        mx = t.clone()
-        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-        ms, S = float(mx[0]), float(t[1])
-    else:
-        ms, S = ms_local, float(S_local)
-    value = S / (ms / 1e3) / GB
-
     peak, peak_src = measured_peak()
     stages = {"reshard_fused": (fused_bytes, fused_ms, "fused"),
               "convert_gather": (conv_bytes, conv_ms, "conv"),
@@ -610,32 +940,32 @@ def run_ours(args):
                               "step_hbm_frac": plan.hbm_bytes / (ms_local / 1e3) / GB / peak}}
     gpu_launches = args.steps * plan.n_launches
 
-    # ---- live copy reference in the same process (context for roofline.peak):
-    # torch copy_ of 1 Gi bf16 elements (MEASURED_PEAKS.json's method), best
-    # of 20, read + write bytes
-    plan.free()  # the timed plan's buffers are not needed any more
-    torch.cuda.empty_cache()
-    live = None
-    try:
-        a_ = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
-        b_ = torch.empty_like(a_)
-        best = 1e9
-        for _ in range(20):
-            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            c0.record(stream)
-            b_.copy_(a_)
-            c1.record(stream)
-            torch.cuda.synchronize()
-            best = min(best, c0.elapsed_time(c1))
-        live = 2 * a_.numel() * 2 / (best / 1e3) / GB
-        del a_, b_
+    # ---- the exchange stage (north_star item 3): measured on the main leg
+    # when it is rank-homed; at N > 1 with the default param-homed leg, a
+    # second, rank-homed leg over NCCL shares the resident source arena
+    xstat = None
+    if homed and peer is None:
+        xstat = exchange_stats(exch, xevs, rank, ms_local,
+                               f"all-to-all-v per window ({args.exchange})")
+    elif homed:
+        crossing = sum(nb for w in range(exch.n_windows) for h, (_, nb) in enumerate(exch.send[w])
+                       if h != rank)
+        xstat = {"transport": "peer stores from the reshard kernel (CUDA IPC over NVLink)",
+                 "bytes_sent": crossing, "exchange_ms": fused_ms, "step_ms": ms_local}
+    elif (world > 1 and not windowed and sources is None and not args.no_exchange
+          and args.dist_backend == "nccl"):
+        for k in ("atom", "tgt0", "tgt1"):
+            plan._bufs.pop(k, None)
         torch.cuda.empty_cache()
-    except RuntimeError:
-        live = None
-    roofline["live_copy_GBps_same_run"] = live
-    roofline["live_copy_note"] = ("torch copy_ of 2 x 2 GiB in this process right after the timed "
-                                  "region (same clocks / power state); context only, the roofline "
-                                  "denominator is MEASURED_PEAKS.json")
+        xstat = exchange_leg(args, spec, src, tgt, mine, plan, dev, wdt, world, rank, red_dev)
+    plan.free()  # the timed plans' buffers are not needed any more
+    torch.cuda.empty_cache()
+    stats = gather_stats({"ms": ms_local, "S": float(S_local), "hbm_bytes": float(plan.hbm_bytes),
+                          "clocks": clk, "exchange": xstat}, world)
+    agg = aggregate_ranks(stats, peak)
+    ms, S, value = agg["ms"], agg["S"], agg["value"]
+    roofline["aggregate"] = agg["aggregate"]
+    clk = agg["clocks"]
 
     # ---- e2e: host-streamed sample, H2D + kernels + D2H in the timed region
     e2e = None
@@ -673,8 +1003,8 @@ def run_ours(args):
             host_src[:eplan.src_total].copy_(eplan._bufs["src_arena"][:eplan.src_total])
             eplan._bufs.pop("src_arena", None)
             torch.cuda.empty_cache()
-            if rank == 0 and world == 1 and not args.no_cpu:
-                cpu_names = [p.name for p in wins[-1].params]
+            cpu_names = sample_params(spec, 3e9)  # the reference arm's sample too
+            if rank == 0 and world == 1 and not args.no_cpu and set(cpu_names) <= set(names):
                 hv = host_src.numpy()
                 host_cpu_frags = {}
                 for W in eplan.windows:
@@ -722,10 +1052,17 @@ def run_ours(args):
             S_e2e_local = eplan.state_bytes
             e2e_meta = {"h2d": int(eplan.src_total), "d2h": int(eplan.tgt_total),
                         "windows": len(eplan.windows), "names": names}
-            if cpu_names:  # where the GPU wrote the CPU sample's target fragments
+            if host_cpu_frags:  # where the GPU wrote the CPU sample's target fragments
                 gpu_index = {(g, m.param, m.kind): (W.tgt_base + off, n)
                              for W in eplan.windows for g, i, m, off, n, dt in W.tgt_frags
                              if m.param in cpu_names and dt.itemsize == 4}
+            public = None
+            if not args.no_public_e2e and rank == 0:
+                try:
+                    public = public_e2e(spec, src, tgt, names, eplan, host_src, wdt,
+                                        args.e2e_steps)
+                except Exception as exc:  # noqa: BLE001 - reported, not fatal
+                    public = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:300]}
             del eplan
         except Exception as exc:  # the main line must survive a host-memory failure
             e2e_err = f"{type(exc).__name__}: {exc}"[:300]
@@ -755,13 +1092,16 @@ def run_ours(args):
                    "sample": f"{len(names)} params ({names[0]} .. {names[-1]}; "
                              f"{S_e2e_local / GB:.2f} GB state/rank) from pinned host memory: "
                              f"H2D + fused reshard + D2H in {e2e_meta['windows']} double-buffered "
-                             "windows on 3 streams"}
+                             "windows on 3 streams",
+                   "public_reshard": public}
         else:
             e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0, "error": e2e_err or "failed on another rank"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if cpu_names is None:
+        cpu_names = sample_params(spec, 3e9)
+    if rank == 0 and not args.no_cpu:
         try:
             cpu = cpu_leg(args, spec, src, tgt, host_cpu_frags, cpu_names, gpu_index,
                           host_tgt if gpu_index else None)
@@ -800,7 +1140,13 @@ def run_ours(args):
                                      else "staged on the param-owner GPU"),
                      "atomic_materialised": not args.no_atomic},
           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+          "exchange": agg.get("exchange"),
+          "nccl_debug": ({k: os.environ.get(k) for k in ("NCCL_DEBUG", "NCCL_DEBUG_SUBSYS",
+                                                          "NCCL_DEBUG_FILE")}
+                         if world > 1 and args.dist_backend == "nccl" else None),
           "gpu_launches": gpu_launches, "parity": parity}, rank)
+    if world > 1:
+        dist.barrier()  # rank 0's CPU leg ran while the others waited here
     if peer is not None:
         if world > 1:
             dist.barrier()

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define UCP_ABI_VERSION 2
+#define UCP_ABI_VERSION 3
 
 /* status / return codes (mirrored in paper_2406_18820_b200/_errors.py) */
 #define UCP_OK 0
@@ -69,8 +69,9 @@ extern "C" {
 #define UCP_CLASS_VEC_F32 0   /* COPY, UCP_RUN_VEC, f32 destinations */
 #define UCP_CLASS_VEC_BF16 1  /* COPY, UCP_RUN_VEC, bf16 destinations */
 #define UCP_CLASS_VEC_F16 2   /* COPY, UCP_RUN_VEC, f16 destinations */
-#define UCP_CLASS_GENERAL 3   /* everything else (MEAN/NOISE/ZERO/CHECKZERO, scalar runs) */
-#define UCP_NCLASS 4
+#define UCP_CLASS_GENERAL 3   /* COPY runs whose pieces do not share one 16-B phase (realigned) */
+#define UCP_CLASS_OPS 4       /* MEAN / NOISE / ZERO / CHECKZERO (move tables only) */
+#define UCP_NCLASS 5
 
 /* run flags */
 #define UCP_RUN_VEC 1u       /* every src/dst row start shares one 16-B phase */

@@ -23,7 +23,7 @@ EXPORTS = ("ucp_version", "ucp_build_id", "ucp_status_reset", "ucp_runtile_scan"
            "ucp_load_scatter",
            "ucp_reshard_fused", "ucp_gen_state", "ucp_adam_step", "ucp_compare", "ucp_peek",
            "ucp_dev_alloc", "ucp_dev_free", "ucp_ipc_export", "ucp_ipc_open", "ucp_ipc_close")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lib = None
 

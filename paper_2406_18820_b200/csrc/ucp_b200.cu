@@ -34,6 +34,12 @@ namespace {
 #ifndef UCP_VEC
 #define UCP_VEC 4
 #endif
+#ifndef UCP_SCALAR_MINB
+#define UCP_SCALAR_MINB 3  // CTAs per SM of the realigning kernels (80 registers: no spills; 4 spills)
+#endif
+#ifndef UCP_OPS_MINB
+#define UCP_OPS_MINB 2  // CTAs per SM of the MEAN / NOISE / ZERO / CHECKZERO kernels (f64 accumulators)
+#endif
 #ifndef UCP_PERSISTENT
 #define UCP_PERSISTENT 0  // 1: fused kernel runs 148*UCP_MINB persistent CTAs over the tiles
 #endif
@@ -281,31 +287,83 @@ __device__ __forceinline__ void report(bool bad, uint32_t elem, uint32_t run_idx
   }
 }
 
-// COPY with replica verification, fan-out and cast, U slots of W elements.
-// e[u] = element offset inside the row segment; srow/drow = element index of
-// the segment start in source/destination coordinates.
-template <int W, int U>
-__device__ __forceinline__ void copy_general(const Ctx& c, uint64_t srow, uint64_t drow,
-                                             const uint32_t (&e)[U], const bool (&ok)[U],
-                                             uint32_t ebase, ucp_status* st) {
+// MEAN / NOISE / ZERO / CHECKZERO (the OPS class: Partial vectors, pads),
+// one instantiation per op. Every slot's source vector of a group is in
+// flight before any is used (U loads per lane per replica), like the copy
+// path: a group-at-a-time, slot-at-a-time loop left one load in flight and
+// ran at ~0.14 of the HBM peak (r02a kernel zoo). The f64 accumulation order
+// is the reference's: ascending group, __dadd_rn, one __ddiv_rn, RNE to f32.
+template <int W, int U, int OP>
+__device__ __forceinline__ void op_run(const Ctx& c, uint64_t srow, uint64_t drow,
+                                    const uint32_t (&e)[U], const bool (&ok)[U], uint32_t ebase,
+                                    ucp_status* st) {
   const ucp_run& r = *c.r;
   const int esz = r.dtype == UCP_DT_F32 ? 4 : 2;
-  Lanes<W> v[U];
+  const int G = OP == UCP_OP_MEAN ? (r.groups > 0 ? r.groups : 1) : 1;
+  const int K = r.n_src > 0 ? r.n_src / G : 0;
   bool bad = false;
   uint32_t bad_e = 0xffffffffu;
-  const char* s0 = c.sb + r.src + 4 * srow;
+  Lanes<W> v[U];
+  double acc[OP == UCP_OP_MEAN ? U : 1][W];
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (ok[u]) load_w<W>(v[u], s0 + 4ull * e[u]);
-  for (int k = 1; k < r.n_src; ++k) {
-    const char* sk = c.sb + src_off(c, k) + 4 * srow;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!ok[u]) continue;
-      Lanes<W> w;
-      load_w<W>(w, sk + 4ull * e[u]);
-      const int d = first_diff<W>(v[u], w);
-      if (d < W) { bad = true; bad_e = min(bad_e, e[u] + d); }
+    for (int i = 0; i < W; ++i) v[u].v[i] = 0.0f;
+  if constexpr (OP != UCP_OP_ZERO) {
+    // groups in chunks of GC: every (group, slot) vector of a replica is in
+    // flight at once; accumulation stays in ascending group order
+    constexpr int GC = OP == UCP_OP_MEAN ? 4 : 1;
+    for (int g0 = 0; g0 < G; g0 += GC) {
+      Lanes<W> p[GC][U];
+      for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int j = 0; j < GC; ++j) {
+          if (g0 + j >= G) continue;
+          const char* sk = c.sb + src_off(c, (g0 + j) * K + k) + 4 * srow;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            if (k == 0) {
+              load_w<W>(p[j][u], sk + 4ull * e[u]);
+            } else {
+              Lanes<W> w;
+              load_w<W>(w, sk + 4ull * e[u]);
+              const int d = first_diff<W>(p[j][u], w);
+              if (d < W) { bad = true; bad_e = min(bad_e, e[u] + d); }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < GC; ++j) {
+        if (g0 + j >= G) continue;
+        if constexpr (OP == UCP_OP_MEAN) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+              acc[u][i] = g0 + j == 0 ? (double)p[j][u].v[i]
+                                      : __dadd_rn(acc[u][i], (double)p[j][u].v[i]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = p[j][u];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!ok[u]) continue;
+    if constexpr (OP == UCP_OP_MEAN) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) v[u].v[i] = __double2float_rn(__ddiv_rn(acc[u][i], (double)G));
+    } else if constexpr (OP == UCP_OP_NOISE) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) v[u].v[i] = noise1(v[u].v[i], r.tp_rank, r.tp);
+    } else if constexpr (OP == UCP_OP_CHECKZERO) {
+#pragma unroll
+      for (int i = 0; i < W; ++i)
+        if (bits_of(v[u].v[i]) != 0u) { bad = true; bad_e = min(bad_e, e[u] + i); }
     }
   }
   for (int d = 0; d < r.n_dst; ++d) {
@@ -317,65 +375,15 @@ __device__ __forceinline__ void copy_general(const Ctx& c, uint64_t srow, uint64
   report(bad, ebase + bad_e, c.run_idx, st);
 }
 
-// MEAN / NOISE / ZERO / CHECKZERO (tiny by bytes: Partial vectors, pads);
-// one slot at a time to keep register pressure off the copy paths.
-template <int W, int U>
-__device__ __noinline__ void op_general(const Ctx& c, uint64_t srow, uint64_t drow,
-                                        const uint32_t (&e)[U], const bool (&ok)[U],
-                                        uint32_t ebase, ucp_status* st) {
-  const ucp_run& r = *c.r;
-  const int op = r.op;
-  const int esz = r.dtype == UCP_DT_F32 ? 4 : 2;
-  const int G = r.groups > 0 ? r.groups : 1;
-  const int K = r.n_src > 0 ? r.n_src / G : 0;
-  bool bad = false;
-  uint32_t bad_e = 0xffffffffu;
-  for (int u = 0; u < U; ++u) {
-    if (!ok[u]) continue;
-    Lanes<W> v;
-#pragma unroll
-    for (int i = 0; i < W; ++i) v.v[i] = 0.0f;
-    double acc[W];
-    for (int g = 0; g < (op == UCP_OP_MEAN ? G : (r.n_src > 0 ? 1 : 0)); ++g) {
-      Lanes<W> p;
-      load_w<W>(p, c.sb + src_off(c, g * K) + 4 * (srow + e[u]));
-      for (int k = 1; k < K; ++k) {
-        Lanes<W> w;
-        load_w<W>(w, c.sb + src_off(c, g * K + k) + 4 * (srow + e[u]));
-        const int d = first_diff<W>(p, w);
-        if (d < W) { bad = true; bad_e = min(bad_e, e[u] + d); }
-      }
-#pragma unroll
-      for (int i = 0; i < W; ++i)
-        acc[i] = g == 0 ? (double)p.v[i] : __dadd_rn(acc[i], (double)p.v[i]);
-      if (g == 0) v = p;
-    }
-    if (op == UCP_OP_MEAN) {
-#pragma unroll
-      for (int i = 0; i < W; ++i) v.v[i] = __double2float_rn(__ddiv_rn(acc[i], (double)G));
-    } else if (op == UCP_OP_NOISE) {
-#pragma unroll
-      for (int i = 0; i < W; ++i) v.v[i] = noise1(v.v[i], r.tp_rank, r.tp);
-    } else if (op == UCP_OP_CHECKZERO) {
-#pragma unroll
-      for (int i = 0; i < W; ++i)
-        if (bits_of(v.v[i]) != 0u) { bad = true; bad_e = min(bad_e, e[u] + i); }
-    }
-    for (int d = 0; d < r.n_dst; ++d)
-      store_w<W>(c.db + dst_off(c, d) + (uint64_t)esz * (drow + e[u]), v, r.dtype);
-  }
-  report(bad, ebase + bad_e, c.run_idx, st);
-}
-
-template <int W, int U>
+template <int OP, int W, int U>
 __device__ __forceinline__ void general(const Ctx& c, uint64_t srow, uint64_t drow,
                                         const uint32_t (&e)[U], const bool (&ok)[U],
                                         uint32_t ebase, ucp_status* st) {
-  if (c.r->op == UCP_OP_COPY) copy_general<W, U>(c, srow, drow, e, ok, ebase, st);
-  else op_general<W, U>(c, srow, drow, e, ok, ebase, st);
+  op_run<W, U, OP>(c, srow, drow, e, ok, ebase, st);
 }
 
-// One warp processes columns [cs, cs+len) of one row (general kernel).
+// One warp processes columns [cs, cs+len) of one row (OPS kernels).
+template <int OP>
 __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs, uint32_t len,
                                         ucp_status* st) {
   const ucp_run& r = *c.r;
@@ -392,17 +400,20 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
     if (head > len) head = len;
     const uint32_t nvec = (len - head) >> 2;
     const uint32_t tail = len - head - 4 * nvec;
-    // vector body: slot u of lane -> vector lane + 32u
-    {
-      uint32_t e[kVec];
-      bool ok[kVec];
+    // vector body: slot u of lane -> vector lane + 32u (MEAN: two passes of
+    // half the slots, its f64 accumulators would not fit the registers)
+    constexpr int UH = OP == UCP_OP_MEAN ? kVec / 2 : kVec;
 #pragma unroll
-      for (int u = 0; u < kVec; ++u) {
-        const uint32_t vi = lane + 32u * u;
+    for (int h = 0; h < kVec / UH; ++h) {
+      uint32_t e[UH];
+      bool ok[UH];
+#pragma unroll
+      for (int u = 0; u < UH; ++u) {
+        const uint32_t vi = lane + 32u * (h * UH + u);
         ok[u] = vi < nvec;
         e[u] = head + 4u * vi;
       }
-      general<4, kVec>(c, srow, drow, e, ok, ebase, st);
+      general<OP, 4, UH>(c, srow, drow, e, ok, ebase, st);
     }
     // scalar head + tail (<= 6 elements)
     if (head + tail > 0) {
@@ -411,10 +422,10 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
       const uint32_t l = (uint32_t)lane;
       ok1[0] = l < head + tail;
       e1[0] = l < head ? l : head + 4 * nvec + (l - head);
-      general<1, 1>(c, srow, drow, e1, ok1, ebase, st);
+      general<OP, 1, 1>(c, srow, drow, e1, ok1, ebase, st);
     }
   } else {
-    constexpr int U = 8;
+    constexpr int U = OP == UCP_OP_MEAN ? 4 : 8;
     for (uint32_t base = 0; base < len; base += 32u * U) {
       uint32_t e[U];
       bool ok[U];
@@ -423,7 +434,7 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
         e[u] = base + lane + 32u * u;
         ok[u] = e[u] < len;
       }
-      general<1, U>(c, srow, drow, e, ok, ebase, st);
+      general<OP, 1, U>(c, srow, drow, e, ok, ebase, st);
     }
   }
 }
@@ -761,14 +772,123 @@ __device__ __forceinline__ void stage_out(char* p, const float* buf, int off, ui
   }
 }
 
-// ---------------------------------------------------------------- general kernel
+// ---------------------------------------------------------------- realigning kernels
 //
-// Everything else: MEAN / NOISE / ZERO / CHECKZERO runs and phase-mismatched
-// runs (scalar path). Tiny by bytes (Partial vectors, pads, dp=3 cells).
+// COPY pieces whose sources and destinations do not share one 16-B phase
+// (ZeRO partitions of dp = 3, 5, ... start at k * ceil(n / dp) elements).
+// Each warp moves a row segment at vector width with no shared memory:
+//  * every lane loads aligned 16-B vectors on the primary's phase grid
+//    (lane l, slot u: source vector I = l + 32u; a 512-element segment spans
+//    <= 129 vectors, so kRU = 5 slots);
+//  * replicas on the same grid are loaded the same way and compared in
+//    registers;
+//  * a lane's right neighbour vector I + 1 comes from one round of warp
+//    shuffles (lane 31 takes lane 0's next slot);
+//  * destination d with phase pd writes its aligned vector J = I + kappa as
+//    funnel(v_I, v_I+1, (ps - pd) & 3), plus <= 3 head and <= 3 tail scalars.
+// The former shared-memory staging (stage_in / stage_out: an STS.128 per
+// replica vector and 4 scalar LDS per destination vector) stays as the
+// fallback for runs whose replicas sit on different phase grids.
+constexpr int kRU = (kSeg / 4 + 1 + 31) / 32;
 
-// Phase-mismatched COPY runs of the unfused path, staged through shared
-// memory like the fused cells (fused_tile_staged): aligned 16-B loads on
-// each replica's phase grid, aligned stores on each destination's.
+__device__ __forceinline__ float4 funnel4(const float4& a, const float4& b, uint32_t d) {
+  switch (d) {
+    case 0: return a;
+    case 1: return make_float4(a.y, a.z, a.w, b.x);
+    case 2: return make_float4(a.z, a.w, b.x, b.y);
+    default: return make_float4(a.w, b.x, b.y, b.z);
+  }
+}
+
+// Store segment elements [0, len) to p (element 0's address) from the
+// source-grid vectors v of phase ps; a lane's right neighbour vector comes
+// from one warp shuffle round per slot (lane 31 takes lane 0's next slot);
+// sp = the primary's element 0 (head / tail scalars re-read, L2 hits).
+template <int DT>
+__device__ __forceinline__ void realign_store(char* p, const float4 (&v)[kRU], uint32_t ps,
+                                              uint32_t len, uint32_t lane, const char* sp) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  const uintptr_t da = reinterpret_cast<uintptr_t>(p);
+  const uint32_t pd = (uint32_t)((da / ESZ) & 3);
+  const uint32_t delta = (ps - pd) & 3u;
+  const int kappa = ps >= pd ? 0 : 1;  // destination vector J = source vector I + kappa
+  char* dv = p - (size_t)ESZ * pd;     // aligned destination vector 0
+  const int J0 = pd ? 1 : 0;
+  const int J1 = (int)((len + pd) >> 2) - 1;
+  const int from = (int)((lane + 1) & 31);
+#pragma unroll
+  for (int u = 0; u < kRU; ++u) {
+    const float4 give = (lane == 0 && u + 1 < kRU) ? v[u + 1] : v[u];
+    float4 nx;
+    nx.x = __shfl_sync(0xffffffffu, give.x, from);
+    nx.y = __shfl_sync(0xffffffffu, give.y, from);
+    nx.z = __shfl_sync(0xffffffffu, give.z, from);
+    nx.w = __shfl_sync(0xffffffffu, give.w, from);
+    const int J = (int)(lane + 32u * u) + kappa;
+    if (J >= J0 && J <= J1) store4<DT>(dv + (size_t)ESZ * 4 * J, funnel4(v[u], nx, delta));
+  }
+  const uint32_t head_end = min(4u * (uint32_t)J0 - pd, len);
+  uint32_t tail_start = J1 >= J0 ? 4u * (uint32_t)(J1 + 1) - pd : head_end;
+  if (tail_start < head_end) tail_start = head_end;
+  if (lane < head_end + (len - tail_start)) {
+    const uint32_t e = lane < head_end ? lane : tail_start + (lane - head_end);
+    store1<DT>(p + (size_t)ESZ * e, ld_stream1(sp + 4ull * e));
+  }
+}
+
+// One row segment [0, len): sources at sb + src_k + soff (src_0 = s0, src_k
+// = s_aux[k - 1]; all on the primary's 16-B grid), optional f32 atom at
+// ab + aoff, destinations at db + dst_d + doff (dst_0 = d0, dst_d =
+// s_aux[ns - 1 + d - 1]).
+template <int DT>
+__device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uint64_t s0,
+                                                const uint64_t* s_aux, int ns, uint64_t soff,
+                                                char* __restrict__ ab, uint64_t aoff, bool atom_on,
+                                                char* __restrict__ db, uint64_t d0, int nd,
+                                                uint64_t doff, uint32_t len, uint32_t lane,
+                                                bool& bad, uint32_t& bad_e) {
+  const char* sp = sb + s0 + soff;
+  const uint32_t ps = (uint32_t)((reinterpret_cast<uintptr_t>(sp) >> 2) & 3);
+  const uint32_t nsv = (ps + len + 3) >> 2;
+  float4 v[kRU];
+#pragma unroll
+  for (int u = 0; u < kRU; ++u) {
+    const uint32_t I = lane + 32u * u;
+    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (I < nsv) v[u] = ld_stream4(sp - 4 * ps + 16ull * I);
+  }
+  for (int k = 1; k < ns; ++k) {
+    const char* rp = sb + s_aux[k - 1] + soff - 4 * ps;
+#pragma unroll
+    for (int u = 0; u < kRU; ++u) {
+      const uint32_t I = lane + 32u * u;
+      if (I >= nsv) continue;
+      const float4 w = ld_stream4(rp + 16ull * I);
+      // first differing element of this vector inside [0, len)
+      const uint32_t x[4] = {bits_of(v[u].x) ^ bits_of(w.x), bits_of(v[u].y) ^ bits_of(w.y),
+                             bits_of(v[u].z) ^ bits_of(w.z), bits_of(v[u].w) ^ bits_of(w.w)};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = 4 * (int)I - (int)ps + c;
+        if (x[c] && e >= 0 && e < (int)len) { bad = true; bad_e = min(bad_e, (uint32_t)e); }
+      }
+    }
+  }
+  if (atom_on) realign_store<UCP_DT_F32>(ab + aoff, v, ps, len, lane, sp);
+  for (int d = 0; d < nd; ++d)
+    realign_store<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + doff, v, ps, len, lane, sp);
+}
+
+// every replica of the run on the primary's 16-B grid (the realign path)
+__device__ __forceinline__ bool replicas_on_grid(uint64_t s0, const uint64_t* s_aux, int ns) {
+  bool same = true;
+  for (int k = 1; k < ns; ++k) same &= ((s_aux[k - 1] - s0) & 15) == 0;
+  return same;
+}
+
+// Phase-mismatched COPY runs of the unfused path whose replicas do not share
+// one grid: staged through shared memory (aligned 16-B loads on each
+// replica's phase grid, aligned stores on each destination's).
 template <int DT>
 __device__ __noinline__ void move_tile_staged(const TileGeom& g, const ucp_run& r,
                                               const uint64_t* s_aux, const char* __restrict__ sb,
@@ -805,7 +925,29 @@ __device__ __noinline__ void move_tile_staged(const TileGeom& g, const ucp_run& 
   }
 }
 
-__device__ __forceinline__ void general_body(const ucp_run* __restrict__ runs,
+template <int DT>
+__device__ __forceinline__ void move_tile_realign(const TileGeom& g, const ucp_run& r,
+                                               const uint64_t* s_aux, const char* __restrict__ sb,
+                                               char* __restrict__ db, uint32_t run_idx,
+                                               ucp_status* st) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
+    const uint32_t rr = it / g.spr;
+    const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, g.col0 + g.nc) - cs;
+    const uint32_t row = g.row0 + rr;
+    bool bad = false;
+    uint32_t bad_e = 0xffffffffu;
+    realign_segment<DT>(sb, r.src, s_aux, r.n_src, 4ull * ((uint64_t)row * r.src_pitch + cs),
+                        nullptr, 0, false, db, r.dst, r.n_dst,
+                        (uint64_t)ESZ * ((uint64_t)row * r.dst_pitch + cs), len, lane, bad, bad_e);
+    report(bad, row * r.cols + cs + bad_e, run_idx, st);
+  }
+}
+
+// UCP_CLASS_GENERAL of the move tables: phase-mismatched COPY runs.
+__device__ __forceinline__ void realign_body(const ucp_run* __restrict__ runs,
                                              const uint64_t* __restrict__ aux,
                                              const ucp_runtile* __restrict__ rt, uint32_t r0,
                                              uint32_t nr, const char* __restrict__ sb,
@@ -813,25 +955,53 @@ __device__ __forceinline__ void general_body(const ucp_run* __restrict__ runs,
   __shared__ __align__(16) ucp_run s_run;
   __shared__ uint4 s_t;
   __shared__ uint64_t s_aux[kMaxAux];
+  __shared__ __align__(16) float s_stage[kWarps * 2 * kStage];
   const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
   const TileGeom g = tile_prologue(aux, tile, s_run, s_aux);
-#if UCP_STAGED
-  __shared__ __align__(16) float s_stage[kWarps * 2 * kStage];
-  if (s_run.op == UCP_OP_COPY && !(s_run.flags & UCP_RUN_VEC) && s_run.n_src >= 1 &&
-      s_run.n_src + s_run.n_dst - 2 < kMaxAux) {
+  if (replicas_on_grid(s_run.src, s_aux, s_run.n_src)) {
+    if (s_run.dtype == UCP_DT_F32) move_tile_realign<UCP_DT_F32>(g, s_run, s_aux, sb, db, tile.run, st);
+    else if (s_run.dtype == UCP_DT_BF16) move_tile_realign<UCP_DT_BF16>(g, s_run, s_aux, sb, db, tile.run, st);
+    else move_tile_realign<UCP_DT_F16>(g, s_run, s_aux, sb, db, tile.run, st);
+  } else {
     if (s_run.dtype == UCP_DT_F32) move_tile_staged<UCP_DT_F32>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
     else if (s_run.dtype == UCP_DT_BF16) move_tile_staged<UCP_DT_BF16>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
     else move_tile_staged<UCP_DT_F16>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
-    return;
   }
-#endif
-  const Ctx c{&s_run, s_aux, sb, db, tile.run};
+}
+
+// ---------------------------------------------------------------- ops kernels
+
+template <int OP>
+__device__ __noinline__ void ops_tile(const Ctx& c, const TileGeom g, ucp_status* st) {
   const uint32_t warp = threadIdx.x >> 5;
   for (uint32_t it = warp; it < g.n_items; it += kWarps) {
     const uint32_t rr = it / g.spr;
     const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
     const uint32_t ce = min(cs + kSeg, g.col0 + g.nc);
-    segment(c, g.row0 + rr, cs, ce - cs, st);
+    segment<OP>(c, g.row0 + rr, cs, ce - cs, st);
+  }
+}
+
+//
+// UCP_CLASS_OPS: MEAN / NOISE / ZERO / CHECKZERO runs (Partial vectors, ZeRO
+// pads). Tiny by bytes in every BASELINE config; vector loads when the run
+// shares one 16-B phase, coalesced 4-B ones otherwise.
+__device__ __forceinline__ void ops_body(const ucp_run* __restrict__ runs,
+                                         const uint64_t* __restrict__ aux,
+                                         const ucp_runtile* __restrict__ rt, uint32_t r0,
+                                         uint32_t nr, const char* __restrict__ sb,
+                                         char* __restrict__ db, ucp_status* st) {
+  __shared__ __align__(16) ucp_run s_run;
+  __shared__ uint4 s_t;
+  __shared__ uint64_t s_aux[kMaxAux];
+  const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
+  const TileGeom g = tile_prologue(aux, tile, s_run, s_aux);
+  const Ctx c{&s_run, s_aux, sb, db, tile.run};
+  switch (s_run.op) {  // one op per run, so per tile
+    case UCP_OP_MEAN: ops_tile<UCP_OP_MEAN>(c, g, st); break;
+    case UCP_OP_NOISE: ops_tile<UCP_OP_NOISE>(c, g, st); break;
+    case UCP_OP_ZERO: ops_tile<UCP_OP_ZERO>(c, g, st); break;
+    default: ops_tile<UCP_OP_CHECKZERO>(c, g, st); break;
   }
 }
 
@@ -1208,11 +1378,12 @@ __device__ __noinline__ void fused_tile_staged(const uint64_t* __restrict__ aux,
                                                   const ucp_tile& tile, const ucp_xrun& s_run,
                                                   uint64_t* s_aux, const char* __restrict__ sb,
                                                   char* __restrict__ ab, char* __restrict__ db,
-                                                  ucp_status* st, float* sbuf) {
+                                                  ucp_status* st, float* sbuf,
+                                                  bool preloaded = false) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   const int ns = s_run.n_src, nd = s_run.n_dst;
   const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
-  if (n_aux > 0) {
+  if (n_aux > 0 && !preloaded) {
     for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
     __syncthreads();
   }
@@ -1253,12 +1424,43 @@ __device__ __noinline__ void fused_tile_staged(const uint64_t* __restrict__ aux,
   }
 }
 
-// The GENERAL class of fused tables: phase-mismatched cells; each CTA
-// dispatches on its run's target dtype.
-#ifndef UCP_SCALAR_MINB
-#define UCP_SCALAR_MINB 4  // CTAs per SM of the staged kernel (2 / 3 / 4 measured equal within 2 %)
+template <int DT>
+__device__ __forceinline__ void fused_tile_realign(const uint64_t* __restrict__ aux,
+                                                const ucp_tile& tile, const ucp_xrun& s_run,
+                                                uint64_t* s_aux, const char* __restrict__ sb,
+                                                char* __restrict__ ab, char* __restrict__ db,
+                                                ucp_status* st) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  uint32_t nrows, nc;
+  if (s_run.flags & UCP_RUN_ROWSPLIT) { nrows = 1; nc = tile.count; }
+  else { nrows = tile.count; nc = s_run.cols; }
+  const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nrows * spr;
+  const bool atom_on = s_run.atom != ~0ull;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t it = warp; it < n_items; it += kWarps) {
+    const uint32_t rr = it / spr;
+    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
+    const uint32_t row = tile.row0 + rr;
+    bool bad = false;
+    uint32_t bad_e = 0xffffffffu;
+    realign_segment<DT>(sb, s_run.src, s_aux, s_run.n_src,
+                        4ull * ((uint64_t)row * s_run.src_pitch + cs), ab,
+                        atom_on ? s_run.atom + 4ull * ((uint64_t)row * s_run.atom_pitch + cs) : 0,
+                        atom_on, db, s_run.dst, s_run.n_dst,
+                        (uint64_t)ESZ * ((uint64_t)row * s_run.dst_pitch + cs), len, lane, bad,
+                        bad_e);
+    report(bad, row * s_run.cols + cs + bad_e, tile.run, st);
+  }
+}
+
+// The GENERAL class of fused tables: phase-mismatched cells, realigned in
+// registers (shared-memory staging when replicas sit on different 16-B
+// grids); each CTA dispatches on its run's target dtype.
+#ifndef UCP_REALIGN
+#define UCP_REALIGN 1  // 0: phase-mismatched fused cells always take the shared-memory staging
 #endif
-__global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) reshard_fused_scalar(UCP_FUSED_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) reshard_fused_realign(UCP_FUSED_ARGS) {
   (void)n_tiles;
   __shared__ __align__(16) ucp_xrun s_run;
   __shared__ uint4 s_t;
@@ -1268,9 +1470,23 @@ __global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) reshard_fused_scala
 #endif
   const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
 #if UCP_STAGED
-  if (s_run.dtype == UCP_DT_F32) fused_tile_staged<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage);
-  else if (s_run.dtype == UCP_DT_BF16) fused_tile_staged<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage);
-  else fused_tile_staged<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage);
+  {
+    const int ns = s_run.n_src, nd = s_run.n_dst;
+    const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
+    for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
+    __syncthreads();
+  }
+  if (UCP_REALIGN && replicas_on_grid(s_run.src, s_aux, s_run.n_src)) {
+    if (s_run.dtype == UCP_DT_F32) fused_tile_realign<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st);
+    else if (s_run.dtype == UCP_DT_BF16) fused_tile_realign<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st);
+    else fused_tile_realign<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st);
+  } else if (s_run.dtype == UCP_DT_F32) {
+    fused_tile_staged<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage, true);
+  } else if (s_run.dtype == UCP_DT_BF16) {
+    fused_tile_staged<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage, true);
+  } else {
+    fused_tile_staged<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage, true);
+  }
 #else
   if (s_run.dtype == UCP_DT_F32) fused_tile_scalar<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st);
   else if (s_run.dtype == UCP_DT_BF16) fused_tile_scalar<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st);
@@ -1300,11 +1516,17 @@ __global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_bf16(UCP_MOVE
 __global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_f16(UCP_MOVE_ARGS) {
   vec_body<UCP_DT_F16>(runs, aux, rt, r0, nr, sb, db, st);
 }
-__global__ void __launch_bounds__(kThreads) convert_gather_general(UCP_MOVE_ARGS) {
-  general_body(runs, aux, rt, r0, nr, sb, db, st);
+__global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) convert_gather_realign(UCP_MOVE_ARGS) {
+  realign_body(runs, aux, rt, r0, nr, sb, db, st);
 }
-__global__ void __launch_bounds__(kThreads) load_scatter_general(UCP_MOVE_ARGS) {
-  general_body(runs, aux, rt, r0, nr, sb, db, st);
+__global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) load_scatter_realign(UCP_MOVE_ARGS) {
+  realign_body(runs, aux, rt, r0, nr, sb, db, st);
+}
+__global__ void __launch_bounds__(kThreads, UCP_OPS_MINB) convert_gather_ops(UCP_MOVE_ARGS) {
+  ops_body(runs, aux, rt, r0, nr, sb, db, st);
+}
+__global__ void __launch_bounds__(kThreads, UCP_OPS_MINB) load_scatter_ops(UCP_MOVE_ARGS) {
+  ops_body(runs, aux, rt, r0, nr, sb, db, st);
 }
 
 // ---------------------------------------------------------------- generator
@@ -1401,7 +1623,9 @@ int launch_move(bool gather, const ucp_run* runs, int64_t n_runs, const uint64_t
   ClassRange cr;
   uint32_t nt[UCP_NCLASS];
   if (!parse_classes(class_info, n_runs, cr, nt)) return UCP_EINVAL;
-  if (nt[0] + nt[1] + nt[2] + nt[3] == 0) return UCP_OK;
+  uint32_t all = 0;
+  for (int c = 0; c < UCP_NCLASS; ++c) all += nt[c];
+  if (all == 0) return UCP_OK;
   if (!runs || !rt || !status) return UCP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const char* sb = static_cast<const char*>(src_base);
@@ -1413,7 +1637,8 @@ int launch_move(bool gather, const ucp_run* runs, int64_t n_runs, const uint64_t
     if (gather) {
       switch (c) {
         case UCP_CLASS_VEC_F32: convert_gather_f32<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
-        case UCP_CLASS_GENERAL: convert_gather_general<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
+        case UCP_CLASS_GENERAL: convert_gather_realign<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
+        case UCP_CLASS_OPS: convert_gather_ops<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
         default: return UCP_EINVAL;  // convert writes f32 atomics only
       }
     } else {
@@ -1421,7 +1646,8 @@ int launch_move(bool gather, const ucp_run* runs, int64_t n_runs, const uint64_t
         case UCP_CLASS_VEC_F32: load_scatter_f32<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
         case UCP_CLASS_VEC_BF16: load_scatter_bf16<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
         case UCP_CLASS_VEC_F16: load_scatter_f16<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
-        default: load_scatter_general<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
+        case UCP_CLASS_GENERAL: load_scatter_realign<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
+        default: load_scatter_ops<<<grid, block, 0, s>>>(runs, aux, rt, r0, nr, sb, db, status); break;
       }
     }
   }
@@ -1490,6 +1716,7 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
   ClassRange cr;
   uint32_t nt[UCP_NCLASS];
   if (!parse_classes(class_info, n_runs, cr, nt)) return UCP_EINVAL;
+  if (nt[UCP_CLASS_OPS] != 0) return UCP_EINVAL;  // fused tables hold COPY cells only
   if (nt[0] + nt[1] + nt[2] + nt[3] == 0) return UCP_OK;
   if (!runs || !rt || !status) return UCP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1500,8 +1727,8 @@ int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
     const uint32_t n = nt[c];
     if (n == 0) continue;
     if (c == UCP_CLASS_GENERAL) {  // fused tables: phase-mismatched cells, scalar path
-      reshard_fused_scalar<<<dim3(n), dim3(kThreads), 0, s>>>(runs, aux, rt, cr.begin[c], cr.n[c], n,
-                                                            sb, ab, db, status);
+      reshard_fused_realign<<<dim3(n), dim3(kThreads), 0, s>>>(runs, aux, rt, cr.begin[c], cr.n[c], n,
+                                                             sb, ab, db, status);
       continue;
     }
 #if UCP_PERSISTENT

@@ -55,8 +55,8 @@ from .spec import DType, ParallelConfig, ParamSpec, RecordMeta
 
 OP_COPY, OP_MEAN, OP_NOISE, OP_ZERO, OP_CHECKZERO = 0, 1, 2, 3, 4
 RUN_VEC, RUN_ROWSPLIT = 1, 2
-CLASS_VEC_F32, CLASS_VEC_BF16, CLASS_VEC_F16, CLASS_GENERAL = 0, 1, 2, 3
-NCLASS = 4
+CLASS_VEC_F32, CLASS_VEC_BF16, CLASS_VEC_F16, CLASS_GENERAL, CLASS_OPS = 0, 1, 2, 3, 4
+NCLASS = 5
 SEG = 512            # elements per warp segment (kSeg in the kernel)
 MAX_AUX = 256        # kMaxAux in the kernel
 MAX_SRC = 64         # sources per run before verify-only continuation runs
@@ -207,12 +207,14 @@ class RunTable:
 
 def run_classes(runs: np.ndarray) -> np.ndarray:
     """Kernel class of each run (UCP_CLASS_* in include/ucp_b200.h): the
-    vector kernels take COPY runs with a shared 16-B phase; everything else
-    goes to the general kernel."""
-    vec = ((runs["flags"] & RUN_VEC) != 0) & (runs["op"] == OP_COPY) & (runs["n_src"] >= 1)
+    vector kernels take COPY runs with a shared 16-B phase, the GENERAL
+    (realigning) kernels the other COPY runs, the OPS kernels MEAN / NOISE /
+    ZERO / CHECKZERO."""
+    copy = (runs["op"] == OP_COPY) & (runs["n_src"] >= 1)
+    vec = ((runs["flags"] & RUN_VEC) != 0) & copy
     by_dt = np.select([runs["dtype"] == DType.F32.value, runs["dtype"] == DType.BF16.value],
                       [CLASS_VEC_F32, CLASS_VEC_BF16], CLASS_VEC_F16)
-    return np.where(vec, by_dt, CLASS_GENERAL).astype(np.int64)
+    return np.select([vec, copy], [by_dt, CLASS_GENERAL], CLASS_OPS).astype(np.int64)
 
 
 def make_runtiles(runs: np.ndarray, tile_bytes: int, extra_bpe=None) -> np.ndarray:

@@ -295,12 +295,14 @@ class ReshardPlan:
                 ev[3].record(stream)
 
     def step_device_homed(self, exch, group=None, stream=None, comm_stream=None,
-                          events=None, comm=None) -> None:
+                          events=None, comm=None, xevents=None) -> None:
         """Rank-homed variant of ``step_device`` (north_star item 3): after
         window w's reshard launches, its target region (ordered by home GPU,
         see ``layout_windows``) is exchanged with one all-to-all-v over NCCL
         on ``comm_stream`` while window w+1 computes. Window w+2 reuses the
-        ring slot only after the exchange of w has drained it."""
+        ring slot only after the exchange of w has drained it. xevents[w]
+        (optional): two CUDA events recorded on ``comm_stream`` around window
+        w's all-to-all-v (the exchange stage's own time)."""
         import torch.distributed as dist
 
         stream = stream or torch.cuda.current_stream(self.device)
@@ -331,8 +333,11 @@ class ReshardPlan:
                 ev[2].record(stream)
                 ev[3].record(stream)
             sizes = [nb for _, nb in exch.send[w]]
+            xev = xevents[w] if xevents is not None and w < len(xevents) else None
             with torch.cuda.stream(comm_stream):
                 comm_stream.wait_event(ready)
+                if xev:
+                    xev[0].record(comm_stream)
                 if comm is not None:  # libucp_b200_comm.so: grouped ncclSend/ncclRecv
                     comm.alltoallv(ring[slot].data_ptr(), sizes, recv[slot].data_ptr(),
                                    exch.recv[w], comm_stream.cuda_stream)
@@ -340,6 +345,8 @@ class ReshardPlan:
                     dist.all_to_all_single(recv[slot][:exch.recv_bytes(w)],
                                            ring[slot][:sum(sizes)], exch.recv[w], sizes,
                                            group=group)
+                if xev:
+                    xev[1].record(comm_stream)
                 fin = torch.cuda.Event()
                 fin.record(comm_stream)
             done[slot] = fin
@@ -407,20 +414,56 @@ class ReshardPlan:
 
     # ------------------------------------------------------------------ host-streamed
 
-    def pack_host(self, shards: dict, pinned: torch.Tensor | None = None) -> torch.Tensor:
-        """Copy {g: [array per source record]} into a pinned source arena."""
-        host = pinned if pinned is not None else pinned_host(self.src_total)
+    def pack_host(self, shards: dict, pinned: torch.Tensor | None = None,
+                  threads: int = 16) -> torch.Tensor:
+        """Copy {g: [array per source record]} into a pinned source arena
+        (the plan's own, reused across calls, unless ``pinned`` is given);
+        the copies run on ``threads`` host threads (numpy releases the GIL)."""
+        from ._errors import ShapeError
+
+        host = pinned if pinned is not None else self._pinned("src", self.src_total)
         hv = host.numpy()
+        jobs = []
         for W in self.windows:
             for g, i, m, off, n in W.src_frags:
                 a = np.ascontiguousarray(shards[g][i], dtype=np.float32).reshape(-1)
                 if a.size != n:
-                    from ._errors import ShapeError
-
                     raise ShapeError(f"rank {g} {m.param}.{m.kind}: {a.size} elements, want {n}")
-                at = W.src_base + off
-                hv[at:at + 4 * n] = a.view(np.uint8)
+                jobs.append((W.src_base + off, a))
+
+        def copy(job):
+            at, a = job
+            hv[at:at + a.nbytes] = a.view(np.uint8)
+
+        if threads > 1 and len(jobs) > 1:
+            from concurrent.futures import ThreadPoolExecutor
+
+            with ThreadPoolExecutor(min(threads, len(jobs))) as pool:
+                list(pool.map(copy, jobs))
+        else:
+            for j in jobs:
+                copy(j)
         return host
+
+    def _pinned(self, key: str, nbytes: int) -> torch.Tensor:
+        """A grow-only pinned host buffer owned by the plan."""
+        h = getattr(self, "_host_bufs", None)
+        if h is None:
+            h = self._host_bufs = {}
+        b = h.get(key)
+        if b is None or b.numel() < nbytes:
+            h.pop(key, None)
+            b = h[key] = pinned_host(nbytes)
+        return b
+
+    def _target_arena(self) -> torch.Tensor:
+        """Pinned host target arena for run_host: the previous call's is
+        reused once no array it returned is alive any more (they are views
+        of it), else a fresh one is allocated."""
+        prev = getattr(self, "_tgt_views", None)
+        if prev is not None and prev[1]() is None:
+            return prev[0]
+        return pinned_host(self.tgt_total)
 
     def stream_host(self, host_src: torch.Tensor, host_tgt: torch.Tensor | None, windows=None,
                     streams=None, slots: int | None = None,
@@ -482,7 +525,10 @@ class ReshardPlan:
     def unpack_host(self, host_tgt: torch.Tensor) -> dict:
         """{g: [array per target record, canonical order]} views of the host
         target arena."""
+        import weakref
+
         hv = host_tgt.numpy()
+        self._tgt_views = (host_tgt, weakref.ref(hv))
         out: dict = {}
         for W in self.windows:
             for g, i, m, off, n, dt in W.tgt_frags:
@@ -530,7 +576,7 @@ class ReshardPlan:
         """End-to-end in-memory reshard of host arrays; returns target arrays
         per rank in canonical record order."""
         host_src = self.pack_host(shards)
-        host_tgt = pinned_host(self.tgt_total)
+        host_tgt = self._target_arena()
         self.status.reset()
         self.run_pinned(host_src, host_tgt)
         return self.unpack_host(host_tgt)
@@ -643,25 +689,29 @@ def _rebind(v: np.ndarray, starts: np.ndarray, real: np.ndarray, lo: int = _SRC_
 
 
 class _D2DTemplate:
-    """The compiled tables of one device-to-device reshard layout, built on
-    virtual addresses (source fragment (g, i) at _SRC_V + offset, target
-    fragment at _TGT_V + offset, 256-B aligned). Each call patches the
-    caller's and the outputs' real addresses into host copies of the run /
-    aux tables (vectorised) and uploads them; the tile scan and the classing
-    stay. Valid for calls whose source pointers have the template's 16-B
-    phase (fresh torch allocations always do)."""
+    """The compiled tables of one device-to-device reshard layout.
+
+    Sources are compiled at virtual addresses (source fragment (g, i) at
+    _SRC_V + offset, 256-B aligned) and re-bound to the caller's tensors;
+    targets are compiled as offsets into ONE output arena, passed as the
+    launches' dst_base, so a call with the same source tensors as the
+    previous one patches and uploads nothing. Units that do not fuse
+    (Partial mean / noise) use a scratch atomic sized to them alone. Valid
+    for calls whose source pointers keep the template's 16-B phase (fresh
+    torch allocations always do)."""
 
     def __init__(self, spec, src, tgt, dtype, strict, device, window_bytes, tile_bytes,
-                 src_addr, tgt_addr):
+                 src_addr, tgt_addr, tgt_total):
         frags, targets = {}, {}
         for (g, i), (m, a, n) in src_addr.items():
             frags.setdefault((m.param, m.kind), []).append((m, a, n))
         for (g, i), (m, a) in tgt_addr.items():
             targets.setdefault((m.param, m.kind), []).append((m, a))
+        self.tgt_total, self.device = tgt_total, device
         wins = make_windows(spec.params, window_bytes)
         # the atomic of a unit is compiled at a virtual address; only units
-        # that do not fuse (Partial mean / noise) need real scratch, packed
-        # per window and bound once the largest window's need is known
+        # that do not fuse need real scratch, packed per window and bound
+        # once the largest window's need is known
         built, need = [], 0
         for W in wins:
             fx, rc, rl = XRunTable(), RunTable(), RunTable()
@@ -670,14 +720,13 @@ class _D2DTemplate:
                 for k in STATE_KINDS:
                     dt = dtype if k == "weight" else DType.F32
                     v = _ATOM_V + len(vstarts) * (1 << 40)
-                    if not compile_fused(fx, rc, rl, p, src, frags.get((p.name, k), []), v, tgt,
-                                         targets.get((p.name, k), []), dt, strict, False):
-                        vstarts.append(v)
+                    vstarts.append(v)
+                    if compile_fused(fx, rc, rl, p, src, frags.get((p.name, k), []), v, tgt,
+                                     targets.get((p.name, k), []), dt, strict, False):
+                        offs.append(-1)
+                    else:
                         offs.append(at)
                         at += align_up(4 * p.numel)
-                    else:
-                        vstarts.append(v)
-                        offs.append(-1)
             need = max(need, at)
             built.append((fx, rc, rl, vstarts, offs))
         self.scratch = (torch.empty(need, dtype=torch.uint8, device=device) if need else None)
@@ -696,23 +745,82 @@ class _D2DTemplate:
             for prog in progs:
                 prog.virt = (prog.runs_host.copy(), prog.aux_host.copy())
             self.progs.append(progs)
+        self.bound = None  # source addresses the device tables currently hold
+        self.status = Status(device)
+        self.word = torch.empty(2, dtype=torch.int64, pin_memory=True)
 
     def patch(self, starts: np.ndarray, real: np.ndarray) -> None:
-        """Rebind every virtual address to real[k] + (v - starts[k])."""
-        def rebind(v: np.ndarray) -> np.ndarray:
-            return _rebind(v, starts, real)
-
+        """Rebind every virtual source address to real[k] + (v - starts[k])
+        and upload the tables (skipped when the sources did not move)."""
+        if self.bound is not None and np.array_equal(self.bound, real):
+            return
         for progs in self.progs:
             for prog in progs:
                 runs0, aux0 = prog.virt
                 runs = runs0.copy()
                 for f in ("src", "dst"):
-                    runs[f] = rebind(runs0[f])
-                aux = rebind(aux0)
-                prog.runs_host, prog.aux_host = runs, aux
-                if len(runs):
-                    prog._runs.copy_(torch.from_numpy(np.ascontiguousarray(runs).view(np.uint8)))
-                prog._aux.copy_(torch.from_numpy(np.ascontiguousarray(aux).view(np.uint8)))
+                    runs[f] = _rebind(runs0[f], starts, real)
+                prog.set_tables(runs, _rebind(aux0, starts, real))
+        self.bound = real
+
+    def launch(self, arena: int, stream) -> None:
+        for fused, conv, load in self.progs:
+            fused.launch(0, 0, arena, self.status, stream)
+            conv.launch(True, 0, 0, self.status, stream)
+            load.launch(False, 0, arena, self.status, stream)
+
+    def localise(self, arena: int, stream) -> Exception:
+        """Re-run the source-reading launches one at a time (error path)."""
+        from .engine import describe_failure
+
+        for fused, conv, _ in self.progs:
+            for prog in (fused, conv):
+                self.status.reset(stream)
+                if prog is fused:
+                    prog.launch(0, 0, arena, self.status, stream)
+                else:
+                    prog.launch(True, 0, 0, self.status, stream)
+                stream.synchronize()
+                f, _ = self.status.read()
+                if f != (1 << 64) - 1:
+                    return describe_failure(prog, f >> 32, f & 0xFFFFFFFF, 0, (conv,))
+        return RuntimeError("reshard reported a failure that did not reproduce")
+
+
+class _D2DLayout:
+    """Per (spec, layouts, dtype): records, fragment sizes, the output arena
+    layout and the views to hand back (host-only, built once)."""
+
+    def __init__(self, spec, src, tgt, dtype):
+        src_recs, tgt_recs = all_rank_records(spec, src), all_rank_records(spec, tgt)
+        self.src_recs = src_recs
+        self.src_n = [[fragment_elems(spec.param(m.param), src, m) for m in src_recs[g]]
+                      for g in range(src.world_size)]
+        self.src_virt, vat = {}, _SRC_V
+        for g in range(src.world_size):
+            for i, m in enumerate(src_recs[g]):
+                n = self.src_n[g][i]
+                self.src_virt[(g, i)] = (m, vat, n)
+                vat += align_up(4 * max(n, 1))
+        self.starts = np.array([v[1] for v in self.src_virt.values()], dtype=np.uint64)
+        self.tgt_off, self.views, at = {}, [], 0
+        for g in range(tgt.world_size):
+            row = []
+            for i, m in enumerate(tgt_recs[g]):
+                dt = dtype if m.kind == "weight" else DType.F32
+                shape = tuple(fragment_shape(spec.param(m.param), tgt, m))
+                n = 1
+                for d in shape:
+                    n *= int(d)
+                self.tgt_off[(g, i)] = (m, at)
+                stride, acc = [], 1
+                for d in reversed(shape):
+                    stride.append(acc)
+                    acc *= int(d)
+                row.append((dt, shape, tuple(reversed(stride)), at // dt.itemsize))
+                at += align_up(dt.itemsize * max(n, 1))
+            self.views.append(row)
+        self.tgt_total = max(at, 256)
 
 
 def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: dict,
@@ -720,101 +828,91 @@ def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, sh
                    window_bytes: int = 5 << 29, tile_bytes: int = 1 << 17) -> dict:
     """Zero-copy device-to-device reshard: source fragments already in HBM
     ({g: [CUDA tensor per record of enumerate_rank_records(spec, src, g)]})
-    -> freshly allocated CUDA target fragments {g: [tensor per target
-    record]} (weights as torch.bfloat16 / float16 for a 16-bit dtype,
-    holding exactly the reference cast's bits).
+    -> CUDA target fragments {g: [tensor per target record]} (weights as
+    torch.bfloat16 / float16 for a 16-bit dtype, holding exactly the
+    reference cast's bits), views of one freshly allocated output arena.
 
-    The descriptor tables address the caller's tensors and the outputs by
-    absolute device address (every base pointer is 0), so nothing is staged:
+    The descriptor tables address the caller's tensors by absolute device
+    address and the targets by offset into the arena, so nothing is staged:
     one fused launch per window reads each source replica once, checks it
-    and writes every target replica. The atomic tensor is not materialised;
-    only units that cannot fuse (Partial mean / noise) go through a window
-    scratch buffer. The compiled tables are cached per thread and layout and
-    re-bound to each call's addresses (``_D2DTemplate``). Raises the
+    and writes every target replica; the atomic tensor is not materialised
+    (units that cannot fuse go through a small scratch). The compiled tables
+    are cached per thread and layout (``_D2DTemplate``) and re-bound only
+    when the source tensors move; the output views are built on the host
+    while the kernels run, and the call waits on a pinned status word rather
+    than the whole device. The per-thread cache keeps a reference to the
+    last call's source tensors (that is how a repeated call recognises them
+    without re-validating); ``api.release_staging()`` drops it. Raises the
     reference's exceptions (ReplicateMismatchError, PaddingError,
     ShapeError, ...)."""
     from ._errors import ShapeError
-    from .engine import describe_failure
     from .spec import spec_to_json
 
     validate_model_config(spec, src)
     validate_model_config(spec, tgt)
-    src_recs, tgt_recs = all_rank_records(spec, src), all_rank_records(spec, tgt)
     first = next((t for v in shards.values() for t in v), None)
     device = require_device(first.device if isinstance(first, torch.Tensor) else None)
-    src_real, src_virt, vat = {}, {}, _SRC_V
-    for g in range(src.world_size):
-        got = shards.get(g, [])
-        if len(got) != len(src_recs[g]):
-            raise ShapeError(f"rank {g}: {len(got)} fragments, want {len(src_recs[g])}")
-        for i, (m, t) in enumerate(zip(src_recs[g], got)):
-            n = fragment_elems(spec.param(m.param), src, m)
-            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
-                    and t.is_contiguous() and t.numel() == n and t.device == device):
-                raise ShapeError(f"rank {g} {m.param}.{m.kind}: want a contiguous float32 CUDA "
-                                 f"tensor of {n} elements on {device}")
-            src_real[(g, i)] = (m, t.data_ptr(), n)
-            src_virt[(g, i)] = (m, vat, n)
-            vat += align_up(4 * max(n, 1))
-    out: dict = {g: [] for g in range(tgt.world_size)}
-    tgt_real, tgt_virt, vat = {}, {}, _TGT_V
-    for g in range(tgt.world_size):
-        for i, m in enumerate(tgt_recs[g]):
-            p = spec.param(m.param)
-            dt = dtype if m.kind == "weight" else DType.F32
-            t = torch.empty(fragment_shape(p, tgt, m), dtype=_TORCH_OF[dt], device=device)
-            out[g].append(t)
-            tgt_real[(g, i)] = (m, t.data_ptr())
-            tgt_virt[(g, i)] = (m, vat)
-            vat += align_up(max(t.numel(), 1) * t.element_size())
-    # a cached template holds when every source keeps the virtual 16-B phase
-    phase_ok = (all((src_real[k][1] - src_virt[k][1]) % 16 == 0 for k in src_real)
-                and all((tgt_real[k][1] - tgt_virt[k][1]) % 16 == 0 for k in tgt_real))
     key = (spec_to_json(spec), format_config_string(src), getattr(src, "vocab_multiple", 1),
            format_config_string(tgt), getattr(tgt, "vocab_multiple", 1), dtype.name, strict,
            window_bytes, tile_bytes, str(device))
     cache = getattr(_D2D, "cache", None)
     if cache is None:
         cache = _D2D.cache = {}
-    tpl = cache.get(key) if phase_ok else None
+    lay = cache.get(("layout", key))
+    if lay is None:
+        lay = _D2DLayout(spec, src, tgt, dtype)
+    # validate the caller's fragments (skipped when they are the very tensors
+    # of the previous call: same objects at the same addresses)
+    tensors = [t for g in range(src.world_size) for t in shards.get(g, [])]
+    ids = [id(t) for t in tensors]
+    prev = cache.get(("last", key))
+    if prev is not None and prev[0] == ids:
+        # the cache holds the previous call's tensors, so equal ids are the
+        # very same (still live) objects
+        real = prev[1]
+    else:
+        for g in range(src.world_size):
+            got = shards.get(g, [])
+            if len(got) != len(lay.src_recs[g]):
+                raise ShapeError(f"rank {g}: {len(got)} fragments, want {len(lay.src_recs[g])}")
+            for i, t in enumerate(got):
+                n = lay.src_n[g][i]
+                if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
+                        and t.is_contiguous() and t.numel() == n and t.device == device):
+                    m = lay.src_recs[g][i]
+                    raise ShapeError(f"rank {g} {m.param}.{m.kind}: want a contiguous float32 CUDA "
+                                     f"tensor of {n} elements on {device}")
+        real = np.array([t.data_ptr() for t in tensors], dtype=np.uint64)
+    cache[("last", key)] = (ids, real, tensors)
+    # a cached template holds when every source keeps the virtual 16-B phase
+    phase_ok = bool(((real - lay.starts) % np.uint64(16) == 0).all())
+    tpl = cache.get(("tpl", key)) if phase_ok else None
     if tpl is None:
+        src_addr = lay.src_virt if phase_ok else {
+            k: (m, int(real[j]), n) for j, (k, (m, _, n)) in enumerate(lay.src_virt.items())}
+        tpl = _D2DTemplate(spec, src, tgt, dtype, strict, device, window_bytes, tile_bytes,
+                           src_addr, lay.tgt_off, lay.tgt_total)
         if phase_ok:
-            tpl = _D2DTemplate(spec, src, tgt, dtype, strict, device, window_bytes, tile_bytes,
-                               src_virt, tgt_virt)
-            cache.clear()  # one template (and its scratch) per thread
-            cache[key] = tpl
-        else:  # odd source alignment: compile on the real addresses, uncached
-            tpl = _D2DTemplate(spec, src, tgt, dtype, strict, device, window_bytes, tile_bytes,
-                               src_real, tgt_real)
+            for k in [k for k in cache if k[0] != "last" and k[1] != key]:
+                del cache[k]  # one layout (and its scratch) per thread
+            cache[("layout", key)] = lay
+            cache[("tpl", key)] = tpl
     if phase_ok:
-        keys = sorted(src_virt, key=lambda k: src_virt[k][1])
-        tkeys = sorted(tgt_virt, key=lambda k: tgt_virt[k][1])
-        starts = np.array([src_virt[k][1] for k in keys] + [tgt_virt[k][1] for k in tkeys],
-                          dtype=np.uint64)
-        real = np.array([src_real[k][1] for k in keys] + [tgt_real[k][1] for k in tkeys],
-                        dtype=np.uint64)
-        tpl.patch(starts, real)
-    status = Status(device)
-    status.reset()
+        tpl.patch(lay.starts, real)
+    arena = torch.empty(lay.tgt_total, dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream(device)
-    # stream-ordered: windows reuse the scratch in order; a failure anywhere
-    # is localised afterwards by re-running the source-reading launches
-    for progs in tpl.progs:
-        progs[0].launch(0, 0, 0, status, stream)
-        progs[1].launch(True, 0, 0, status, stream)
-        progs[2].launch(False, 0, 0, status, stream)
-    torch.cuda.synchronize(device)
-    if status.read()[0] != (1 << 64) - 1:
-        for fused, conv, _ in tpl.progs:  # localise: re-run the source-reading launches
-            for prog in (fused, conv):
-                status.reset()
-                if prog is fused:
-                    prog.launch(0, 0, 0, status, stream)
-                else:
-                    prog.launch(True, 0, 0, status, stream)
-                torch.cuda.synchronize(device)
-                f, _ = status.read()
-                if f != (1 << 64) - 1:
-                    raise describe_failure(prog, f >> 32, f & 0xFFFFFFFF, 0, (conv,))
-        raise RuntimeError("reshard reported a failure that did not reproduce")
+    tpl.status.reset(stream)
+    tpl.launch(arena.data_ptr(), stream)
+    tpl.word.copy_(tpl.status.t, non_blocking=True)
+    done = torch.cuda.Event()
+    done.record(stream)
+    # the output views are built while the kernels run
+    typed = {DType.F32: arena.view(torch.float32)}
+    if dtype is not DType.F32:
+        typed[dtype] = arena.view(_TORCH_OF[dtype])
+    out = {g: [typed[dt].as_strided(shape, stride, off) for dt, shape, stride, off in row]
+           for g, row in enumerate(lay.views)}
+    done.synchronize()
+    if int(tpl.word[0]) != -1:
+        raise tpl.localise(arena.data_ptr(), stream)
     return out

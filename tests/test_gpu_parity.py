@@ -772,25 +772,25 @@ def test_pad_error_outranks_tp_mismatch(path):
     spec = U.make_model("DenseGPT", {"n_layers": 1, "hidden": 1024})
     src, tgt = cfg(dp=3, tp=2, zero="z1"), cfg(dp=2, zero="z1")
     shards = O.partition_mem(spec, O.init_state(spec, 7), src)
-    recs = U.enumerate_rank_records(spec, src, 0)
     for g in range(src.world_size):
         for i, (m, a) in enumerate(shards[g]):
-            if (m.param, m.kind) != ("layers.0.ln_b", "m") or m.placement[1] != 1:
+            if (m["param"], m["kind"]) != ("layers.0.ln_b", "m") or m["placement"][1] != 1:
                 continue
             a = a.copy()
-            if m.pad_elems:
+            if m["pad_elems"]:
                 a[-1] = np.float32(1.0)  # nonzero pad on the last dp rank of tp 1
             else:
                 a[3] = np.float32(0.25)  # tp 1 differs from tp 0
             shards[g][i] = (m, a)
-    assert recs
     with pytest.raises(O.OracleError, match="PaddingError"):
         O.convert_mem(spec, src, shards)
     with pytest.raises(U.PaddingError):
         if path == "union":
             p = spec.param("layers.0.ln_b")
             U.union(p, src, [U.FragmentMsg(m, a) for g in range(src.world_size)
-                             for m, a in shards[g] if (m.param, m.kind) == (p.name, "m")])
+                             for m, (_, a) in zip(U.enumerate_rank_records(spec, src, g),
+                                                  shards[g])
+                             if (m.param, m.kind) == (p.name, "m")])
         elif path == "device":
             U.reshard(spec, src, tgt, {g: [torch.from_numpy(a).cuda() for _, a in v]
                                        for g, v in shards.items()})

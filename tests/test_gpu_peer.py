@@ -1,7 +1,8 @@
 """Rank-homed load through CUDA IPC peer memory (north_star item 3), run as
-2 processes sharing cuda:0 (the only GPU this build gets): each rank's fused
-reshard kernel stores the target fragments homed on the other rank straight
-into that rank's IPC-mapped receive buffer. Checked against the oracle."""
+2 processes (on cuda:0 and cuda:1 when two GPUs exist, else both on cuda:0):
+each rank's fused reshard kernel stores the target fragments homed on the
+other rank straight into that rank's IPC-mapped receive buffer. Checked
+against the oracle."""
 
 import os
 import socket
@@ -23,7 +24,9 @@ def _free_port():
 
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
+    # rank r on cuda:r when there are enough GPUs (real cross-device IPC over
+    # NVLink); otherwise both ranks share cuda:0
+    torch.cuda.set_device(rank % torch.cuda.device_count())
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2406_18820_b200 as U

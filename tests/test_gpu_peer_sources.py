@@ -2,8 +2,8 @@
 source rank g's fragments live on GPU g mod world, target rank t's on GPU t
 mod world, and each param owner's fused kernel reads its sources from the
 home GPUs and stores the targets into the home GPUs over IPC-mapped peer
-memory -- no staging, no collective. Run as 2 processes sharing cuda:0 (the
-only GPU this build gets); checked byte-for-byte against the oracle."""
+memory -- no staging, no collective. Run as 2 processes, on two GPUs when
+present, else sharing cuda:0; checked byte-for-byte against the oracle."""
 
 import os
 import socket
@@ -25,7 +25,9 @@ def _free_port():
 
 def _worker(rank, world, port, q, fault):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
+    # rank r on cuda:r when there are enough GPUs (real cross-device IPC over
+    # NVLink); otherwise both ranks share cuda:0
+    torch.cuda.set_device(rank % torch.cuda.device_count())
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2406_18820_b200 as U

@@ -40,6 +40,7 @@ def test_abi_constants_match_header():
     assert int(consts["UCP_OP_CHECKZERO"]) == plan.OP_CHECKZERO
     assert int(consts["UCP_NCLASS"]) == plan.NCLASS
     assert int(consts["UCP_CLASS_GENERAL"]) == plan.CLASS_GENERAL
+    assert int(consts["UCP_CLASS_OPS"]) == plan.CLASS_OPS
     assert int(consts["UCP_CLASS_VEC_BF16"]) == plan.CLASS_VEC_BF16
     assert RUN_DTYPE.itemsize == 64 and TILE_DTYPE.itemsize == 16 and RUNTILE_DTYPE.itemsize == 16
 
@@ -48,10 +49,12 @@ def test_argument_errors_without_device():
     lib = _native.load_library()
     # invalid arguments are rejected before any CUDA call
     import numpy as np
-    bad = np.array([0, -1, 0, 0] + [0] * 4, dtype=np.int64)
-    zero = np.zeros(8, dtype=np.int64)
-    tiles_without_runs = np.array([5, 0, 0, 0] + [0] * 4, dtype=np.int64)
-    runs_mismatch = np.array([0] * 4 + [2, 0, 0, 0], dtype=np.int64)  # n_runs passed as 3
+    from paper_2406_18820_b200.plan import NCLASS
+
+    bad = np.array([0, -1] + [0] * (2 * NCLASS - 2), dtype=np.int64)
+    zero = np.zeros(2 * NCLASS, dtype=np.int64)
+    tiles_without_runs = np.array([5] + [0] * (2 * NCLASS - 1), dtype=np.int64)
+    runs_mismatch = np.array([0] * NCLASS + [2] + [0] * (NCLASS - 1), dtype=np.int64)  # n_runs passed as 3
     assert lib.ucp_convert_gather(None, 0, None, None, bad.ctypes.data, None, None, None, None) == -10
     assert lib.ucp_convert_gather(None, 0, None, None, None, None, None, None, None) == -10
     assert lib.ucp_convert_gather(None, 0, None, None, tiles_without_runs.ctypes.data, None, None,

@@ -38,18 +38,18 @@ CASES = {
     "fused_f32": ("llama", CFG(4, 2), CFG(2, 4), True, DType.F32, ["reshard_fused_f32"]),
     "fused_bf16": ("llama", CFG(4, 2), CFG(2, 4), True, DType.BF16, ["reshard_fused_bf16"]),
     "fused_f16": ("llama", CFG(4, 2), CFG(2, 4), True, DType.F16, ["reshard_fused_f16"]),
-    "fused_staged": ("llama", CFG(3, 2), CFG(2, 4), True, DType.F32, ["reshard_fused_scalar"]),
-    "fused_staged5": ("llama", CFG(5, 2), CFG(2, 4), True, DType.F32, ["reshard_fused_scalar"]),
+    "fused_staged": ("llama", CFG(3, 2), CFG(2, 4), True, DType.F32, ["reshard_fused_realign"]),
+    "fused_staged5": ("llama", CFG(5, 2), CFG(2, 4), True, DType.F32, ["reshard_fused_realign"]),
     "unfused_f32": ("llama", CFG(4, 2), CFG(2, 4), False, DType.F32,
                     ["convert_gather_f32", "load_scatter_f32"]),
     "unfused_bf16": ("llama", CFG(4, 2), CFG(2, 4), False, DType.BF16, ["load_scatter_bf16"]),
     "unfused_f16": ("llama", CFG(4, 2), CFG(2, 4), False, DType.F16, ["load_scatter_f16"]),
     "unfused_staged": ("llama", CFG(3, 2), CFG(2, 4), False, DType.F32,
-                       ["convert_gather_general"]),
+                       ["convert_gather_realign"]),
     # f64 MEAN over tp=4 groups + ZeRO pad checks (convert); partial NOISE
     # + ZeRO re-pad (load): the GENERAL class of the move kernels
     "general_ops": ("partial", CFG(2, 4), CFG(3, 2), False, DType.F32,
-                    ["convert_gather_general", "load_scatter_general"]),
+                    ["convert_gather_ops", "load_scatter_ops"]),
 }
 
 
