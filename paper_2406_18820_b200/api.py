@@ -280,7 +280,7 @@ def release_staging() -> None:
 
     _LOCAL.stage = _Staging()
     _LOCAL.plans = {}
-    getattr(_reshard._D2D, "cache", {}).clear()  # reshard_device templates + their scratch
+    _reshard._D2D.state = None  # reshard_device's template, scratch and last sources
 
 
 def _run(prog: Program, gather: bool, src_base: int, dst_base: int, dev) -> None:

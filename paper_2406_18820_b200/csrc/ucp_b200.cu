@@ -40,6 +40,9 @@ namespace {
 #ifndef UCP_OPS_MINB
 #define UCP_OPS_MINB 2  // CTAs per SM of the MEAN / NOISE / ZERO / CHECKZERO kernels (f64 accumulators)
 #endif
+#ifndef UCP_OPS_GC
+#define UCP_OPS_GC 4  // MEAN: averaged groups whose loads are in flight together
+#endif
 #ifndef UCP_PERSISTENT
 #define UCP_PERSISTENT 0  // 1: fused kernel runs 148*UCP_MINB persistent CTAs over the tiles
 #endif
@@ -312,7 +315,7 @@ __device__ __forceinline__ void op_run(const Ctx& c, uint64_t srow, uint64_t dro
   if constexpr (OP != UCP_OP_ZERO) {
     // groups in chunks of GC: every (group, slot) vector of a replica is in
     // flight at once; accumulation stays in ascending group order
-    constexpr int GC = OP == UCP_OP_MEAN ? 4 : 1;
+    constexpr int GC = OP == UCP_OP_MEAN ? UCP_OPS_GC : 1;
     for (int g0 = 0; g0 < G; g0 += GC) {
       Lanes<W> p[GC][U];
       for (int k = 0; k < K; ++k) {

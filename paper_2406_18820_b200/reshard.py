@@ -855,21 +855,19 @@ def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, sh
     key = (spec_to_json(spec), format_config_string(src), getattr(src, "vocab_multiple", 1),
            format_config_string(tgt), getattr(tgt, "vocab_multiple", 1), dtype.name, strict,
            window_bytes, tile_bytes, str(device))
-    cache = getattr(_D2D, "cache", None)
-    if cache is None:
-        cache = _D2D.cache = {}
-    lay = cache.get(("layout", key))
-    if lay is None:
-        lay = _D2DLayout(spec, src, tgt, dtype)
+    # one cached layout per thread: its template, scratch and last sources
+    st = getattr(_D2D, "state", None)
+    if st is None or st["key"] != key:
+        st = _D2D.state = {"key": key, "lay": _D2DLayout(spec, src, tgt, dtype), "tpl": None,
+                           "last": None}
+    lay = st["lay"]
     # validate the caller's fragments (skipped when they are the very tensors
-    # of the previous call: same objects at the same addresses)
+    # of the previous call: the state holds them, so equal ids are the same
+    # live objects)
     tensors = [t for g in range(src.world_size) for t in shards.get(g, [])]
     ids = [id(t) for t in tensors]
-    prev = cache.get(("last", key))
-    if prev is not None and prev[0] == ids:
-        # the cache holds the previous call's tensors, so equal ids are the
-        # very same (still live) objects
-        real = prev[1]
+    if st["last"] is not None and st["last"][0] == ids:
+        real = st["last"][1]
     else:
         for g in range(src.world_size):
             got = shards.get(g, [])
@@ -883,22 +881,20 @@ def reshard_device(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, sh
                     raise ShapeError(f"rank {g} {m.param}.{m.kind}: want a contiguous float32 CUDA "
                                      f"tensor of {n} elements on {device}")
         real = np.array([t.data_ptr() for t in tensors], dtype=np.uint64)
-    cache[("last", key)] = (ids, real, tensors)
-    # a cached template holds when every source keeps the virtual 16-B phase
+    st["last"] = (ids, real, tensors)
+    # the cached template holds when every source keeps the virtual 16-B phase;
+    # otherwise compile on the real addresses, uncached
     phase_ok = bool(((real - lay.starts) % np.uint64(16) == 0).all())
-    tpl = cache.get(("tpl", key)) if phase_ok else None
-    if tpl is None:
-        src_addr = lay.src_virt if phase_ok else {
-            k: (m, int(real[j]), n) for j, (k, (m, _, n)) in enumerate(lay.src_virt.items())}
+    if phase_ok:
+        if st["tpl"] is None:
+            st["tpl"] = _D2DTemplate(spec, src, tgt, dtype, strict, device, window_bytes,
+                                     tile_bytes, lay.src_virt, lay.tgt_off, lay.tgt_total)
+        tpl = st["tpl"]
+        tpl.patch(lay.starts, real)
+    else:
+        src_addr = {k: (m, int(real[j]), n) for j, (k, (m, _, n)) in enumerate(lay.src_virt.items())}
         tpl = _D2DTemplate(spec, src, tgt, dtype, strict, device, window_bytes, tile_bytes,
                            src_addr, lay.tgt_off, lay.tgt_total)
-        if phase_ok:
-            for k in [k for k in cache if k[0] != "last" and k[1] != key]:
-                del cache[k]  # one layout (and its scratch) per thread
-            cache[("layout", key)] = lay
-            cache[("tpl", key)] = tpl
-    if phase_ok:
-        tpl.patch(lay.starts, real)
     arena = torch.empty(lay.tgt_total, dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream(device)
     tpl.status.reset(stream)
