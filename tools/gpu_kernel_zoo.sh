@@ -6,7 +6,7 @@
 # raw pages) and the .ncu-rep deleted (gpurun copies back <= 64 MiB).
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 TAG=${1:-x}; shift
-CASES=${@:-fused_f32 fused_bf16 fused_f16 fused_staged fused_staged5 unfused_f32 unfused_bf16 unfused_f16 unfused_staged general_ops}
+CASES=${@:-fused_f32 fused_bf16 fused_f16 fused_staged fused_staged5 unfused_f32 unfused_bf16 unfused_f16 unfused_staged unfused_staged_load fused_staged_bf16 general_ops}
 mkdir -p gpurun_out
 M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv"
 for c in $CASES; do

@@ -46,6 +46,10 @@ CASES = {
     "unfused_f16": ("llama", CFG(4, 2), CFG(2, 4), False, DType.F16, ["load_scatter_f16"]),
     "unfused_staged": ("llama", CFG(3, 2), CFG(2, 4), False, DType.F32,
                        ["convert_gather_realign"]),
+    "unfused_staged_load": ("llama", CFG(4, 2), CFG(3, 2), False, DType.F32,
+                            ["load_scatter_realign"]),
+    "fused_staged_bf16": ("llama", CFG(3, 2), CFG(2, 4), True, DType.BF16,
+                          ["reshard_fused_realign"]),
     # f64 MEAN over tp=4 groups + ZeRO pad checks (convert); partial NOISE
     # + ZeRO re-pad (load): the GENERAL class of the move kernels
     "general_ops": ("partial", CFG(2, 4), CFG(3, 2), False, DType.F32,

@@ -1,28 +1,35 @@
 #!/usr/bin/env python
-"""Dump SASS of the hot kernels of libucp_b200.so into profiles/ and print
-the instruction mix that proves the vector path (LDG.E.NA.128 / STG.E.128,
-no local-memory spills)."""
+"""Dump SASS of every shipped kernel of libucp_b200.so into profiles/ and
+print the instruction mix that proves the vector path (LDG.E.NA.128 /
+STG.E.128, funnel shuffles for the realigning kernels, no local-memory
+spills).
+
+    python tools/sass_dump.py TAG        # writes profiles/sass_<kernel>_<TAG>.txt
+"""
 import re
 import subprocess
 import sys
 
 LIB = "paper_2406_18820_b200/libucp_b200.so"
-tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
 txt = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s*Function : ", txt)
-out = []
+MIX = {"LDG.NA.128": r"LDG\.E\.NA\.128", "LDG.128": r"LDG\.E\.128", "LDG.NA.32": r"LDG\.E\.NA ",
+       "STG.128": r"STG\.E\.128", "STG.64": r"STG\.E\.64", "STG.32": r"STG\.E(\.U16)? ",
+       "SHFL.IDX": r"SHFL\.IDX", "STS.128": r"STS\.128", "LDS": r"LDS[ .]", "F2FP": r"F2FP",
+       "STL": r"\bSTL\b", "LDL": r"\bLDL\b", "DADD": r"DADD", "DMUL": r"DMUL"}
+rows = []
 for f in funcs[1:]:
     name = f.split("\n", 1)[0].strip()
     m = re.search(r"(convert_gather_\w+?|load_scatter_\w+?|reshard_fused_\w+?|adam_step_kernel|"
-                  r"gen_state_kernel|compare_kernel)E", name)
-    short = m.group(1) if m else name
-    body = f
-    mix = {k: len(re.findall(k, body)) for k in (r"LDG\.E\.NA\.128", r"LDG\.E\.128", r"STG\.E\.128",
-                                                 r"STG\.E\.64", r"\bSTL\b", r"\bLDL\b", r"DADD", r"DMUL")}
-    out.append((short, mix))
-    if any(k in name for k in ("convert_gather_f32", "load_scatter_bf16", "reshard_fused_f32",
-                               "reshard_fused_bf16")):
-        with open(f"profiles/sass_{short}_{tag}.txt", "w") as fh:
-            fh.write("Function : " + f)
-for n, m in out:
-    print(n[:60].ljust(60), m)
+                  r"gen_state_kernel|compare_kernel|runtile_scan_kernel)E", name)
+    if not m:
+        continue
+    short = m.group(1)
+    mix = {k: len(re.findall(v, f)) for k, v in MIX.items()}
+    n_instr = len(re.findall(r"/\*[0-9a-f]{4,}\*/", f))
+    rows.append((short, n_instr, mix))
+    with open(f"profiles/sass_{short}_{tag}.txt", "w") as fh:
+        fh.write("Function : " + f)
+for n, ni, m in sorted(rows):
+    print(n.ljust(26), str(ni).rjust(6), {k: v for k, v in m.items() if v})
