@@ -39,11 +39,21 @@ GB = 1e9
 
 
 def mem_available() -> int:
+    """MemAvailable, capped by the cgroup's headroom (memory.max - memory.current)
+    when the process runs under a memory limit."""
+    avail = 0
     with open("/proc/meminfo") as f:
         for line in f:
             if line.startswith("MemAvailable:"):
-                return int(line.split()[1]) * 1024
-    return 0
+                avail = int(line.split()[1]) * 1024
+    try:
+        lim = open("/sys/fs/cgroup/memory.max").read().strip()
+        cur = int(open("/sys/fs/cgroup/memory.current").read().strip())
+        if lim != "max":
+            avail = min(avail, int(lim) - cur)
+    except (OSError, ValueError):
+        pass
+    return avail
 
 
 def main():
