@@ -1169,6 +1169,9 @@ def partition(state: ModelState, cfg: ParallelConfig, out_dir: str, workers: int
 # --------------------------------------------------------------------------- in-memory reshard
 
 
+HOST_WINDOW_BYTES = 400_000_000  # state bytes per window of the host-streamed reshard()
+
+
 def reshard(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: dict,
             dtype: DType = DType.F32, strict: bool = True, *, device=None,
             fused: bool = True) -> dict:
@@ -1192,7 +1195,10 @@ def reshard(spec: ModelSpec, src: ParallelConfig, tgt: ParallelConfig, shards: d
     cache = _LOCAL.plans  # per thread: a plan's streams and device slots are not shared
     plan = cache.get(key)
     if plan is None:
-        plan = ReshardPlan(spec, src, tgt, dtype=dtype, strict=strict, device=dev, fused=fused)
+        # small windows: packing, PCIe in, HBM work and PCIe out overlap with
+        # little pipeline fill / drain (the e2e leg's 0.4 GB, bench.py)
+        plan = ReshardPlan(spec, src, tgt, dtype=dtype, strict=strict, device=dev, fused=fused,
+                           window_bytes=HOST_WINDOW_BYTES)
         cache.clear()  # keep one compiled plan (its device slots) per thread
         cache[key] = plan
     return plan.run_host(shards)

@@ -34,8 +34,8 @@ namespace {
 #ifndef UCP_VEC
 #define UCP_VEC 4
 #endif
-#ifndef UCP_SCALAR_MINB
-#define UCP_SCALAR_MINB 3  // CTAs per SM of the realigning kernels (80 registers: no spills; 4 spills)
+#ifndef UCP_REALIGN_MINB
+#define UCP_REALIGN_MINB 4  // CTAs per SM of the realigning kernels (64 registers, no shared staging)
 #endif
 #ifndef UCP_OPS_MINB
 #define UCP_OPS_MINB 2  // CTAs per SM of the MEAN / NOISE / ZERO / CHECKZERO kernels (f64 accumulators)
@@ -53,10 +53,6 @@ constexpr uint32_t kSeg = 32 * 4 * kVec;  // elements per warp segment (512)
 constexpr int kMaxAux = 256;             // host splits runs beyond this
 
 // ---------------------------------------------------------------- memory ops
-
-#ifndef UCP_SCALAR_U
-#define UCP_SCALAR_U 8  // elements per lane per step on the scalar fused path (4 / 8 / 16: 1467 / 1480 / 1449 GB/s at dp=3)
-#endif
 
 #ifndef UCP_PREFETCH_NEXT
 #define UCP_PREFETCH_NEXT 0  // fused kernel: L2 bulk prefetch distance in warp items (0: off)
@@ -726,73 +722,41 @@ __device__ __forceinline__ void vec_body(const ucp_run* __restrict__ runs,
   }
 }
 
-#ifndef UCP_STAGED
-#define UCP_STAGED 1  // phase-mismatched fused cells through shared memory (0: scalar path)
-#endif
-
-// Phase-mismatched fused cells at vector width: each warp stages its row
-// segment through shared memory. Every source replica is read with aligned
-// 16-B loads on its own phase grid into a warp-private buffer; replicas are
-// compared element-wise from shared memory; the atomic and every target are
-// written with aligned 16-B (8-B for 16-bit targets) stores on their own
-// phase grids, reading four shifted elements from shared memory -- the
-// "shared-memory staging" the strided pieces need, with no register
-// pressure added to the aligned kernels.
-constexpr int kStage = kSeg + 8;  // floats per warp buffer: 512 + up to 3 + 3 slop
-
-__device__ __forceinline__ int stage_in(float* buf, const char* p, uint32_t len, uint32_t lane) {
-  // p: address of element 0 (4-B aligned). Returns off: element j sits at buf[j + off].
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const int off = (int)((a >> 2) & 3);
-  const float4* v0 = reinterpret_cast<const float4*>(a - 4 * off);
-  const uint32_t nv = (off + len + 3) >> 2;
-  for (uint32_t i = lane; i < nv; i += 32) {
-    const float4 x = ld_stream4(v0 + i);
-    reinterpret_cast<float4*>(buf)[i] = x;
-  }
-  return off;
-}
-
-template <int DT>
-__device__ __forceinline__ void stage_out(char* p, const float* buf, int off, uint32_t len,
-                                          uint32_t lane) {
-  // p: address of element 0 of the destination (ESZ-aligned)
-  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const uint32_t ph = (uint32_t)((a / ESZ) & 3);
-  uint32_t head = (4u - ph) & 3u;
-  if (head > len) head = len;
-  const uint32_t nvec = (len - head) >> 2;
-  const uint32_t tail = len - head - 4 * nvec;
-  for (uint32_t i = lane; i < nvec; i += 32) {
-    const uint32_t j = head + 4 * i + off;
-    const float4 x = make_float4(buf[j], buf[j + 1], buf[j + 2], buf[j + 3]);
-    store4<DT>(p + (uint64_t)ESZ * (head + 4 * i), x);
-  }
-  if (lane < head + tail) {
-    const uint32_t e = lane < head ? lane : head + 4 * nvec + (lane - head);
-    store1<DT>(p + (uint64_t)ESZ * e, buf[e + off]);
-  }
-}
-
 // ---------------------------------------------------------------- realigning kernels
 //
 // COPY pieces whose sources and destinations do not share one 16-B phase
 // (ZeRO partitions of dp = 3, 5, ... start at k * ceil(n / dp) elements).
-// Each warp moves a row segment at vector width with no shared memory:
-//  * every lane loads aligned 16-B vectors on the primary's phase grid
-//    (lane l, slot u: source vector I = l + 32u; a 512-element segment spans
-//    <= 129 vectors, so kRU = 5 slots);
-//  * replicas on the same grid are loaded the same way and compared in
-//    registers;
+// Each warp moves a row segment at vector width, with no shared memory:
+//  * segments are cut on the primary source's 16-B grid (a tile row's first
+//    segment ends at a grid boundary), so a 512-element segment spans <= 128
+//    source vectors: kRU = 4 aligned 16-B loads per lane, as in the vector
+//    kernels, and the register budget of 4 CTAs per SM;
+//  * replicas on the primary's grid are loaded the same way and compared in
+//    registers; a replica on another grid (hand-made layouts only) is
+//    compared with coalesced 4-B loads;
 //  * a lane's right neighbour vector I + 1 comes from one round of warp
-//    shuffles (lane 31 takes lane 0's next slot);
+//    shuffles per segment (lane 31 takes lane 0's next slot), shared by the
+//    atomic and every destination, and skipped when no phase differs;
 //  * destination d with phase pd writes its aligned vector J = I + kappa as
 //    funnel(v_I, v_I+1, (ps - pd) & 3), plus <= 3 head and <= 3 tail scalars.
-// The former shared-memory staging (stage_in / stage_out: an STS.128 per
-// replica vector and 4 scalar LDS per destination vector) stays as the
-// fallback for runs whose replicas sit on different phase grids.
-constexpr int kRU = (kSeg / 4 + 1 + 31) / 32;
+constexpr int kRU = kVec;
+
+// Segment k of a tile row of nc elements whose element 0 sits at phase p0
+// (0..3) of the primary source's 16-B grid: [start, start + len), cut at grid
+// boundaries. False for the empty last segment of a row that needs fewer.
+__device__ __forceinline__ bool realign_seg(uint32_t k, uint32_t nc, uint32_t p0, uint32_t& start,
+                                            uint32_t& len) {
+  const uint32_t lo = k * kSeg;
+  const uint32_t s = lo > p0 ? lo - p0 : 0;
+  const uint32_t e = min(nc, lo + kSeg - p0);
+  if (s >= e) return false;
+  start = s;
+  len = e - s;
+  return true;
+}
+
+// segments per tile row of nc elements at any phase
+__device__ __forceinline__ uint32_t realign_spr(uint32_t nc) { return (nc + 3 + kSeg - 1) / kSeg; }
 
 __device__ __forceinline__ float4 funnel4(const float4& a, const float4& b, uint32_t d) {
   switch (d) {
@@ -803,13 +767,17 @@ __device__ __forceinline__ float4 funnel4(const float4& a, const float4& b, uint
   }
 }
 
+__device__ __forceinline__ float comp4(const float4& a, int c) {
+  return c == 0 ? a.x : c == 1 ? a.y : c == 2 ? a.z : a.w;
+}
+
 // Store segment elements [0, len) to p (element 0's address) from the
-// source-grid vectors v of phase ps; a lane's right neighbour vector comes
-// from one warp shuffle round per slot (lane 31 takes lane 0's next slot);
-// sp = the primary's element 0 (head / tail scalars re-read, L2 hits).
+// source-grid vectors v (phase ps) and their right neighbours nx; sp = the
+// primary's element 0 (head / tail scalars re-read, L2 hits).
 template <int DT>
-__device__ __forceinline__ void realign_store(char* p, const float4 (&v)[kRU], uint32_t ps,
-                                              uint32_t len, uint32_t lane, const char* sp) {
+__device__ __forceinline__ void realign_store(char* p, const float4 (&v)[kRU],
+                                              const float4 (&nx)[kRU], uint32_t ps, uint32_t len,
+                                              uint32_t lane, const char* sp) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   const uintptr_t da = reinterpret_cast<uintptr_t>(p);
   const uint32_t pd = (uint32_t)((da / ESZ) & 3);
@@ -818,17 +786,10 @@ __device__ __forceinline__ void realign_store(char* p, const float4 (&v)[kRU], u
   char* dv = p - (size_t)ESZ * pd;     // aligned destination vector 0
   const int J0 = pd ? 1 : 0;
   const int J1 = (int)((len + pd) >> 2) - 1;
-  const int from = (int)((lane + 1) & 31);
 #pragma unroll
   for (int u = 0; u < kRU; ++u) {
-    const float4 give = (lane == 0 && u + 1 < kRU) ? v[u + 1] : v[u];
-    float4 nx;
-    nx.x = __shfl_sync(0xffffffffu, give.x, from);
-    nx.y = __shfl_sync(0xffffffffu, give.y, from);
-    nx.z = __shfl_sync(0xffffffffu, give.z, from);
-    nx.w = __shfl_sync(0xffffffffu, give.w, from);
     const int J = (int)(lane + 32u * u) + kappa;
-    if (J >= J0 && J <= J1) store4<DT>(dv + (size_t)ESZ * 4 * J, funnel4(v[u], nx, delta));
+    if (J >= J0 && J <= J1) store4<DT>(dv + (size_t)ESZ * 4 * J, funnel4(v[u], nx[u], delta));
   }
   const uint32_t head_end = min(4u * (uint32_t)J0 - pd, len);
   uint32_t tail_start = J1 >= J0 ? 4u * (uint32_t)(J1 + 1) - pd : head_end;
@@ -839,10 +800,9 @@ __device__ __forceinline__ void realign_store(char* p, const float4 (&v)[kRU], u
   }
 }
 
-// One row segment [0, len): sources at sb + src_k + soff (src_0 = s0, src_k
-// = s_aux[k - 1]; all on the primary's 16-B grid), optional f32 atom at
-// ab + aoff, destinations at db + dst_d + doff (dst_0 = d0, dst_d =
-// s_aux[ns - 1 + d - 1]).
+// One row segment [0, len), cut on the primary's grid: sources at sb + src_k
+// + soff (src_0 = s0, src_k = s_aux[k - 1]), optional f32 atom at ab + aoff,
+// destinations at db + dst_d + doff (dst_0 = d0, dst_d = s_aux[ns - 1 + d - 1]).
 template <int DT>
 __device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uint64_t s0,
                                                 const uint64_t* s_aux, int ns, uint64_t soff,
@@ -850,96 +810,89 @@ __device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uin
                                                 char* __restrict__ db, uint64_t d0, int nd,
                                                 uint64_t doff, uint32_t len, uint32_t lane,
                                                 bool& bad, uint32_t& bad_e) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   const char* sp = sb + s0 + soff;
   const uint32_t ps = (uint32_t)((reinterpret_cast<uintptr_t>(sp) >> 2) & 3);
-  const uint32_t nsv = (ps + len + 3) >> 2;
+  const uint32_t nsv = (ps + len + 3) >> 2;  // <= 32 * kRU: the segment is cut on this grid
+  const char* sv = sp - 4 * ps;
   float4 v[kRU];
 #pragma unroll
   for (int u = 0; u < kRU; ++u) {
     const uint32_t I = lane + 32u * u;
     v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (I < nsv) v[u] = ld_stream4(sp - 4 * ps + 16ull * I);
+    if (I < nsv) v[u] = ld_stream4(sv + 16ull * I);
   }
   for (int k = 1; k < ns; ++k) {
-    const char* rp = sb + s_aux[k - 1] + soff - 4 * ps;
+    const char* rp = sb + s_aux[k - 1] + soff;
+    const bool on_grid = ((reinterpret_cast<uintptr_t>(rp) >> 2) & 3) == ps;
 #pragma unroll
     for (int u = 0; u < kRU; ++u) {
       const uint32_t I = lane + 32u * u;
       if (I >= nsv) continue;
-      const float4 w = ld_stream4(rp + 16ull * I);
-      // first differing element of this vector inside [0, len)
-      const uint32_t x[4] = {bits_of(v[u].x) ^ bits_of(w.x), bits_of(v[u].y) ^ bits_of(w.y),
-                             bits_of(v[u].z) ^ bits_of(w.z), bits_of(v[u].w) ^ bits_of(w.w)};
+      if (on_grid) {
+        const float4 w = ld_stream4(rp - 4 * ps + 16ull * I);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int e = 4 * (int)I - (int)ps + c;
-        if (x[c] && e >= 0 && e < (int)len) { bad = true; bad_e = min(bad_e, (uint32_t)e); }
+        for (int c = 0; c < 4; ++c) {
+          const int e = 4 * (int)I - (int)ps + c;
+          if (bits_of(comp4(v[u], c)) != bits_of(comp4(w, c)) && e >= 0 && e < (int)len) {
+            bad = true;
+            bad_e = min(bad_e, (uint32_t)e);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int e = 4 * (int)I - (int)ps + c;
+          if (e >= 0 && e < (int)len && bits_of(ld_stream1(rp + 4ll * e)) != bits_of(comp4(v[u], c))) {
+            bad = true;
+            bad_e = min(bad_e, (uint32_t)e);
+          }
+        }
       }
     }
   }
-  if (atom_on) realign_store<UCP_DT_F32>(ab + aoff, v, ps, len, lane, sp);
+  // destination phases (warp-uniform): the neighbour round only if one differs
+  uint32_t differ = atom_on ? (uint32_t)((reinterpret_cast<uintptr_t>(ab + aoff) >> 2) & 3) ^ ps : 0u;
   for (int d = 0; d < nd; ++d)
-    realign_store<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + doff, v, ps, len, lane, sp);
-}
-
-// every replica of the run on the primary's 16-B grid (the realign path)
-__device__ __forceinline__ bool replicas_on_grid(uint64_t s0, const uint64_t* s_aux, int ns) {
-  bool same = true;
-  for (int k = 1; k < ns; ++k) same &= ((s_aux[k - 1] - s0) & 15) == 0;
-  return same;
-}
-
-// Phase-mismatched COPY runs of the unfused path whose replicas do not share
-// one grid: staged through shared memory (aligned 16-B loads on each
-// replica's phase grid, aligned stores on each destination's).
-template <int DT>
-__device__ __noinline__ void move_tile_staged(const TileGeom& g, const ucp_run& r,
-                                              const uint64_t* s_aux, const char* __restrict__ sb,
-                                              char* __restrict__ db, uint32_t run_idx,
-                                              ucp_status* st, float* sbuf) {
-  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  const int ns = r.n_src, nd = r.n_dst;
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* buf = sbuf + warp * 2 * kStage;
-  float* rep = buf + kStage;
-  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
-    const uint32_t rr = it / g.spr;
-    const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
-    const uint32_t len = min(cs + kSeg, g.col0 + g.nc) - cs;
-    const uint32_t row = g.row0 + rr;
-    const uint64_t srow = (uint64_t)row * r.src_pitch + cs;
-    const uint64_t drow = (uint64_t)row * r.dst_pitch + cs;
-    bool bad = false;
-    uint32_t bad_e = 0xffffffffu;
-    __syncwarp();
-    const int off = stage_in(buf, sb + r.src + 4 * srow, len, lane);
-    for (int k = 1; k < ns; ++k) {
-      const int offk = stage_in(rep, sb + s_aux[k - 1] + 4 * srow, len, lane);
-      __syncwarp();
-      for (uint32_t e = lane; e < len; e += 32)
-        if (bits_of(rep[e + offk]) != bits_of(buf[e + off])) { bad = true; bad_e = min(bad_e, e); }
-      __syncwarp();
+    differ |= (uint32_t)(((reinterpret_cast<uintptr_t>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + doff)) / ESZ) & 3) ^ ps;
+  float4 nx[kRU];
+  const int from = (int)((lane + 1) & 31);
+#pragma unroll
+  for (int u = 0; u < kRU; ++u) {
+    nx[u] = v[u];
+    if (differ) {
+      const float4 give = (lane == 0 && u + 1 < kRU) ? v[u + 1] : v[u];
+      nx[u].x = __shfl_sync(0xffffffffu, give.x, from);
+      nx[u].y = __shfl_sync(0xffffffffu, give.y, from);
+      nx[u].z = __shfl_sync(0xffffffffu, give.z, from);
+      nx[u].w = __shfl_sync(0xffffffffu, give.w, from);
     }
-    __syncwarp();
-    for (int d = 0; d < nd; ++d)
-      stage_out<DT>(db + (d == 0 ? r.dst : s_aux[ns - 1 + d - 1]) + (uint64_t)ESZ * drow, buf, off,
-                    len, lane);
-    report(bad, row * r.cols + cs + bad_e, run_idx, st);
   }
+  if (atom_on) realign_store<UCP_DT_F32>(ab + aoff, v, nx, ps, len, lane, sp);
+  for (int d = 0; d < nd; ++d)
+    realign_store<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + doff, v, nx, ps, len, lane, sp);
+}
+
+// phase (0..3) of element `at` of a source run on its 16-B grid
+__device__ __forceinline__ uint32_t src_phase(const char* sb, uint64_t s0, uint64_t at) {
+  return (uint32_t)(((reinterpret_cast<uintptr_t>(sb + s0) >> 2) + at) & 3);
 }
 
 template <int DT>
 __device__ __forceinline__ void move_tile_realign(const TileGeom& g, const ucp_run& r,
-                                               const uint64_t* s_aux, const char* __restrict__ sb,
-                                               char* __restrict__ db, uint32_t run_idx,
-                                               ucp_status* st) {
+                                                  const uint64_t* s_aux, const char* __restrict__ sb,
+                                                  char* __restrict__ db, uint32_t run_idx,
+                                                  ucp_status* st) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
-    const uint32_t rr = it / g.spr;
-    const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
-    const uint32_t len = min(cs + kSeg, g.col0 + g.nc) - cs;
+  const uint32_t spr = realign_spr(g.nc), n_items = g.nr * spr;
+  for (uint32_t it = warp; it < n_items; it += kWarps) {
+    const uint32_t rr = it / spr;
     const uint32_t row = g.row0 + rr;
+    uint32_t cs, len;
+    const uint32_t p0 = src_phase(sb, r.src, (uint64_t)row * r.src_pitch + g.col0);
+    if (!realign_seg(it - rr * spr, g.nc, p0, cs, len)) continue;  // warp-uniform
+    cs += g.col0;
     bool bad = false;
     uint32_t bad_e = 0xffffffffu;
     realign_segment<DT>(sb, r.src, s_aux, r.n_src, 4ull * ((uint64_t)row * r.src_pitch + cs),
@@ -958,18 +911,11 @@ __device__ __forceinline__ void realign_body(const ucp_run* __restrict__ runs,
   __shared__ __align__(16) ucp_run s_run;
   __shared__ uint4 s_t;
   __shared__ uint64_t s_aux[kMaxAux];
-  __shared__ __align__(16) float s_stage[kWarps * 2 * kStage];
   const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
   const TileGeom g = tile_prologue(aux, tile, s_run, s_aux);
-  if (replicas_on_grid(s_run.src, s_aux, s_run.n_src)) {
-    if (s_run.dtype == UCP_DT_F32) move_tile_realign<UCP_DT_F32>(g, s_run, s_aux, sb, db, tile.run, st);
-    else if (s_run.dtype == UCP_DT_BF16) move_tile_realign<UCP_DT_BF16>(g, s_run, s_aux, sb, db, tile.run, st);
-    else move_tile_realign<UCP_DT_F16>(g, s_run, s_aux, sb, db, tile.run, st);
-  } else {
-    if (s_run.dtype == UCP_DT_F32) move_tile_staged<UCP_DT_F32>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
-    else if (s_run.dtype == UCP_DT_BF16) move_tile_staged<UCP_DT_BF16>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
-    else move_tile_staged<UCP_DT_F16>(g, s_run, s_aux, sb, db, tile.run, st, s_stage);
-  }
+  if (s_run.dtype == UCP_DT_F32) move_tile_realign<UCP_DT_F32>(g, s_run, s_aux, sb, db, tile.run, st);
+  else if (s_run.dtype == UCP_DT_BF16) move_tile_realign<UCP_DT_BF16>(g, s_run, s_aux, sb, db, tile.run, st);
+  else move_tile_realign<UCP_DT_F16>(g, s_run, s_aux, sb, db, tile.run, st);
 }
 
 // ---------------------------------------------------------------- ops kernels
@@ -1310,141 +1256,27 @@ __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f16(UCP_FUSE
 }
 
 // Fused cells whose sources, atomic and targets do not share one 16-B
-// phase (ZeRO partitions of dp = 3, 5, ...): the same single pass with
-// coalesced 4-B accesses -- lane l takes elements l, l + 32, ... of a
-// 512-element row segment, 4 per lane per step for memory-level
-// parallelism.
+// phase (ZeRO partitions of dp = 3, 5, ...): the same single pass, realigned
+// in registers (realign_segment) on segments cut on the primary's grid.
 template <int DT>
-__device__ __forceinline__ void fused_tile_scalar(const uint64_t* __restrict__ aux,
-                                                  const ucp_tile& tile, const ucp_xrun& s_run,
-                                                  uint64_t* s_aux, const char* __restrict__ sb,
-                                                  char* __restrict__ ab, char* __restrict__ db,
-                                                  ucp_status* st) {
-  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  constexpr int U = UCP_SCALAR_U;
-  const int ns = s_run.n_src, nd = s_run.n_dst;
-  const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
-  if (n_aux > 0) {
-    for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
-    __syncthreads();
-  }
-  uint32_t nrows, nc;
-  if (s_run.flags & UCP_RUN_ROWSPLIT) { nrows = 1; nc = tile.count; }
-  else { nrows = tile.count; nc = s_run.cols; }
-  const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nrows * spr;
-  const uint64_t s0 = s_run.src, a0 = s_run.atom, d0 = s_run.dst;
-  const bool atom_on = a0 != ~0ull;
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t it = warp; it < n_items; it += kWarps) {
-    const uint32_t rr = it / spr;
-    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
-    const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
-    const uint32_t row = tile.row0 + rr;
-    const uint64_t srow = (uint64_t)row * s_run.src_pitch + cs;
-    const uint64_t arow = (uint64_t)row * s_run.atom_pitch + cs;
-    const uint64_t drow = (uint64_t)row * s_run.dst_pitch + cs;
-    bool bad = false;
-    uint32_t bad_e = 0xffffffffu;
-    for (uint32_t base = 0; base < len; base += 32u * U) {
-      float x[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t e = base + lane + 32u * u;
-        if (e < len) x[u] = ld_stream1(sb + s0 + 4 * (srow + e));
-      }
-      for (int k = 1; k < ns; ++k) {
-        const char* pk = sb + s_aux[k - 1];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t e = base + lane + 32u * u;
-          if (e < len && bits_of(ld_stream1(pk + 4 * (srow + e))) != bits_of(x[u])) {
-            bad = true;
-            bad_e = min(bad_e, e);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t e = base + lane + 32u * u;
-        if (e >= len) continue;
-        if (atom_on) *reinterpret_cast<float*>(ab + a0 + 4 * (arow + e)) = x[u];
-        for (int d = 0; d < nd; ++d)
-          store1<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + (uint64_t)ESZ * (drow + e), x[u]);
-      }
-    }
-    report(bad, row * s_run.cols + cs + bad_e, tile.run, st);
-  }
-}
-
-template <int DT>
-__device__ __noinline__ void fused_tile_staged(const uint64_t* __restrict__ aux,
-                                                  const ucp_tile& tile, const ucp_xrun& s_run,
-                                                  uint64_t* s_aux, const char* __restrict__ sb,
-                                                  char* __restrict__ ab, char* __restrict__ db,
-                                                  ucp_status* st, float* sbuf,
-                                                  bool preloaded = false) {
-  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
-  const int ns = s_run.n_src, nd = s_run.n_dst;
-  const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
-  if (n_aux > 0 && !preloaded) {
-    for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
-    __syncthreads();
-  }
-  uint32_t nrows, nc;
-  if (s_run.flags & UCP_RUN_ROWSPLIT) { nrows = 1; nc = tile.count; }
-  else { nrows = tile.count; nc = s_run.cols; }
-  const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nrows * spr;
-  const uint64_t s0 = s_run.src, a0 = s_run.atom, d0 = s_run.dst;
-  const bool atom_on = a0 != ~0ull;
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* buf = sbuf + warp * 2 * kStage;  // primary | replica
-  float* rep = buf + kStage;
-  for (uint32_t it = warp; it < n_items; it += kWarps) {
-    const uint32_t rr = it / spr;
-    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
-    const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
-    const uint32_t row = tile.row0 + rr;
-    const uint64_t srow = (uint64_t)row * s_run.src_pitch + cs;
-    const uint64_t arow = (uint64_t)row * s_run.atom_pitch + cs;
-    const uint64_t drow = (uint64_t)row * s_run.dst_pitch + cs;
-    bool bad = false;
-    uint32_t bad_e = 0xffffffffu;
-    __syncwarp();  // the previous segment's readers are done with buf
-    const int off = stage_in(buf, sb + s0 + 4 * srow, len, lane);
-    for (int k = 1; k < ns; ++k) {
-      const int offk = stage_in(rep, sb + s_aux[k - 1] + 4 * srow, len, lane);
-      __syncwarp();
-      for (uint32_t e = lane; e < len; e += 32)
-        if (bits_of(rep[e + offk]) != bits_of(buf[e + off])) { bad = true; bad_e = min(bad_e, e); }
-      __syncwarp();  // rep is refilled by the next replica
-    }
-    __syncwarp();
-    if (atom_on) stage_out<UCP_DT_F32>(ab + a0 + 4 * arow, buf, off, len, lane);
-    for (int d = 0; d < nd; ++d)
-      stage_out<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + (uint64_t)ESZ * drow, buf, off,
-                    len, lane);
-    report(bad, row * s_run.cols + cs + bad_e, tile.run, st);
-  }
-}
-
-template <int DT>
-__device__ __forceinline__ void fused_tile_realign(const uint64_t* __restrict__ aux,
-                                                const ucp_tile& tile, const ucp_xrun& s_run,
-                                                uint64_t* s_aux, const char* __restrict__ sb,
-                                                char* __restrict__ ab, char* __restrict__ db,
-                                                ucp_status* st) {
+__device__ __forceinline__ void fused_tile_realign(const ucp_tile& tile, const ucp_xrun& s_run,
+                                                   const uint64_t* s_aux, const char* __restrict__ sb,
+                                                   char* __restrict__ ab, char* __restrict__ db,
+                                                   ucp_status* st) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   uint32_t nrows, nc;
   if (s_run.flags & UCP_RUN_ROWSPLIT) { nrows = 1; nc = tile.count; }
   else { nrows = tile.count; nc = s_run.cols; }
-  const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nrows * spr;
+  const uint32_t spr = realign_spr(nc), n_items = nrows * spr;
   const bool atom_on = s_run.atom != ~0ull;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t it = warp; it < n_items; it += kWarps) {
     const uint32_t rr = it / spr;
-    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
-    const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
     const uint32_t row = tile.row0 + rr;
+    uint32_t cs, len;
+    const uint32_t p0 = src_phase(sb, s_run.src, (uint64_t)row * s_run.src_pitch + tile.col0);
+    if (!realign_seg(it - rr * spr, nc, p0, cs, len)) continue;  // warp-uniform
+    cs += tile.col0;
     bool bad = false;
     uint32_t bad_e = 0xffffffffu;
     realign_segment<DT>(sb, s_run.src, s_aux, s_run.n_src,
@@ -1457,44 +1289,23 @@ __device__ __forceinline__ void fused_tile_realign(const uint64_t* __restrict__ 
   }
 }
 
-// The GENERAL class of fused tables: phase-mismatched cells, realigned in
-// registers (shared-memory staging when replicas sit on different 16-B
-// grids); each CTA dispatches on its run's target dtype.
-#ifndef UCP_REALIGN
-#define UCP_REALIGN 1  // 0: phase-mismatched fused cells always take the shared-memory staging
-#endif
-__global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) reshard_fused_realign(UCP_FUSED_ARGS) {
+// The GENERAL class of fused tables: phase-mismatched cells; each CTA
+// dispatches on its run's target dtype.
+__global__ void __launch_bounds__(kThreads, UCP_REALIGN_MINB) reshard_fused_realign(UCP_FUSED_ARGS) {
   (void)n_tiles;
   __shared__ __align__(16) ucp_xrun s_run;
   __shared__ uint4 s_t;
   __shared__ uint64_t s_aux[kMaxAux];
-#if UCP_STAGED
-  __shared__ __align__(16) float s_stage[kWarps * 2 * kStage];
-#endif
   const ucp_tile tile = tile_begin(runs, rt, r0, nr, blockIdx.x, s_run, s_t);
-#if UCP_STAGED
-  {
-    const int ns = s_run.n_src, nd = s_run.n_dst;
-    const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
+  const int ns = s_run.n_src, nd = s_run.n_dst;
+  const int n_aux = (ns > 0 ? ns - 1 : 0) + (nd > 0 ? nd - 1 : 0);
+  if (n_aux > 0) {
     for (int i = threadIdx.x; i < n_aux && i < kMaxAux; i += kThreads) s_aux[i] = aux[s_run.aux + i];
     __syncthreads();
   }
-  if (UCP_REALIGN && replicas_on_grid(s_run.src, s_aux, s_run.n_src)) {
-    if (s_run.dtype == UCP_DT_F32) fused_tile_realign<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st);
-    else if (s_run.dtype == UCP_DT_BF16) fused_tile_realign<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st);
-    else fused_tile_realign<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st);
-  } else if (s_run.dtype == UCP_DT_F32) {
-    fused_tile_staged<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage, true);
-  } else if (s_run.dtype == UCP_DT_BF16) {
-    fused_tile_staged<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage, true);
-  } else {
-    fused_tile_staged<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st, s_stage, true);
-  }
-#else
-  if (s_run.dtype == UCP_DT_F32) fused_tile_scalar<UCP_DT_F32>(aux, tile, s_run, s_aux, sb, ab, db, st);
-  else if (s_run.dtype == UCP_DT_BF16) fused_tile_scalar<UCP_DT_BF16>(aux, tile, s_run, s_aux, sb, ab, db, st);
-  else fused_tile_scalar<UCP_DT_F16>(aux, tile, s_run, s_aux, sb, ab, db, st);
-#endif
+  if (s_run.dtype == UCP_DT_F32) fused_tile_realign<UCP_DT_F32>(tile, s_run, s_aux, sb, ab, db, st);
+  else if (s_run.dtype == UCP_DT_BF16) fused_tile_realign<UCP_DT_BF16>(tile, s_run, s_aux, sb, ab, db, st);
+  else fused_tile_realign<UCP_DT_F16>(tile, s_run, s_aux, sb, ab, db, st);
 }
 
 // ---------------------------------------------------------------- entry kernels
@@ -1519,10 +1330,10 @@ __global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_bf16(UCP_MOVE
 __global__ void __launch_bounds__(kThreads, UCP_MINB) load_scatter_f16(UCP_MOVE_ARGS) {
   vec_body<UCP_DT_F16>(runs, aux, rt, r0, nr, sb, db, st);
 }
-__global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) convert_gather_realign(UCP_MOVE_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_REALIGN_MINB) convert_gather_realign(UCP_MOVE_ARGS) {
   realign_body(runs, aux, rt, r0, nr, sb, db, st);
 }
-__global__ void __launch_bounds__(kThreads, UCP_SCALAR_MINB) load_scatter_realign(UCP_MOVE_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_REALIGN_MINB) load_scatter_realign(UCP_MOVE_ARGS) {
   realign_body(runs, aux, rt, r0, nr, sb, db, st);
 }
 __global__ void __launch_bounds__(kThreads, UCP_OPS_MINB) convert_gather_ops(UCP_MOVE_ARGS) {

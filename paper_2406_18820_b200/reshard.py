@@ -414,32 +414,50 @@ class ReshardPlan:
 
     # ------------------------------------------------------------------ host-streamed
 
+    _PACK_CHUNK = 16 << 20  # bytes per host copy job: big fragments spread over the threads
+
+    def _pack_jobs(self, shards: dict) -> list:
+        """Validated copy jobs [(arena byte offset, uint8 view)] per window, in
+        window order, big fragments cut into _PACK_CHUNK pieces."""
+        from ._errors import ShapeError
+
+        per_win = []
+        for W in self.windows:
+            jobs = []
+            for g, i, m, off, n in W.src_frags:
+                a = np.ascontiguousarray(shards[g][i], dtype=np.float32).reshape(-1)
+                if a.size != n:
+                    raise ShapeError(f"rank {g} {m.param}.{m.kind}: {a.size} elements, want {n}")
+                b = a.view(np.uint8)
+                at = W.src_base + off
+                for c in range(0, max(b.size, 1), self._PACK_CHUNK):
+                    jobs.append((at + c, b[c:c + self._PACK_CHUNK]))
+            per_win.append(jobs)
+        return per_win
+
+    def _pack_pool(self, threads: int = 16):
+        pool = getattr(self, "_pool", None)
+        if pool is None:
+            from concurrent.futures import ThreadPoolExecutor
+
+            pool = self._pool = ThreadPoolExecutor(max(1, threads), thread_name_prefix="ucp-pack")
+        return pool
+
     def pack_host(self, shards: dict, pinned: torch.Tensor | None = None,
                   threads: int = 16) -> torch.Tensor:
         """Copy {g: [array per source record]} into a pinned source arena
         (the plan's own, reused across calls, unless ``pinned`` is given);
         the copies run on ``threads`` host threads (numpy releases the GIL)."""
-        from ._errors import ShapeError
-
         host = pinned if pinned is not None else self._pinned("src", self.src_total)
         hv = host.numpy()
-        jobs = []
-        for W in self.windows:
-            for g, i, m, off, n in W.src_frags:
-                a = np.ascontiguousarray(shards[g][i], dtype=np.float32).reshape(-1)
-                if a.size != n:
-                    raise ShapeError(f"rank {g} {m.param}.{m.kind}: {a.size} elements, want {n}")
-                jobs.append((W.src_base + off, a))
+        jobs = [j for w in self._pack_jobs(shards) for j in w]
 
         def copy(job):
-            at, a = job
-            hv[at:at + a.nbytes] = a.view(np.uint8)
+            at, b = job
+            hv[at:at + b.size] = b
 
         if threads > 1 and len(jobs) > 1:
-            from concurrent.futures import ThreadPoolExecutor
-
-            with ThreadPoolExecutor(min(threads, len(jobs))) as pool:
-                list(pool.map(copy, jobs))
+            list(self._pack_pool(threads).map(copy, jobs))
         else:
             for j in jobs:
                 copy(j)
@@ -467,7 +485,7 @@ class ReshardPlan:
 
     def stream_host(self, host_src: torch.Tensor, host_tgt: torch.Tensor | None, windows=None,
                     streams=None, slots: int | None = None,
-                    dev_tgt: torch.Tensor | None = None) -> None:
+                    dev_tgt: torch.Tensor | None = None, ready=None) -> None:
         """Pinned host source arena -> device -> pinned host target arena,
         multi-buffered (``slots`` device slots per direction, default
         ``self.host_slots``) over windows on three streams. Asynchronous:
@@ -475,7 +493,12 @@ class ReshardPlan:
 
         ``dev_tgt`` (a device byte tensor of ``tgt_total`` bytes, host_tgt
         None): the target fragments stay in HBM at their arena offsets --
-        a resume straight onto the GPU; only the sources cross PCIe."""
+        a resume straight onto the GPU; only the sources cross PCIe.
+
+        ``ready(i)``, if given, is called (and must return) before window
+        i's H2D is enqueued: the host producer of window i's source bytes
+        (run_host's packing threads) overlaps the transfers of the windows
+        before it."""
         wins = self.windows if windows is None else windows
         s_in, s_cmp, s_out = streams or self.host_streams()
         ns = max(2, slots or self.host_slots)
@@ -499,6 +522,8 @@ class ReshardPlan:
         ev_out = [torch.cuda.Event() for _ in wins]
         for i, W in enumerate(wins):
             slot = i % ns
+            if ready is not None:
+                ready(i)
             with torch.cuda.stream(s_in):
                 if i >= ns:
                     s_in.wait_event(ev_cmp[i - ns])
@@ -539,7 +564,7 @@ class ReshardPlan:
 
     def run_pinned(self, host_src: torch.Tensor, host_tgt: torch.Tensor | None, streams=None,
                    status_out: torch.Tensor | None = None, sync: bool = True,
-                   dev_tgt: torch.Tensor | None = None) -> None:
+                   dev_tgt: torch.Tensor | None = None, ready=None) -> None:
         """Public zero-copy entry: pinned host source arena (``pack_host``
         layout) -> H2D -> fused convert+load -> D2H into the pinned host
         target arena (``unpack_host`` layout), double-buffered over windows.
@@ -551,7 +576,7 @@ class ReshardPlan:
         PaddingError, ...); without it the caller checks ``status_out``
         later with ``check_status_word``."""
         streams = streams or self.host_streams()
-        self.stream_host(host_src, host_tgt, None, streams, dev_tgt=dev_tgt)
+        self.stream_host(host_src, host_tgt, None, streams, dev_tgt=dev_tgt, ready=ready)
         if status_out is not None:
             with torch.cuda.stream(streams[2]):
                 status_out.copy_(self.status.t, non_blocking=True)
@@ -574,11 +599,33 @@ class ReshardPlan:
 
     def run_host(self, shards: dict) -> dict:
         """End-to-end in-memory reshard of host arrays; returns target arrays
-        per rank in canonical record order."""
-        host_src = self.pack_host(shards)
+        per rank in canonical record order. Packing into the pinned arena is
+        pipelined with the transfers: the host threads copy window by window
+        (in window order) while the streams move and reshard the windows
+        already packed."""
+        host_src = self._pinned("src", self.src_total)
+        jobs = self._pack_jobs(shards)  # validates every fragment before any work
         host_tgt = self._target_arena()
+        hv = host_src.numpy()
+
+        def copy(job):
+            at, b = job
+            hv[at:at + b.size] = b
+
+        pool = self._pack_pool()
+        futs = [[pool.submit(copy, j) for j in w] for w in jobs]
+
+        def ready(i):
+            for f in futs[i]:
+                f.result()
+
         self.status.reset()
-        self.run_pinned(host_src, host_tgt)
+        try:
+            self.run_pinned(host_src, host_tgt, ready=ready)
+        finally:
+            for w in futs:  # never leave copies running into a reused arena
+                for f in w:
+                    f.cancel() or f.exception()
         return self.unpack_host(host_tgt)
 
     def _check_windows(self, host_src=None) -> None:
