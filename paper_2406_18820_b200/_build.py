@@ -100,8 +100,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
     sid = kernel_id()
     if not force and embedded_id(OUT) == sid:
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, f'-DUCP_BUILD_ID="{sid}"', "-I", os.path.join(ROOT, "include"),
-           SRC, "-o", OUT + ".tmp"]
+    # UCP_NVCC_EXTRA: -D switches for A/B experiments on a GPU box (with
+    # force=True); the shipped library is built without it
+    extra = os.environ.get("UCP_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, f'-DUCP_BUILD_ID="{sid}"', "-I",
+           os.path.join(ROOT, "include"), SRC, "-o", OUT + ".tmp"]
     _run(cmd, OUT, verbose)
     return OUT
 

@@ -726,39 +726,30 @@ __device__ __forceinline__ void vec_body(const ucp_run* __restrict__ runs,
 //
 // COPY pieces whose sources and destinations do not share one 16-B phase
 // (ZeRO partitions of dp = 3, 5, ... start at k * ceil(n / dp) elements).
-// Each warp moves a row segment at vector width, with no shared memory:
-//  * segments are cut on the primary source's 16-B grid (a tile row's first
-//    segment ends at a grid boundary), so a 512-element segment spans <= 128
-//    source vectors: kRU = 4 aligned 16-B loads per lane, as in the vector
-//    kernels, and the register budget of 4 CTAs per SM;
+// Each warp moves a 512-element row segment at vector width, with no shared
+// memory. Segments are cut on the tile's column grid (like the vector
+// kernels), so the atomic tensor -- written by every fused cell -- is
+// stored in whole aligned vectors; the primary source is then read on its
+// own 16-B grid:
+//  * a segment spans <= 129 source vectors: lane l, slot u holds vector
+//    I = l + 32u (kRU = 4 aligned 16-B loads per lane, as in the vector
+//    kernels, within 64 registers = 4 CTAs per SM); the rare 129th vector is
+//    loaded by lane 31 alone as its right neighbour;
+//  * a lane's right neighbour vector I + 1 comes from one round of warp
+//    shuffles per segment (lane 31 takes lane 0's next slot), shared by the
+//    atomic and every destination, moving only the components the largest
+//    shift reads;
 //  * replicas on the primary's grid are loaded the same way and compared in
 //    registers; a replica on another grid (hand-made layouts only) is
 //    compared with coalesced 4-B loads;
-//  * a lane's right neighbour vector I + 1 comes from one round of warp
-//    shuffles per segment (lane 31 takes lane 0's next slot), shared by the
-//    atomic and every destination, and skipped when no phase differs;
 //  * destination d with phase pd writes its aligned vector J = I + kappa as
 //    funnel(v_I, v_I+1, (ps - pd) & 3), plus <= 3 head and <= 3 tail scalars.
 constexpr int kRU = kVec;
+#ifndef UCP_REALIGN_TEMPLATED
+#define UCP_REALIGN_TEMPLATED 0  // 1: store loop instantiated per shift (no selects; spills at 64 regs)
+#endif
 
-// Segment k of a tile row of nc elements whose element 0 sits at phase p0
-// (0..3) of the primary source's 16-B grid: [start, start + len), cut at grid
-// boundaries. False for the empty last segment of a row that needs fewer.
-__device__ __forceinline__ bool realign_seg(uint32_t k, uint32_t nc, uint32_t p0, uint32_t& start,
-                                            uint32_t& len) {
-  const uint32_t lo = k * kSeg;
-  const uint32_t s = lo > p0 ? lo - p0 : 0;
-  const uint32_t e = min(nc, lo + kSeg - p0);
-  if (s >= e) return false;
-  start = s;
-  len = e - s;
-  return true;
-}
-
-// segments per tile row of nc elements at any phase
-__device__ __forceinline__ uint32_t realign_spr(uint32_t nc) { return (nc + 3 + kSeg - 1) / kSeg; }
-
-__device__ __forceinline__ float4 funnel4(const float4& a, const float4& b, uint32_t d) {
+__device__ __forceinline__ float4 funnel4r(const float4& a, const float4& b, uint32_t d) {
   switch (d) {
     case 0: return a;
     case 1: return make_float4(a.y, a.z, a.w, b.x);
@@ -767,8 +758,30 @@ __device__ __forceinline__ float4 funnel4(const float4& a, const float4& b, uint
   }
 }
 
+template <int D>
+__device__ __forceinline__ float4 funnel4(const float4& a, const float4& b) {
+  if constexpr (D == 0) return a;
+  else if constexpr (D == 1) return make_float4(a.y, a.z, a.w, b.x);
+  else if constexpr (D == 2) return make_float4(a.z, a.w, b.x, b.y);
+  else return make_float4(a.w, b.x, b.y, b.z);
+}
+
 __device__ __forceinline__ float comp4(const float4& a, int c) {
   return c == 0 ? a.x : c == 1 ? a.y : c == 2 ? a.z : a.w;
+}
+
+// Aligned destination vectors J0..J1 of one destination: lane slot u holds
+// source vector I = lane + 32u and writes J = I + kappa.
+template <int DT, int D>
+__device__ __forceinline__ void realign_vecs(char* dv, const float4 (&v)[kRU],
+                                             const float4 (&nx)[kRU], int kappa, int J0, int J1,
+                                             uint32_t lane) {
+  constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+#pragma unroll
+  for (int u = 0; u < kRU; ++u) {
+    const int J = (int)(lane + 32u * u) + kappa;
+    if (J >= J0 && J <= J1) store4<DT>(dv + (size_t)ESZ * 4 * J, funnel4<D>(v[u], nx[u]));
+  }
 }
 
 // Store segment elements [0, len) to p (element 0's address) from the
@@ -781,16 +794,25 @@ __device__ __forceinline__ void realign_store(char* p, const float4 (&v)[kRU],
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   const uintptr_t da = reinterpret_cast<uintptr_t>(p);
   const uint32_t pd = (uint32_t)((da / ESZ) & 3);
-  const uint32_t delta = (ps - pd) & 3u;
   const int kappa = ps >= pd ? 0 : 1;  // destination vector J = source vector I + kappa
   char* dv = p - (size_t)ESZ * pd;     // aligned destination vector 0
   const int J0 = pd ? 1 : 0;
   const int J1 = (int)((len + pd) >> 2) - 1;
+#if UCP_REALIGN_TEMPLATED
+  switch ((ps - pd) & 3u) {  // warp-uniform
+    case 0: realign_vecs<DT, 0>(dv, v, nx, kappa, J0, J1, lane); break;
+    case 1: realign_vecs<DT, 1>(dv, v, nx, kappa, J0, J1, lane); break;
+    case 2: realign_vecs<DT, 2>(dv, v, nx, kappa, J0, J1, lane); break;
+    default: realign_vecs<DT, 3>(dv, v, nx, kappa, J0, J1, lane); break;
+  }
+#else
+  const uint32_t delta = (ps - pd) & 3u;
 #pragma unroll
   for (int u = 0; u < kRU; ++u) {
     const int J = (int)(lane + 32u * u) + kappa;
-    if (J >= J0 && J <= J1) store4<DT>(dv + (size_t)ESZ * 4 * J, funnel4(v[u], nx[u], delta));
+    if (J >= J0 && J <= J1) store4<DT>(dv + (size_t)ESZ * 4 * J, funnel4r(v[u], nx[u], delta));
   }
+#endif
   const uint32_t head_end = min(4u * (uint32_t)J0 - pd, len);
   uint32_t tail_start = J1 >= J0 ? 4u * (uint32_t)(J1 + 1) - pd : head_end;
   if (tail_start < head_end) tail_start = head_end;
@@ -800,9 +822,37 @@ __device__ __forceinline__ void realign_store(char* p, const float4 (&v)[kRU],
   }
 }
 
-// One row segment [0, len), cut on the primary's grid: sources at sb + src_k
-// + soff (src_0 = s0, src_k = s_aux[k - 1]), optional f32 atom at ab + aoff,
-// destinations at db + dst_d + doff (dst_0 = d0, dst_d = s_aux[ns - 1 + d - 1]).
+// Compare this lane's copy of source vector I (elements 4I - ps + c, those in
+// [0, len)) with replica bits w.
+__device__ __forceinline__ void realign_cmp(const float4& v, const float4& w, uint32_t I,
+                                            uint32_t ps, uint32_t len, bool& bad, uint32_t& bad_e) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int e = 4 * (int)I - (int)ps + c;
+    if (bits_of(comp4(v, c)) != bits_of(comp4(w, c)) && e >= 0 && e < (int)len) {
+      bad = true;
+      bad_e = min(bad_e, (uint32_t)e);
+    }
+  }
+}
+
+// The same against a replica on another 16-B grid, with 4-B loads.
+__device__ __forceinline__ void realign_cmp_scalar(const float4& v, const char* rp, uint32_t I,
+                                                   uint32_t ps, uint32_t len, bool& bad,
+                                                   uint32_t& bad_e) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int e = 4 * (int)I - (int)ps + c;
+    if (e >= 0 && e < (int)len && bits_of(ld_stream1(rp + 4ll * e)) != bits_of(comp4(v, c))) {
+      bad = true;
+      bad_e = min(bad_e, (uint32_t)e);
+    }
+  }
+}
+
+// One row segment [0, len <= kSeg): sources at sb + src_k + soff (src_0 = s0,
+// src_k = s_aux[k - 1]), optional f32 atom at ab + aoff, destinations at
+// db + dst_d + doff (dst_0 = d0, dst_d = s_aux[ns - 1 + d - 1]).
 template <int DT>
 __device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uint64_t s0,
                                                 const uint64_t* s_aux, int ns, uint64_t soff,
@@ -811,9 +861,10 @@ __device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uin
                                                 uint64_t doff, uint32_t len, uint32_t lane,
                                                 bool& bad, uint32_t& bad_e) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
+  constexpr uint32_t kLast = 32u * kRU;  // index of the 129th source vector
   const char* sp = sb + s0 + soff;
   const uint32_t ps = (uint32_t)((reinterpret_cast<uintptr_t>(sp) >> 2) & 3);
-  const uint32_t nsv = (ps + len + 3) >> 2;  // <= 32 * kRU: the segment is cut on this grid
+  const uint32_t nsv = (ps + len + 3) >> 2;  // <= kLast + 1
   const char* sv = sp - 4 * ps;
   float4 v[kRU];
 #pragma unroll
@@ -822,60 +873,47 @@ __device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uin
     v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (I < nsv) v[u] = ld_stream4(sv + 16ull * I);
   }
-  for (int k = 1; k < ns; ++k) {
-    const char* rp = sb + s_aux[k - 1] + soff;
-    const bool on_grid = ((reinterpret_cast<uintptr_t>(rp) >> 2) & 3) == ps;
-#pragma unroll
-    for (int u = 0; u < kRU; ++u) {
-      const uint32_t I = lane + 32u * u;
-      if (I >= nsv) continue;
-      if (on_grid) {
-        const float4 w = ld_stream4(rp - 4 * ps + 16ull * I);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int e = 4 * (int)I - (int)ps + c;
-          if (bits_of(comp4(v[u], c)) != bits_of(comp4(w, c)) && e >= 0 && e < (int)len) {
-            bad = true;
-            bad_e = min(bad_e, (uint32_t)e);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int e = 4 * (int)I - (int)ps + c;
-          if (e >= 0 && e < (int)len && bits_of(ld_stream1(rp + 4ll * e)) != bits_of(comp4(v[u], c))) {
-            bad = true;
-            bad_e = min(bad_e, (uint32_t)e);
-          }
-        }
-      }
-    }
+  // right neighbours (warp-uniform shift set): the shuffle round moves only
+  // the components the largest shift reads; lane 31 loads the 129th vector
+  uint32_t dmax = atom_on ? (ps - (uint32_t)((reinterpret_cast<uintptr_t>(ab + aoff) >> 2) & 3)) & 3u : 0u;
+  for (int d = 0; d < nd; ++d) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + doff);
+    dmax = max(dmax, (ps - (uint32_t)((a / ESZ) & 3)) & 3u);
   }
-  // destination phases (warp-uniform): the neighbour round only if one differs
-  uint32_t differ = atom_on ? (uint32_t)((reinterpret_cast<uintptr_t>(ab + aoff) >> 2) & 3) ^ ps : 0u;
-  for (int d = 0; d < nd; ++d)
-    differ |= (uint32_t)(((reinterpret_cast<uintptr_t>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + doff)) / ESZ) & 3) ^ ps;
+  const bool extra = nsv > kLast;  // warp-uniform
   float4 nx[kRU];
   const int from = (int)((lane + 1) & 31);
 #pragma unroll
   for (int u = 0; u < kRU; ++u) {
     nx[u] = v[u];
-    if (differ) {
-      const float4 give = (lane == 0 && u + 1 < kRU) ? v[u + 1] : v[u];
-      nx[u].x = __shfl_sync(0xffffffffu, give.x, from);
-      nx[u].y = __shfl_sync(0xffffffffu, give.y, from);
-      nx[u].z = __shfl_sync(0xffffffffu, give.z, from);
-      nx[u].w = __shfl_sync(0xffffffffu, give.w, from);
+    const float4 give = (lane == 0 && u + 1 < kRU) ? v[u + 1] : v[u];
+    if (dmax >= 1) nx[u].x = __shfl_sync(0xffffffffu, give.x, from);
+    if (dmax >= 2) nx[u].y = __shfl_sync(0xffffffffu, give.y, from);
+    if (dmax >= 3) nx[u].z = __shfl_sync(0xffffffffu, give.z, from);
+  }
+  if (extra && lane == 31) nx[kRU - 1] = ld_stream4(sv + 16ull * kLast);
+  for (int k = 1; k < ns; ++k) {
+    const char* rp = sb + s_aux[k - 1] + soff;
+    if (((reinterpret_cast<uintptr_t>(rp) >> 2) & 3) == ps) {
+      const char* rv = rp - 4 * ps;
+#pragma unroll
+      for (int u = 0; u < kRU; ++u) {
+        const uint32_t I = lane + 32u * u;
+        if (I < nsv) realign_cmp(v[u], ld_stream4(rv + 16ull * I), I, ps, len, bad, bad_e);
+      }
+      if (extra && lane == 31) realign_cmp(nx[kRU - 1], ld_stream4(rv + 16ull * kLast), kLast, ps, len, bad, bad_e);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kRU; ++u) {
+        const uint32_t I = lane + 32u * u;
+        if (I < nsv) realign_cmp_scalar(v[u], rp, I, ps, len, bad, bad_e);
+      }
+      if (extra && lane == 31) realign_cmp_scalar(nx[kRU - 1], rp, kLast, ps, len, bad, bad_e);
     }
   }
   if (atom_on) realign_store<UCP_DT_F32>(ab + aoff, v, nx, ps, len, lane, sp);
   for (int d = 0; d < nd; ++d)
     realign_store<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + doff, v, nx, ps, len, lane, sp);
-}
-
-// phase (0..3) of element `at` of a source run on its 16-B grid
-__device__ __forceinline__ uint32_t src_phase(const char* sb, uint64_t s0, uint64_t at) {
-  return (uint32_t)(((reinterpret_cast<uintptr_t>(sb + s0) >> 2) + at) & 3);
 }
 
 template <int DT>
@@ -885,14 +923,11 @@ __device__ __forceinline__ void move_tile_realign(const TileGeom& g, const ucp_r
                                                   ucp_status* st) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t spr = realign_spr(g.nc), n_items = g.nr * spr;
-  for (uint32_t it = warp; it < n_items; it += kWarps) {
-    const uint32_t rr = it / spr;
+  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
+    const uint32_t rr = it / g.spr;
+    const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, g.col0 + g.nc) - cs;
     const uint32_t row = g.row0 + rr;
-    uint32_t cs, len;
-    const uint32_t p0 = src_phase(sb, r.src, (uint64_t)row * r.src_pitch + g.col0);
-    if (!realign_seg(it - rr * spr, g.nc, p0, cs, len)) continue;  // warp-uniform
-    cs += g.col0;
     bool bad = false;
     uint32_t bad_e = 0xffffffffu;
     realign_segment<DT>(sb, r.src, s_aux, r.n_src, 4ull * ((uint64_t)row * r.src_pitch + cs),
@@ -1257,7 +1292,7 @@ __global__ void __launch_bounds__(kThreads, UCP_MINB) reshard_fused_f16(UCP_FUSE
 
 // Fused cells whose sources, atomic and targets do not share one 16-B
 // phase (ZeRO partitions of dp = 3, 5, ...): the same single pass, realigned
-// in registers (realign_segment) on segments cut on the primary's grid.
+// in registers (realign_segment).
 template <int DT>
 __device__ __forceinline__ void fused_tile_realign(const ucp_tile& tile, const ucp_xrun& s_run,
                                                    const uint64_t* s_aux, const char* __restrict__ sb,
@@ -1267,16 +1302,14 @@ __device__ __forceinline__ void fused_tile_realign(const ucp_tile& tile, const u
   uint32_t nrows, nc;
   if (s_run.flags & UCP_RUN_ROWSPLIT) { nrows = 1; nc = tile.count; }
   else { nrows = tile.count; nc = s_run.cols; }
-  const uint32_t spr = realign_spr(nc), n_items = nrows * spr;
+  const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nrows * spr;
   const bool atom_on = s_run.atom != ~0ull;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t it = warp; it < n_items; it += kWarps) {
     const uint32_t rr = it / spr;
+    const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
+    const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
     const uint32_t row = tile.row0 + rr;
-    uint32_t cs, len;
-    const uint32_t p0 = src_phase(sb, s_run.src, (uint64_t)row * s_run.src_pitch + tile.col0);
-    if (!realign_seg(it - rr * spr, nc, p0, cs, len)) continue;  // warp-uniform
-    cs += tile.col0;
     bool bad = false;
     uint32_t bad_e = 0xffffffffu;
     realign_segment<DT>(sb, s_run.src, s_aux, s_run.n_src,
