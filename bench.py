@@ -444,11 +444,14 @@ def e2e_to_hbm(eplan, host_src, streams, stream, steps: int):
     return a.elapsed_time(b) / steps
 
 
-def pcie_peaks(dev, stream, nbytes: int = 1 << 30, reps: int = 5) -> dict:
+def pcie_peaks(dev, stream, nbytes: int = 1 << 30, reps: int = 5, mix: float | None = None) -> dict:
     """Pinned cudaMemcpyAsync peaks of this process's GPU link, measured in
     the same run (the host staging stage is judged against them):
     H2D alone, D2H alone, and both at once on two streams (GB/s, best of
-    `reps`, CUDA events)."""
+    `reps`, CUDA events). ``mix`` = D2H bytes per H2D byte of the e2e step:
+    also time ``nbytes`` of H2D concurrently with ``mix * nbytes`` of D2H --
+    the step's own byte mix through the link with no compute, i.e. the
+    e2e step's transfer bound (link_roofline scales it to the step)."""
     import torch
 
     try:
@@ -490,9 +493,23 @@ def pcie_peaks(dev, stream, nbytes: int = 1 << 30, reps: int = 5) -> dict:
         d2h()
 
     t_in, t_out, t_both = timed(h2d), timed(d2h), timed(both)
-    return {"h2d_GBps": nbytes / t_in / GB, "d2h_GBps": nbytes / t_out / GB,
-            "bidir_GBps": 2 * nbytes / t_both / GB,
-            "how": f"pinned {nbytes >> 20} MiB cudaMemcpyAsync, best of {reps}, same process"}
+    out = {"h2d_GBps": nbytes / t_in / GB, "d2h_GBps": nbytes / t_out / GB,
+           "bidir_GBps": 2 * nbytes / t_both / GB,
+           "how": f"pinned {nbytes >> 20} MiB cudaMemcpyAsync, best of {reps}, same process"}
+    if mix is not None and mix > 0:
+        n_in = nbytes if mix <= 1 else int(nbytes / mix)
+        n_out = min(nbytes, int(n_in * mix))
+
+        def mixed():
+            with torch.cuda.stream(s1):
+                d_in[:n_in].copy_(h_in[:n_in], non_blocking=True)
+            with torch.cuda.stream(s2):
+                h_out[:n_out].copy_(d_out[:n_out], non_blocking=True)
+
+        out["mixed"] = {"d2h_per_h2d": n_out / n_in, "s_per_h2d_byte": timed(mixed) / n_in,
+                        "how": f"{n_in >> 20} MiB H2D concurrent with {n_out >> 20} MiB D2H "
+                               "(the e2e step's byte mix), no compute"}
+    return out
 
 
 def link_roofline(link: dict, h2d: int, d2h: int, ms: float) -> dict:
@@ -505,6 +522,12 @@ def link_roofline(link: dict, h2d: int, d2h: int, ms: float) -> dict:
     out.update({"achieved_GBps": (h2d + d2h) / t / GB, "h2d_GBps_in_step": h2d / t / GB,
                 "d2h_GBps_in_step": d2h / t / GB,
                 "frac": (h2d + d2h) / t / GB / link["bidir_GBps"]})
+    mx = link.get("mixed")
+    if mx:  # the step's transfers alone, at the measured mixed-direction rate
+        bound = mx["s_per_h2d_byte"] * h2d * 1e3
+        out["mixed"] = dict(mx, bound_ms=bound, frac=bound / ms,
+                            what="frac = (this step's H2D + D2H bytes through the link with no "
+                                 "compute, same mix) / step time: the e2e step's transfer roofline")
     return out
 
 
@@ -1048,7 +1071,7 @@ def run_ours(args):
                 eplan._check_windows(host_src)
             e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
             to_hbm_ms = e2e_to_hbm(eplan, host_src, streams, stream, args.e2e_steps)
-            link = pcie_peaks(dev, stream)
+            link = pcie_peaks(dev, stream, mix=eplan.tgt_total / max(1, eplan.src_total))
             S_e2e_local = eplan.state_bytes
             e2e_meta = {"h2d": int(eplan.src_total), "d2h": int(eplan.tgt_total),
                         "windows": len(eplan.windows), "names": names}
