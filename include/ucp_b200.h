@@ -200,8 +200,8 @@ int ucp_gen_state(uint64_t base, uint64_t start, uint64_t count, int abs_flag, f
  * class_info as for ucp_convert_gather, runs sorted by class. Classes
  * VEC_F32 / VEC_BF16 / VEC_F16 hold vector runs (UCP_RUN_VEC: one shared 16-B
  * phase) of one target dtype each; for fused tables the GENERAL slot holds
- * phase-mismatched cells (UCP_RUN_VEC clear, any target dtype), run on a
- * coalesced 4-B path (kernel reshard_fused_scalar).
+ * phase-mismatched cells (UCP_RUN_VEC clear, any target dtype), realigned in
+ * registers at vector width (kernel reshard_fused_realign).
  */
 int ucp_reshard_fused(const ucp_xrun* runs, int64_t n_runs, const uint64_t* aux,
                       const ucp_runtile* rt, const int64_t* class_info, const void* src_base,

@@ -955,8 +955,25 @@ __device__ __forceinline__ void realign_body(const ucp_run* __restrict__ runs,
 
 // ---------------------------------------------------------------- ops kernels
 
+#ifndef UCP_OPS_INLINE
+#define UCP_OPS_INLINE 0  // 1: the four op instantiations inlined into the kernel
+#endif
+#if UCP_OPS_INLINE
+#define UCP_OPS_TILE_ATTR __forceinline__
+#else
+#define UCP_OPS_TILE_ATTR __noinline__
+#endif
+#ifndef UCP_OPS_BYVAL
+#define UCP_OPS_BYVAL 1  // 1: Ctx passed by value (registers), 0: by reference (local memory)
+#endif
+#if UCP_OPS_BYVAL
+using OpsCtx = const Ctx;
+#else
+using OpsCtx = const Ctx&;
+#endif
+
 template <int OP>
-__device__ __noinline__ void ops_tile(const Ctx& c, const TileGeom g, ucp_status* st) {
+__device__ UCP_OPS_TILE_ATTR void ops_tile(OpsCtx c, const TileGeom g, ucp_status* st) {
   const uint32_t warp = threadIdx.x >> 5;
   for (uint32_t it = warp; it < g.n_items; it += kWarps) {
     const uint32_t rr = it / g.spr;

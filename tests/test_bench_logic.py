@@ -64,6 +64,11 @@ def test_link_roofline_and_peak_fallback(tmp_path, monkeypatch):
     r = bench.link_roofline(link, 10 ** 9, 10 ** 9, 40.0)
     assert r["achieved_GBps"] == pytest.approx(50.0) and r["frac"] == pytest.approx(0.5)
     assert bench.link_roofline({}, 1, 1, 1.0) == {}
+    # the step's own byte mix pushed through the link alone: 1 GB of H2D
+    # (with its D2H alongside) takes 20 ms, so a 40 ms step is at 0.5
+    mixed = dict(link, mixed={"d2h_per_h2d": 1.0, "s_per_h2d_byte": 0.02 / 10 ** 9})
+    m = bench.link_roofline(mixed, 10 ** 9, 10 ** 9, 40.0)["mixed"]
+    assert m["bound_ms"] == pytest.approx(20.0) and m["frac"] == pytest.approx(0.5)
     monkeypatch.setattr(bench, "ROOT", str(tmp_path))
     peak, src = bench.measured_peak()
     assert peak > 0 and src.startswith("fallback")

@@ -39,6 +39,7 @@ int main(int argc, char** argv) {
   const size_t bytes = gb << 30, chunk = 64ull << 20;
 
   // the test file, written with plain buffered I/O
+  fprintf(stderr, "gds_probe: writing %zu GB to %s\n", gb, path);
   {
     int fd = open(path, O_CREAT | O_TRUNC | O_WRONLY, 0644);
     if (fd < 0) { perror("open"); return 1; }
@@ -55,7 +56,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&dev, bytes);
 
   // cuFile
+  fprintf(stderr, "gds_probe: cuFileDriverOpen\n");
   CUfileError_t e = cuFileDriverOpen();
+  fprintf(stderr, "gds_probe: driver open err=%d\n", (int)e.err);
   int drv_ok = e.err == CU_FILE_SUCCESS;
   CUfileDrvProps_t props;
   memset(&props, 0, sizeof(props));
@@ -73,6 +76,7 @@ int main(int argc, char** argv) {
   if (drv_ok) {
     CUfileError_t r = cuFileHandleRegister(&fh, &d);
     reg_err = r.err;
+    fprintf(stderr, "gds_probe: handle register err=%d (O_DIRECT %d)\n", reg_err, direct);
     if (r.err == CU_FILE_SUCCESS) {
       buf_err = cuFileBufRegister(dev, bytes, 0).err;
       double best = 1e30;
@@ -95,6 +99,7 @@ int main(int argc, char** argv) {
   close(fd);
 
   // pinned host staging: pread + async H2D, two chunks in flight
+  fprintf(stderr, "gds_probe: cufile read %.3f GB/s; pinned leg\n", gds_gbs);
   double pin_gbs = -1;
   {
     int f2 = open(path, O_RDONLY);

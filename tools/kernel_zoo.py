@@ -54,6 +54,10 @@ CASES = {
     # + ZeRO re-pad (load): the GENERAL class of the move kernels
     "general_ops": ("partial", CFG(2, 4), CFG(3, 2), False, DType.F32,
                     ["convert_gather_ops", "load_scatter_ops"]),
+    # the same ops with every source and destination on one 16-B phase
+    # (n = 2^26, dp 2 -> 2): the vector branch of the OPS kernels alone
+    "ops_vec": ("partial_even", CFG(2, 4), CFG(2, 2), False, DType.F32,
+                ["convert_gather_ops", "load_scatter_ops"]),
 }
 
 
@@ -78,7 +82,8 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     a = ap.parse_args()
     kind, src, tgt, fused, dtype, kernels = CASES[a.case]
-    spec = U.llama_spec("7b", a.layers) if kind == "llama" else partial_spec()
+    spec = (U.llama_spec("7b", a.layers) if kind == "llama"
+            else partial_spec(1 << 26) if kind == "partial_even" else partial_spec())
     plan = ReshardPlan(spec, src, tgt, dtype=dtype, fused=fused)
     plan.synthesize(7)
     par = plan.verify(7)
