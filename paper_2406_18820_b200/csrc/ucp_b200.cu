@@ -38,10 +38,25 @@ namespace {
 #define UCP_REALIGN_MINB 4  // CTAs per SM of the realigning kernels (64 registers, no shared staging)
 #endif
 #ifndef UCP_OPS_MINB
-#define UCP_OPS_MINB 2  // CTAs per SM of the MEAN / NOISE / ZERO / CHECKZERO kernels (f64 accumulators)
+#define UCP_OPS_MINB 4  // CTAs per SM of the MEAN / NOISE / ZERO / CHECKZERO kernels (f64 accumulators)
+#endif
+#ifndef UCP_OPS_MINB_LOAD
+#define UCP_OPS_MINB_LOAD 4  // the same for load_scatter_ops (NOISE / ZERO: no f64 divide)
 #endif
 #ifndef UCP_OPS_GC
 #define UCP_OPS_GC 4  // MEAN: averaged groups whose loads are in flight together
+#endif
+#ifndef UCP_OPS_VU
+#define UCP_OPS_VU 4  // OPS vector path: 16-B slots per lane per pass (divides UCP_VEC)
+#endif
+#ifndef UCP_OPS_VU_MEAN
+#define UCP_OPS_VU_MEAN 1  // the same for MEAN (f64 accumulators)
+#endif
+#ifndef UCP_OPS_SU
+#define UCP_OPS_SU 8  // OPS 4-B path: elements per lane per pass
+#endif
+#ifndef UCP_OPS_SU_MEAN
+#define UCP_OPS_SU_MEAN 4
 #endif
 #ifndef UCP_PERSISTENT
 #define UCP_PERSISTENT 0  // 1: fused kernel runs 148*UCP_MINB persistent CTAs over the tiles
@@ -147,26 +162,34 @@ __device__ __forceinline__ uint32_t step_down(uint32_t u) {
   return (u >> 31) ? u + 1u : u - 1u;
 }
 
-// partial_noise for one element (ucp/parallel.py:340-370)
+// partial_noise for one element (ucp/parallel.py:340-370). Zero, inf and NaN
+// are returned unchanged (the reference's isfinite & x != 0 mask). When the
+// `steps` nextafter steps cross neither zero nor +-inf (every element but
+// those within `steps` ulps of them) they are plain +-steps on the bit
+// pattern, computed without the step loop's branches; the symmetry test
+// hi + lo == 2x stays the reference's f64 arithmetic.
 __device__ __forceinline__ float noise1(float x, int t, int tp) {
   if (tp <= 1 || ((tp & 1) && t == tp - 1)) return x;
   const uint32_t u = bits_of(x);
-  uint32_t hi = u, lo = u;
-  const int steps = t / 2 + 1;
-  for (int s = 0; s < steps; ++s) {
-    hi = step_up(hi);
-    lo = step_down(lo);
+  const uint32_t steps = (uint32_t)(t / 2 + 1);
+  const uint32_t mag = u & 0x7fffffffu;
+  if (mag == 0u || mag >= 0x7f800000u) return x;
+  uint32_t hi, lo;
+  if (mag > steps && mag + steps <= 0x7f800000u) {
+    const bool neg = (u >> 31) != 0u;
+    hi = neg ? u - steps : u + steps;
+    lo = neg ? u + steps : u - steps;
+  } else {
+    hi = u;
+    lo = u;
+    for (uint32_t s = 0; s < steps; ++s) {
+      hi = step_up(hi);
+      lo = step_down(lo);
+    }
   }
-  const bool finite = (u & 0x7f800000u) != 0x7f800000u;
-  const bool nonzero = (u & 0x7fffffffu) != 0u;
-  bool ok = false;
-  if (finite && nonzero) {
-    const double sum = __dadd_rn((double)float_of(hi), (double)float_of(lo));
-    const double twice = __dmul_rn(2.0, (double)x);
-    ok = (sum == twice);
-  }
-  if (!ok) return x;
-  return float_of((t & 1) ? lo : hi);
+  const double sum = __dadd_rn((double)float_of(hi), (double)float_of(lo));
+  const double twice = __dmul_rn(2.0, (double)x);
+  return sum == twice ? float_of((t & 1) ? lo : hi) : x;
 }
 
 // f32 -> bf16 bits (ucp/tensor.py:192-201)
@@ -292,6 +315,20 @@ __device__ __forceinline__ void report(bool bad, uint32_t elem, uint32_t run_idx
 // path: a group-at-a-time, slot-at-a-time loop left one load in flight and
 // ran at ~0.14 of the HBM peak (r02a kernel zoo). The f64 accumulation order
 // is the reference's: ascending group, __dadd_rn, one __ddiv_rn, RNE to f32.
+// The f64 divide of a MEAN, out of line: its inlined sequence (MUFU.RCP64H,
+// DFMA refinement, special-case branch) would set every OPS kernel's register
+// budget for the rare non-power-of-two group count.
+__device__ __noinline__ double ddiv_rn_call(double a, double b) { return __ddiv_rn(a, b); }
+
+// acc / G rounded to f64 like __ddiv_rn(acc, G). For G = 2^k and finite acc
+// the quotient is exact: acc is 0 or a multiple of 2^-149 (a sum of f32
+// values), so acc * 2^-k stays far above the f64 subnormal range and the
+// multiply is the exact, hence correctly rounded, quotient.
+__device__ __forceinline__ double mean_div(double acc, int G) {
+  if ((G & (G - 1)) == 0 && isfinite(acc)) return __dmul_rn(acc, 1.0 / (double)G);
+  return ddiv_rn_call(acc, (double)G);
+}
+
 template <int W, int U, int OP>
 __device__ __forceinline__ void op_run(const Ctx& c, uint64_t srow, uint64_t drow,
                                     const uint32_t (&e)[U], const bool (&ok)[U], uint32_t ebase,
@@ -355,7 +392,7 @@ __device__ __forceinline__ void op_run(const Ctx& c, uint64_t srow, uint64_t dro
     if (!ok[u]) continue;
     if constexpr (OP == UCP_OP_MEAN) {
 #pragma unroll
-      for (int i = 0; i < W; ++i) v[u].v[i] = __double2float_rn(__ddiv_rn(acc[u][i], (double)G));
+      for (int i = 0; i < W; ++i) v[u].v[i] = __double2float_rn(mean_div(acc[u][i], G));
     } else if constexpr (OP == UCP_OP_NOISE) {
 #pragma unroll
       for (int i = 0; i < W; ++i) v[u].v[i] = noise1(v[u].v[i], r.tp_rank, r.tp);
@@ -401,7 +438,7 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
     const uint32_t tail = len - head - 4 * nvec;
     // vector body: slot u of lane -> vector lane + 32u (MEAN: two passes of
     // half the slots, its f64 accumulators would not fit the registers)
-    constexpr int UH = OP == UCP_OP_MEAN ? kVec / 2 : kVec;
+    constexpr int UH = OP == UCP_OP_MEAN ? UCP_OPS_VU_MEAN : UCP_OPS_VU;
 #pragma unroll
     for (int h = 0; h < kVec / UH; ++h) {
       uint32_t e[UH];
@@ -424,7 +461,7 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
       general<OP, 1, 1>(c, srow, drow, e1, ok1, ebase, st);
     }
   } else {
-    constexpr int U = OP == UCP_OP_MEAN ? 4 : 8;
+    constexpr int U = OP == UCP_OP_MEAN ? UCP_OPS_SU_MEAN : UCP_OPS_SU;
     for (uint32_t base = 0; base < len; base += 32u * U) {
       uint32_t e[U];
       bool ok[U];
@@ -956,7 +993,7 @@ __device__ __forceinline__ void realign_body(const ucp_run* __restrict__ runs,
 // ---------------------------------------------------------------- ops kernels
 
 #ifndef UCP_OPS_INLINE
-#define UCP_OPS_INLINE 0  // 1: the four op instantiations inlined into the kernel
+#define UCP_OPS_INLINE 1  // 0: one noinline function per op (r02 A/B: inlined + 3-4 CTAs/SM is 1.7x faster)
 #endif
 #if UCP_OPS_INLINE
 #define UCP_OPS_TILE_ATTR __forceinline__
@@ -1389,7 +1426,7 @@ __global__ void __launch_bounds__(kThreads, UCP_REALIGN_MINB) load_scatter_reali
 __global__ void __launch_bounds__(kThreads, UCP_OPS_MINB) convert_gather_ops(UCP_MOVE_ARGS) {
   ops_body(runs, aux, rt, r0, nr, sb, db, st);
 }
-__global__ void __launch_bounds__(kThreads, UCP_OPS_MINB) load_scatter_ops(UCP_MOVE_ARGS) {
+__global__ void __launch_bounds__(kThreads, UCP_OPS_MINB_LOAD) load_scatter_ops(UCP_MOVE_ARGS) {
   ops_body(runs, aux, rt, r0, nr, sb, db, st);
 }
 
