@@ -953,23 +953,6 @@ __device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uin
     realign_store<DT>(db + (d == 0 ? d0 : s_aux[ns - 1 + d - 1]) + doff, v, nx, ps, len, lane, sp);
 }
 
-#ifndef UCP_REALIGN_PREFETCH
-#define UCP_REALIGN_PREFETCH 0  // realigning kernels: L2 bulk prefetch distance in warp items (0: off)
-#endif
-
-// Bulk-prefetch into L2 the aligned source vectors of one realigning segment
-// (row-major f32 sources at sb + src_k + soff, k < ns; lane k issues source k).
-__device__ __forceinline__ void realign_prefetch(const char* sb, uint64_t s0, const uint64_t* s_aux,
-                                                 int ns, uint64_t soff, uint32_t len, uint32_t lane) {
-  if (lane < (uint32_t)ns) {
-    uint64_t a = reinterpret_cast<uint64_t>(sb + (lane == 0 ? s0 : s_aux[lane - 1]) + soff);
-    uint64_t e = (a + 4ull * len + 15) & ~15ull;
-    a &= ~15ull;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a))
-                 : "memory");
-  }
-}
-
 template <int DT>
 __device__ __forceinline__ void move_tile_realign(const TileGeom& g, const ucp_run& r,
                                                   const uint64_t* s_aux, const char* __restrict__ sb,
@@ -978,18 +961,6 @@ __device__ __forceinline__ void move_tile_realign(const TileGeom& g, const ucp_r
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t it = warp; it < g.n_items; it += kWarps) {
-#if UCP_REALIGN_PREFETCH
-    {
-      const uint32_t nit = it + UCP_REALIGN_PREFETCH * kWarps;
-      if (nit < g.n_items) {
-        const uint32_t nrr = nit / g.spr;
-        const uint32_t ncs = g.col0 + (nit - nrr * g.spr) * kSeg;
-        realign_prefetch(sb, r.src, s_aux, r.n_src,
-                         4ull * ((uint64_t)(g.row0 + nrr) * r.src_pitch + ncs),
-                         min(ncs + kSeg, g.col0 + g.nc) - ncs, lane);
-      }
-    }
-#endif
     const uint32_t rr = it / g.spr;
     const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
     const uint32_t len = min(cs + kSeg, g.col0 + g.nc) - cs;
@@ -1389,18 +1360,6 @@ __device__ __forceinline__ void fused_tile_realign(const ucp_tile& tile, const u
   const bool atom_on = s_run.atom != ~0ull;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t it = warp; it < n_items; it += kWarps) {
-#if UCP_REALIGN_PREFETCH
-    {
-      const uint32_t nit = it + UCP_REALIGN_PREFETCH * kWarps;
-      if (nit < n_items) {
-        const uint32_t nrr = nit / spr;
-        const uint32_t ncs = tile.col0 + (nit - nrr * spr) * kSeg;
-        realign_prefetch(sb, s_run.src, s_aux, s_run.n_src,
-                         4ull * ((uint64_t)(tile.row0 + nrr) * s_run.src_pitch + ncs),
-                         min(ncs + kSeg, tile.col0 + nc) - ncs, lane);
-      }
-    }
-#endif
     const uint32_t rr = it / spr;
     const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
     const uint32_t len = min(cs + kSeg, tile.col0 + nc) - cs;
