@@ -844,6 +844,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+    t_plan = time.perf_counter()
     plan = ReshardPlan(spec, src, tgt, params=mine, device=dev, dtype=wdt, src_peer=sources,
                        window_bytes=int(args.window_gb * GB), tile_bytes=args.tile_kb * 1024,
                        fused=not args.unfused, strict=not args.non_strict,
@@ -851,6 +852,7 @@ def run_ours(args):
                        home_of=[g % world for g in range(tgt.world_size)] if homed else None,
                        n_homes=world if homed else 1,
                        peer=(exch, peer) if peer is not None else None)
+    t_plan = time.perf_counter() - t_plan  # host descriptor compile + table upload, outside the timed region
     S_local = plan.state_bytes
     free, _ = torch.cuda.mem_get_info(dev)
     need = (0 if sources else plan.src_total) + plan.max_atom * 3 + plan.max_tgt * 2 + (2 << 30)
@@ -1146,6 +1148,7 @@ def run_ours(args):
                          plan.bytes["R_c"] + plan.bytes["W_c"] + plan.fused_bytes["R"] + 2 * plan.fused_bytes["W_atom"]
                          + plan.bytes["R_l"] + plan.bytes["W_l"] + plan.fused_bytes["W_tgt"]),
                      "windows": nW,
+                     "plan_compile_s": round(t_plan, 3),
                      "parallelism": f"param-sharded x{world}" + (
                          (", rank-homed targets: kernel stores into peer GPUs' IPC-mapped buffers "
                           if peer is not None else
