@@ -890,35 +890,26 @@ __device__ __forceinline__ void realign_cmp_scalar(const float4& v, const char* 
 // One row segment [0, len <= kSeg): sources at sb + src_k + soff (src_0 = s0,
 // src_k = s_aux[k - 1]), optional f32 atom at ab + aoff, destinations at
 // db + dst_d + doff (dst_0 = d0, dst_d = s_aux[ns - 1 + d - 1]).
-// The primary's aligned source vectors of a segment starting at sp: lane l,
-// slot u loads vector I = l + 32u of the 16-B grid (zero past the segment).
-__device__ __forceinline__ void realign_load(const char* sp, uint32_t len, uint32_t lane,
-                                             float4 (&v)[kRU]) {
-  const uint32_t ps = (uint32_t)((reinterpret_cast<uintptr_t>(sp) >> 2) & 3);
-  const uint32_t nsv = (ps + len + 3) >> 2;
-  const char* sv = sp - 4 * ps;
-#pragma unroll
-  for (int u = 0; u < kRU; ++u) {
-    const uint32_t I = lane + 32u * u;
-    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (I < nsv) v[u] = ld_stream4(sv + 16ull * I);
-  }
-}
-
-// realign_segment with the primary's vectors already loaded (realign_load).
 template <int DT>
-__device__ __forceinline__ void realign_segment_v(const char* __restrict__ sb, uint64_t s0,
-                                                  const uint64_t* s_aux, int ns, uint64_t soff,
-                                                  char* __restrict__ ab, uint64_t aoff, bool atom_on,
-                                                  char* __restrict__ db, uint64_t d0, int nd,
-                                                  uint64_t doff, uint32_t len, uint32_t lane,
-                                                  const float4 (&v)[kRU], bool& bad, uint32_t& bad_e) {
+__device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uint64_t s0,
+                                                const uint64_t* s_aux, int ns, uint64_t soff,
+                                                char* __restrict__ ab, uint64_t aoff, bool atom_on,
+                                                char* __restrict__ db, uint64_t d0, int nd,
+                                                uint64_t doff, uint32_t len, uint32_t lane,
+                                                bool& bad, uint32_t& bad_e) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   constexpr uint32_t kLast = 32u * kRU;  // index of the 129th source vector
   const char* sp = sb + s0 + soff;
   const uint32_t ps = (uint32_t)((reinterpret_cast<uintptr_t>(sp) >> 2) & 3);
   const uint32_t nsv = (ps + len + 3) >> 2;  // <= kLast + 1
   const char* sv = sp - 4 * ps;
+  float4 v[kRU];
+#pragma unroll
+  for (int u = 0; u < kRU; ++u) {
+    const uint32_t I = lane + 32u * u;
+    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (I < nsv) v[u] = ld_stream4(sv + 16ull * I);
+  }
   // right neighbours (warp-uniform shift set): the shuffle round moves only
   // the components the largest shift reads; lane 31 loads the 129th vector
   uint32_t dmax = atom_on ? (ps - (uint32_t)((reinterpret_cast<uintptr_t>(ab + aoff) >> 2) & 3)) & 3u : 0u;
@@ -963,62 +954,12 @@ __device__ __forceinline__ void realign_segment_v(const char* __restrict__ sb, u
 }
 
 template <int DT>
-__device__ __forceinline__ void realign_segment(const char* __restrict__ sb, uint64_t s0,
-                                                const uint64_t* s_aux, int ns, uint64_t soff,
-                                                char* __restrict__ ab, uint64_t aoff, bool atom_on,
-                                                char* __restrict__ db, uint64_t d0, int nd,
-                                                uint64_t doff, uint32_t len, uint32_t lane,
-                                                bool& bad, uint32_t& bad_e) {
-  float4 v[kRU];
-  realign_load(sb + s0 + soff, len, lane, v);
-  realign_segment_v<DT>(sb, s0, s_aux, ns, soff, ab, aoff, atom_on, db, d0, nd, doff, len, lane,
-                        v, bad, bad_e);
-}
-
-#ifndef UCP_REALIGN_PIPE
-#define UCP_REALIGN_PIPE 0  // 1: a warp loads its next segment before storing the current one
-#endif
-
-template <int DT>
 __device__ __forceinline__ void move_tile_realign(const TileGeom& g, const ucp_run& r,
                                                   const uint64_t* s_aux, const char* __restrict__ sb,
                                                   char* __restrict__ db, uint32_t run_idx,
                                                   ucp_status* st) {
   constexpr int ESZ = DT == UCP_DT_F32 ? 4 : 2;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#if UCP_REALIGN_PIPE
-  float4 v[kRU];
-  auto soff_of = [&](uint32_t it, uint32_t& row, uint32_t& cs, uint32_t& len) {
-    const uint32_t rr = it / g.spr;
-    cs = g.col0 + (it - rr * g.spr) * kSeg;
-    len = min(cs + kSeg, g.col0 + g.nc) - cs;
-    row = g.row0 + rr;
-    return 4ull * ((uint64_t)row * r.src_pitch + cs);
-  };
-  if (warp < g.n_items) {
-    uint32_t row, cs, len;
-    const uint64_t so = soff_of(warp, row, cs, len);
-    realign_load(sb + r.src + so, len, lane, v);
-  }
-  for (uint32_t it = warp; it < g.n_items; it += kWarps) {
-    uint32_t row, cs, len;
-    const uint64_t soff = soff_of(it, row, cs, len);
-    float4 vn[kRU];
-    if (it + kWarps < g.n_items) {
-      uint32_t nrow, ncs, nlen;
-      const uint64_t nso = soff_of(it + kWarps, nrow, ncs, nlen);
-      realign_load(sb + r.src + nso, nlen, lane, vn);
-    }
-    bool bad = false;
-    uint32_t bad_e = 0xffffffffu;
-    realign_segment_v<DT>(sb, r.src, s_aux, r.n_src, soff, nullptr, 0, false, db, r.dst, r.n_dst,
-                          (uint64_t)ESZ * ((uint64_t)row * r.dst_pitch + cs), len, lane, v, bad,
-                          bad_e);
-    report(bad, row * r.cols + cs + bad_e, run_idx, st);
-#pragma unroll
-    for (int u = 0; u < kRU; ++u) v[u] = vn[u];
-  }
-#else
   for (uint32_t it = warp; it < g.n_items; it += kWarps) {
     const uint32_t rr = it / g.spr;
     const uint32_t cs = g.col0 + (it - rr * g.spr) * kSeg;
@@ -1031,7 +972,6 @@ __device__ __forceinline__ void move_tile_realign(const TileGeom& g, const ucp_r
                         (uint64_t)ESZ * ((uint64_t)row * r.dst_pitch + cs), len, lane, bad, bad_e);
     report(bad, row * r.cols + cs + bad_e, run_idx, st);
   }
-#endif
 }
 
 // UCP_CLASS_GENERAL of the move tables: phase-mismatched COPY runs.
@@ -1419,41 +1359,6 @@ __device__ __forceinline__ void fused_tile_realign(const ucp_tile& tile, const u
   const uint32_t spr = (nc + kSeg - 1) / kSeg, n_items = nrows * spr;
   const bool atom_on = s_run.atom != ~0ull;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#if UCP_REALIGN_PIPE
-  float4 v[kRU];
-  auto soff_of = [&](uint32_t it, uint32_t& row, uint32_t& cs, uint32_t& len) {
-    const uint32_t rr = it / spr;
-    cs = tile.col0 + (it - rr * spr) * kSeg;
-    len = min(cs + kSeg, tile.col0 + nc) - cs;
-    row = tile.row0 + rr;
-    return 4ull * ((uint64_t)row * s_run.src_pitch + cs);
-  };
-  if (warp < n_items) {
-    uint32_t row, cs, len;
-    const uint64_t so = soff_of(warp, row, cs, len);
-    realign_load(sb + s_run.src + so, len, lane, v);
-  }
-  for (uint32_t it = warp; it < n_items; it += kWarps) {
-    uint32_t row, cs, len;
-    const uint64_t soff = soff_of(it, row, cs, len);
-    float4 vn[kRU];
-    if (it + kWarps < n_items) {
-      uint32_t nrow, ncs, nlen;
-      const uint64_t nso = soff_of(it + kWarps, nrow, ncs, nlen);
-      realign_load(sb + s_run.src + nso, nlen, lane, vn);
-    }
-    bool bad = false;
-    uint32_t bad_e = 0xffffffffu;
-    realign_segment_v<DT>(sb, s_run.src, s_aux, s_run.n_src, soff, ab,
-                          atom_on ? s_run.atom + 4ull * ((uint64_t)row * s_run.atom_pitch + cs) : 0,
-                          atom_on, db, s_run.dst, s_run.n_dst,
-                          (uint64_t)ESZ * ((uint64_t)row * s_run.dst_pitch + cs), len, lane, v,
-                          bad, bad_e);
-    report(bad, row * s_run.cols + cs + bad_e, tile.run, st);
-#pragma unroll
-    for (int u = 0; u < kRU; ++u) v[u] = vn[u];
-  }
-#else
   for (uint32_t it = warp; it < n_items; it += kWarps) {
     const uint32_t rr = it / spr;
     const uint32_t cs = tile.col0 + (it - rr * spr) * kSeg;
@@ -1469,7 +1374,6 @@ __device__ __forceinline__ void fused_tile_realign(const ucp_tile& tile, const u
                         bad_e);
     report(bad, row * s_run.cols + cs + bad_e, tile.run, st);
   }
-#endif
 }
 
 // The GENERAL class of fused tables: phase-mismatched cells; each CTA
