@@ -38,7 +38,7 @@ namespace {
 #define UCP_REALIGN_MINB 4  // CTAs per SM of the realigning kernels (64 registers, no shared staging)
 #endif
 #ifndef UCP_OPS_MINB
-#define UCP_OPS_MINB 4  // CTAs per SM of the MEAN / NOISE / ZERO / CHECKZERO kernels (f64 accumulators)
+#define UCP_OPS_MINB 5  // CTAs per SM of the MEAN / NOISE / ZERO / CHECKZERO kernels (f64 accumulators)
 #endif
 #ifndef UCP_OPS_MINB_LOAD
 #define UCP_OPS_MINB_LOAD 4  // the same for load_scatter_ops (NOISE / ZERO: no f64 divide)
@@ -167,7 +167,8 @@ __device__ __forceinline__ uint32_t step_down(uint32_t u) {
 // `steps` nextafter steps cross neither zero nor +-inf (every element but
 // those within `steps` ulps of them) they are plain +-steps on the bit
 // pattern, computed without the step loop's branches; the symmetry test
-// hi + lo == 2x stays the reference's f64 arithmetic.
+// hi + lo == 2x stays the reference's f64 arithmetic (an integer form of it,
+// E(m-s) == E(m+s-1) on binade indices, is exact but measured 14 % slower).
 __device__ __forceinline__ float noise1(float x, int t, int tp) {
   if (tp <= 1 || ((tp & 1) && t == tp - 1)) return x;
   const uint32_t u = bits_of(x);
@@ -275,6 +276,15 @@ __device__ __forceinline__ int first_diff(const Lanes<W>& a, const Lanes<W>& b) 
   for (int i = 0; i < W; ++i)
     if (bits_of(a.v[i]) != bits_of(b.v[i])) return i;
   return W;
+}
+
+// first component where a and b differ bitwise, or 4
+__device__ __forceinline__ int diff4(const float4& a, const float4& b) {
+  if (bits_of(a.x) != bits_of(b.x)) return 0;
+  if (bits_of(a.y) != bits_of(b.y)) return 1;
+  if (bits_of(a.z) != bits_of(b.z)) return 2;
+  if (bits_of(a.w) != bits_of(b.w)) return 3;
+  return 4;
 }
 
 struct Ctx {
@@ -418,6 +428,65 @@ __device__ __forceinline__ void general(const Ctx& c, uint64_t srow, uint64_t dr
   op_run<W, U, OP>(c, srow, drow, e, ok, ebase, st);
 }
 
+#ifndef UCP_MEAN_CHUNK
+#define UCP_MEAN_CHUNK 4  // MEAN vector path: source vectors a lane has in flight at once
+#endif
+#ifndef UCP_MEAN_UNROLL
+#define UCP_MEAN_UNROLL 1  // MEAN vector path: slots the compiler may interleave
+#endif
+constexpr int kMeanUnroll = UCP_MEAN_UNROLL;
+#ifndef UCP_MEAN_LEAN
+#define UCP_MEAN_LEAN 1  // 0: MEAN vector runs through the generic op_run
+#endif
+
+// MEAN of one 16-B slot per lane (vector runs, ucp/convert.py:279-284): the
+// slot's source vectors -- groups in ascending order, each group's replicas
+// right after its primary -- are loaded UCP_MEAN_CHUNK at a time; replicas
+// are compared with their group's primary; primaries are summed in f64 in
+// group order, divided once (mean_div) and rounded to f32.
+__device__ __forceinline__ void mean_vec_slot(const Ctx& c, uint64_t srow, uint64_t drow,
+                                              uint32_t e, bool ok, int G, int K, bool& bad,
+                                              uint32_t& bad_e) {
+  const ucp_run& r = *c.r;
+  const int ns = r.n_src;
+  const uint64_t eo = 4ull * (srow + e);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  float4 prim = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k = 0;  // replica index of source i0 + j within its group
+  for (int i0 = 0; i0 < ns; i0 += UCP_MEAN_CHUNK) {
+    float4 q[UCP_MEAN_CHUNK];
+#pragma unroll
+    for (int j = 0; j < UCP_MEAN_CHUNK; ++j) {
+      q[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok && i0 + j < ns) q[j] = ld_stream4(c.sb + src_off(c, i0 + j) + eo);
+    }
+#pragma unroll
+    for (int j = 0; j < UCP_MEAN_CHUNK; ++j) {
+      if (i0 + j >= ns) break;
+      if (k == 0) {
+        prim = q[j];
+        if (i0 + j == 0) {
+          a0 = (double)prim.x; a1 = (double)prim.y; a2 = (double)prim.z; a3 = (double)prim.w;
+        } else {
+          a0 = __dadd_rn(a0, (double)prim.x); a1 = __dadd_rn(a1, (double)prim.y);
+          a2 = __dadd_rn(a2, (double)prim.z); a3 = __dadd_rn(a3, (double)prim.w);
+        }
+      } else {
+        const int d = diff4(prim, q[j]);
+        if (d < 4) { bad = true; bad_e = min(bad_e, e + d); }
+      }
+      if (++k == K) k = 0;
+    }
+  }
+  if (!ok) return;
+  Lanes<4> v;
+  v.v[0] = __double2float_rn(mean_div(a0, G)); v.v[1] = __double2float_rn(mean_div(a1, G));
+  v.v[2] = __double2float_rn(mean_div(a2, G)); v.v[3] = __double2float_rn(mean_div(a3, G));
+  const int esz = r.dtype == UCP_DT_F32 ? 4 : 2;
+  for (int d = 0; d < r.n_dst; ++d)
+    store_w<4>(c.db + dst_off(c, d) + (uint64_t)esz * (drow + e), v, r.dtype);
+}
+
 // One warp processes columns [cs, cs+len) of one row (OPS kernels).
 template <int OP>
 __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs, uint32_t len,
@@ -439,6 +508,19 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
     // vector body: slot u of lane -> vector lane + 32u (MEAN: two passes of
     // half the slots, its f64 accumulators would not fit the registers)
     constexpr int UH = OP == UCP_OP_MEAN ? UCP_OPS_VU_MEAN : UCP_OPS_VU;
+    if constexpr (OP == UCP_OP_MEAN && UCP_MEAN_LEAN) {
+      const int G = r.groups > 0 ? r.groups : 1;
+      const int K = r.n_src / G;
+      bool bad = false;
+      uint32_t bad_e = 0xffffffffu;
+#pragma unroll (kMeanUnroll)
+      for (int u = 0; u < kVec; ++u) {
+        const uint32_t vi = lane + 32u * u;
+        if (32u * u >= nvec) break;  // warp-uniform
+        mean_vec_slot(c, srow, drow, head + 4u * vi, vi < nvec, G, K, bad, bad_e);
+      }
+      report(bad, ebase + bad_e, c.run_idx, st);
+    } else
 #pragma unroll
     for (int h = 0; h < kVec / UH; ++h) {
       uint32_t e[UH];
@@ -665,13 +747,6 @@ __device__ __forceinline__ void store1(char* p, float v) {
   else *reinterpret_cast<uint16_t*>(p) = (uint16_t)cvt16(v, DT);
 }
 
-__device__ __forceinline__ int diff4(const float4& a, const float4& b) {
-  if (bits_of(a.x) != bits_of(b.x)) return 0;
-  if (bits_of(a.y) != bits_of(b.y)) return 1;
-  if (bits_of(a.z) != bits_of(b.z)) return 2;
-  if (bits_of(a.w) != bits_of(b.w)) return 3;
-  return 4;
-}
 
 template <int DT>
 __device__ __forceinline__ void vec_body(const ucp_run* __restrict__ runs,
