@@ -487,6 +487,54 @@ __device__ __forceinline__ void mean_vec_slot(const Ctx& c, uint64_t srow, uint6
     store_w<4>(c.db + dst_off(c, d) + (uint64_t)esz * (drow + e), v, r.dtype);
 }
 
+#ifndef UCP_NOISE_LEAN
+#define UCP_NOISE_LEAN 1  // 0: NOISE vector runs through the generic op_run
+#endif
+
+// NOISE of a vector run's segment (ucp/parallel.py:340-370 per element): each
+// lane's kVec slots of the primary are loaded together, replicas (if any)
+// compared with them, then every element noised and every destination stored.
+__device__ __forceinline__ void noise_vec_segment(const Ctx& c, uint64_t srow, uint64_t drow,
+                                                  uint32_t head, uint32_t nvec, uint32_t lane,
+                                                  bool& bad, uint32_t& bad_e) {
+  const ucp_run& r = *c.r;
+  float4 v[kVec];
+  const char* s0 = c.sb + r.src + 4ull * (srow + head);
+#pragma unroll
+  for (int u = 0; u < kVec; ++u) {
+    const uint32_t vi = lane + 32u * u;
+    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (vi < nvec) v[u] = ld_stream4(s0 + 16ull * vi);
+  }
+  for (int k = 1; k < r.n_src; ++k) {
+    const char* sk = c.sb + src_off(c, k) + 4ull * (srow + head);
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) {
+      const uint32_t vi = lane + 32u * u;
+      if (vi >= nvec) continue;
+      const int d = diff4(v[u], ld_stream4(sk + 16ull * vi));
+      if (d < 4) { bad = true; bad_e = min(bad_e, head + 4u * vi + d); }
+    }
+  }
+  const int t = r.tp_rank, tp = r.tp;
+#pragma unroll
+  for (int u = 0; u < kVec; ++u)
+    v[u] = make_float4(noise1(v[u].x, t, tp), noise1(v[u].y, t, tp), noise1(v[u].z, t, tp),
+                       noise1(v[u].w, t, tp));
+  const int esz = r.dtype == UCP_DT_F32 ? 4 : 2;
+  for (int d = 0; d < r.n_dst; ++d) {
+    char* dp = c.db + dst_off(c, d) + (uint64_t)esz * (drow + head);
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) {
+      const uint32_t vi = lane + 32u * u;
+      if (vi >= nvec) continue;
+      Lanes<4> x;
+      x.v[0] = v[u].x; x.v[1] = v[u].y; x.v[2] = v[u].z; x.v[3] = v[u].w;
+      store_w<4>(dp + (uint64_t)esz * 4 * vi, x, r.dtype);
+    }
+  }
+}
+
 // One warp processes columns [cs, cs+len) of one row (OPS kernels).
 template <int OP>
 __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs, uint32_t len,
@@ -519,6 +567,11 @@ __device__ __forceinline__ void segment(const Ctx& c, uint32_t row, uint32_t cs,
         if (32u * u >= nvec) break;  // warp-uniform
         mean_vec_slot(c, srow, drow, head + 4u * vi, vi < nvec, G, K, bad, bad_e);
       }
+      report(bad, ebase + bad_e, c.run_idx, st);
+    } else if constexpr (OP == UCP_OP_NOISE && UCP_NOISE_LEAN) {
+      bool bad = false;
+      uint32_t bad_e = 0xffffffffu;
+      noise_vec_segment(c, srow, drow, head, nvec, (uint32_t)lane, bad, bad_e);
       report(bad, ebase + bad_e, c.run_idx, st);
     } else
 #pragma unroll
