@@ -41,7 +41,7 @@ namespace {
 #define UCP_OPS_MINB 5  // CTAs per SM of the MEAN / NOISE / ZERO / CHECKZERO kernels (f64 accumulators)
 #endif
 #ifndef UCP_OPS_MINB_LOAD
-#define UCP_OPS_MINB_LOAD 4  // the same for load_scatter_ops (NOISE / ZERO: no f64 divide)
+#define UCP_OPS_MINB_LOAD 5  // the same for load_scatter_ops (NOISE / ZERO: no f64 divide)
 #endif
 #ifndef UCP_OPS_GC
 #define UCP_OPS_GC 4  // MEAN: averaged groups whose loads are in flight together
