@@ -597,10 +597,16 @@ def public_e2e(spec, src, tgt, names, eplan, host_src, wdt, steps: int) -> dict:
             "state_bytes": S, "in_bytes": in_bytes, "out_bytes": out_bytes,
             "host_copy_GBps": hc,
             "pack_s_at_host_copy_rate": in_bytes / (hc * GB) if hc else None,
-            "pack_note": "reshard() first copies the caller's arrays into pinned memory (16 "
-                         "threads, window by window, overlapped with the transfers); that host "
-                         "copy alone, at the measured host_copy_GBps, takes pack_s_at_host_copy"
-                         "_rate of s_per_call, while the DMA engines read the same memory",
+            "host_bytes_per_call": 3 * in_bytes + out_bytes,
+            "host_bound_s": (3 * in_bytes + out_bytes) / (2 * hc * GB) if hc else None,
+            "host_frac": (3 * in_bytes + out_bytes) / (2 * hc * GB) / t if hc else None,
+            "pack_note": "reshard() copies the caller's arrays into pinned memory (16 threads, "
+                         "window by window, overlapped with the transfers): host memory then "
+                         "carries the pack's read + write of in_bytes, the H2D DMA's read of "
+                         "in_bytes and the D2H DMA's write of out_bytes = host_bytes_per_call; "
+                         "host_bound_s = that / (2 x host_copy_GBps, the read + write traffic "
+                         "of a 16-thread numpy -> pinned copy), host_frac = host_bound_s / "
+                         "s_per_call",
             "api": "paper_2406_18820_b200.reshard(spec, src, tgt, {g: [np.ndarray]}) -> "
                    "{g: [np.ndarray]} (the in-memory resume(): pack into pinned memory, H2D, "
                    "fused reshard, D2H, numpy views), wall clock, median; rank 0"}

@@ -215,3 +215,45 @@ def test_fuzz_failure_reports_match():
         first, _ = st.read()
         run_sorted, elem = first >> 32, first & 0xFFFFFFFF
         assert (int(prog.run_order[run_sorted]), elem) == (i, e), trial
+
+
+@pytest.mark.parametrize("op", [OP_MEAN, OP_NOISE])
+def test_fuzz_failure_reports_match_ops(op):
+    """The same for the OPS kernels: a flipped element in a replica (k >= 1)
+    of a MEAN group or a NOISE source is reported at its (run, element),
+    through the vector and the 4-B paths alike."""
+    rng = np.random.default_rng(11 + op)
+    hit = 0
+    for trial in range(40):
+        tab, src, dst_n = _build_move(rng, 8)
+        runs, aux, tiles = tab.finish(8192)
+        cand = []
+        for i, r in enumerate(runs):
+            G = max(1, int(r["groups"])) if int(r["op"]) == OP_MEAN else 1
+            if int(r["op"]) == op and int(r["n_src"]) > G:
+                cand.append((i, int(r["n_src"]) // G))
+        if not cand:
+            continue
+        i, K = cand[int(rng.integers(0, len(cand)))]
+        r = runs[i]
+        j = int(rng.integers(0, int(r["n_src"])))
+        if j % K == 0:
+            j += 1  # a replica, not a group's primary
+        off = int(aux[int(r["aux"]) + j - 1])
+        e = int(rng.integers(0, int(r["rows"]) * int(r["cols"])))
+        row, col = divmod(e, int(r["cols"]))
+        pos = off + 4 * (row * int(r["src_pitch"]) + col)
+        src[pos:pos + 4] ^= np.uint8(0x01)
+        want_fails = execute(runs, aux, tiles, src.copy(), np.zeros(dst_n, dtype=np.uint8))
+        assert (i, e) in want_fails
+        prog = Program(tab, torch.device("cuda"), 8192)
+        st = Status(torch.device("cuda"))
+        st.reset()
+        got = torch.zeros(dst_n, dtype=torch.uint8, device="cuda")
+        prog.launch(False, torch.from_numpy(src).cuda().data_ptr(), got.data_ptr(), st)
+        torch.cuda.synchronize()
+        first, _ = st.read()
+        run_sorted, elem = first >> 32, first & 0xFFFFFFFF
+        assert (int(prog.run_order[run_sorted]), elem) == (i, e), trial
+        hit += 1
+    assert hit >= 3, hit
