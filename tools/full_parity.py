@@ -40,7 +40,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2406_18820_b200 as U  # noqa: E402
 from oracle import ucp_oracle as O  # noqa: E402
-from paper_2406_18820_b200.layout import all_rank_records, vocab_padded_rows  # noqa: E402
+from paper_2406_18820_b200.layout import vocab_padded_rows  # noqa: E402
 from paper_2406_18820_b200.reshard import ReshardPlan  # noqa: E402
 
 GEN_CHUNK = 1 << 24  # elements per hash_unit call (bounded temporaries per thread)
@@ -55,6 +55,9 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--no-gen-check", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--windows", default=None,
+                    help="A:B -- only windows A..B-1 (a long config split over calls); the "
+                         "JSON then counts those windows' units only")
     a = ap.parse_args()
     ucp = bench.reference_ucp()
     if ucp is None:
@@ -78,7 +81,14 @@ def main():
            "target_mismatch": [], "generator_mismatch": [], "state_bytes": plan.state_bytes}
     t_gpu = t_cpu = 0.0
     t0 = time.perf_counter()
+    w_lo, w_hi = 0, len(plan.windows)
+    if a.windows:
+        lo_s, hi_s = a.windows.split(":")
+        w_lo, w_hi = int(lo_s or 0), int(hi_s or len(plan.windows))
+    res["window_range"] = [w_lo, w_hi]
     for wi, W in enumerate(plan.windows):
+        if not w_lo <= wi < w_hi:
+            continue
         tg = time.perf_counter()
         plan.status.reset()
         plan.gen_atomic(W, atom, 7)
@@ -163,8 +173,8 @@ def main():
               f"{len(res['target_mismatch'])}/{len(res['generator_mismatch'])}",
               file=sys.stderr, flush=True)
     res.update({"gpu_s": t_gpu, "cpu_s": t_cpu, "wall_s": time.perf_counter() - t0,
-                "expected_units": 3 * len(spec.params),
-                "expected_fragments": sum(len(v) for v in all_rank_records(spec, tgt)),
+                "expected_units": sum(3 * len(W.params) for W in plan.windows[w_lo:w_hi]),
+                "expected_fragments": sum(len(W.tgt_frags) for W in plan.windows[w_lo:w_hi]),
                 "identical": not (res["atomic_mismatch"] or res["target_mismatch"]
                                   or res["generator_mismatch"]),
                 "what": "GPU fused reshard vs the unmodified reference (ucp.convert.union + "
