@@ -24,6 +24,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "ucp_b200.cu")
 HDR = os.path.join(ROOT, "include", "ucp_b200.h")
+NOISE_HDR = os.path.join(HERE, "csrc", "ucp_noise.h")
 OUT = os.path.join(HERE, "libucp_b200.so")
 COMM_SRC = os.path.join(HERE, "csrc", "ucp_comm.cpp")
 COMM_HDR = os.path.join(ROOT, "include", "ucp_b200_comm.h")
@@ -64,7 +65,7 @@ def embedded_id(lib_path: str) -> str | None:
 
 
 def kernel_id() -> str | None:
-    return source_id([SRC, HDR])
+    return source_id([SRC, HDR, NOISE_HDR])
 
 
 def comm_id() -> str | None:

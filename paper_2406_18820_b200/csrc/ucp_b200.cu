@@ -7,7 +7,8 @@
 //   * pad check: bitwise zero, so -0.0 fails (ucp/convert.py:127-128)
 //   * MEAN: f64 sum in ascending group order, f64 divide, RNE to f32
 //           (ucp/convert.py:279-284) -- __dadd_rn/__ddiv_rn/__double2float_rn
-//   * NOISE: repeated nextafterf by bit stepping + exact f64 pair check
+//   * NOISE: nextafterf steps and the exact f64 pair check, restated on bit
+//           patterns (ucp_noise.h; exhaustively checked on the host)
 //           (ucp/parallel.py:340-370); no FTZ anywhere (built without fast math)
 //   * bf16 cast: (bits + 0x7FFF + lsb) >> 16, NaN quieted (ucp/tensor.py:192-201)
 //   * f16 cast: numpy's portable float->half bit algorithm (ucp/tensor.py:216)
@@ -18,6 +19,7 @@
 #include <string.h>
 
 #include "ucp_b200.h"
+#include "ucp_noise.h"
 
 static_assert(sizeof(ucp_run) == 64, "ucp_run must be 64 bytes");
 static_assert(sizeof(ucp_tile) == 16, "ucp_tile must be 16 bytes");
@@ -163,12 +165,23 @@ __device__ __forceinline__ uint32_t step_down(uint32_t u) {
 }
 
 // partial_noise for one element (ucp/parallel.py:340-370). Zero, inf and NaN
-// are returned unchanged (the reference's isfinite & x != 0 mask). When the
-// `steps` nextafter steps cross neither zero nor +-inf (every element but
-// those within `steps` ulps of them) they are plain +-steps on the bit
-// pattern, computed without the step loop's branches; the symmetry test
-// hi + lo == 2x stays the reference's f64 arithmetic (an integer form of it,
-// E(m-s) == E(m+s-1) on binade indices, is exact but measured 14 % slower).
+// are returned unchanged (the reference's isfinite & x != 0 mask). Default:
+// the branch-free integer form of ucp_noise.h (steps, the zero crossing and
+// the pair test hi + lo == 2x all on bit patterns, no f64). UCP_NOISE_INT=0
+// keeps the previous form for A/B: plain +-steps when the `steps` nextafter
+// steps cross neither zero nor +-inf, the step loop otherwise, and the f64
+// pair test (an earlier branchy integer test was measured 14 % slower).
+#ifndef UCP_NOISE_INT
+#define UCP_NOISE_INT 1  // 0: the round-2 form below (nextafter loop off the fast path, f64 pair test)
+#endif
+#if UCP_NOISE_INT
+// Branch-free integer form (csrc/ucp_noise.h, proven against the reference's
+// nextafter + f64 test over every f32 pattern by tools/noise_exhaustive.cpp).
+__device__ __forceinline__ float noise1(float x, int t, int tp) {
+  const uint32_t s = ucp_noise_steps(t, tp);
+  return s == 0u ? x : float_of(ucp_noise_bits(bits_of(x), s, (uint32_t)t & 1u));
+}
+#else
 __device__ __forceinline__ float noise1(float x, int t, int tp) {
   if (tp <= 1 || ((tp & 1) && t == tp - 1)) return x;
   const uint32_t u = bits_of(x);
@@ -192,6 +205,7 @@ __device__ __forceinline__ float noise1(float x, int t, int tp) {
   const double twice = __dmul_rn(2.0, (double)x);
   return sum == twice ? float_of((t & 1) ? lo : hi) : x;
 }
+#endif
 
 // f32 -> bf16 bits (ucp/tensor.py:192-201)
 __device__ __forceinline__ uint32_t bf16_bits(float x) {
@@ -276,6 +290,14 @@ __device__ __forceinline__ int first_diff(const Lanes<W>& a, const Lanes<W>& b) 
   for (int i = 0; i < W; ++i)
     if (bits_of(a.v[i]) != bits_of(b.v[i])) return i;
   return W;
+}
+
+// OR of the bitwise differences of a and b: 0 iff every component matches
+// (one LOP3 per component; the branchy diff4 names the component only after a
+// mismatch, on the failure path)
+__device__ __forceinline__ uint32_t xor4(const float4& a, const float4& b) {
+  return (bits_of(a.x) ^ bits_of(b.x)) | (bits_of(a.y) ^ bits_of(b.y)) |
+         (bits_of(a.z) ^ bits_of(b.z)) | (bits_of(a.w) ^ bits_of(b.w));
 }
 
 // first component where a and b differ bitwise, or 4
@@ -435,6 +457,9 @@ __device__ __forceinline__ void general(const Ctx& c, uint64_t srow, uint64_t dr
 #define UCP_MEAN_UNROLL 1  // MEAN vector path: slots the compiler may interleave
 #endif
 constexpr int kMeanUnroll = UCP_MEAN_UNROLL;
+#ifndef UCP_MEAN_XOR
+#define UCP_MEAN_XOR 1  // 0: replicas compared with the branchy diff4 per vector
+#endif
 #ifndef UCP_MEAN_LEAN
 #define UCP_MEAN_LEAN 1  // 0: MEAN vector runs through the generic op_run
 #endif
@@ -472,8 +497,14 @@ __device__ __forceinline__ void mean_vec_slot(const Ctx& c, uint64_t srow, uint6
           a2 = __dadd_rn(a2, (double)prim.z); a3 = __dadd_rn(a3, (double)prim.w);
         }
       } else {
-        const int d = diff4(prim, q[j]);
-        if (d < 4) { bad = true; bad_e = min(bad_e, e + d); }
+#if UCP_MEAN_XOR
+        if (xor4(prim, q[j]) != 0u) {
+#endif
+          const int d = diff4(prim, q[j]);
+          if (d < 4) { bad = true; bad_e = min(bad_e, e + d); }
+#if UCP_MEAN_XOR
+        }
+#endif
       }
       if (++k == K) k = 0;
     }
@@ -512,15 +543,28 @@ __device__ __forceinline__ void noise_vec_segment(const Ctx& c, uint64_t srow, u
     for (int u = 0; u < kVec; ++u) {
       const uint32_t vi = lane + 32u * u;
       if (vi >= nvec) continue;
-      const int d = diff4(v[u], ld_stream4(sk + 16ull * vi));
-      if (d < 4) { bad = true; bad_e = min(bad_e, head + 4u * vi + d); }
+      const float4 w = ld_stream4(sk + 16ull * vi);
+      if (xor4(v[u], w) != 0u) {
+        bad = true;
+        bad_e = min(bad_e, head + 4u * vi + (uint32_t)diff4(v[u], w));
+      }
     }
   }
+#if UCP_NOISE_INT
+  const uint32_t ns = ucp_noise_steps(r.tp_rank, r.tp), odd = (uint32_t)r.tp_rank & 1u;
+  if (ns != 0u) {  // uniform per run
+    auto nz = [&](float x) { return float_of(ucp_noise_bits(bits_of(x), ns, odd)); };
+#pragma unroll
+    for (int u = 0; u < kVec; ++u)
+      v[u] = make_float4(nz(v[u].x), nz(v[u].y), nz(v[u].z), nz(v[u].w));
+  }
+#else
   const int t = r.tp_rank, tp = r.tp;
 #pragma unroll
   for (int u = 0; u < kVec; ++u)
     v[u] = make_float4(noise1(v[u].x, t, tp), noise1(v[u].y, t, tp), noise1(v[u].z, t, tp),
                        noise1(v[u].w, t, tp));
+#endif
   const int esz = r.dtype == UCP_DT_F32 ? 4 : 2;
   for (int d = 0; d < r.n_dst; ++d) {
     char* dp = c.db + dst_off(c, d) + (uint64_t)esz * (drow + head);

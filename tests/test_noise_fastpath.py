@@ -1,14 +1,31 @@
-"""A numpy model of the partial-noise kernel's fast path (noise1 in
-csrc/ucp_b200.cu: `steps` nextafter steps done as +-steps on the bit pattern
-when they cross neither zero nor +-inf, the reference's nextafter loop
-otherwise) against the oracle restatement of ucp/parallel.py:340-370, on every
-exponent's edge mantissas, the neighbourhoods of zero and of the largest
-finite value, and random bit patterns, for every rank of tp up to 16. The GPU
-kernel itself is checked against the reference's own tables and the same
-edges in tests/test_gpu_parity.py."""
+"""Partial noise (ucp/parallel.py:340-370) as the kernels compute it.
+
+* The branch-free integer form the OPS kernels run (ucp_noise_bits in
+  csrc/ucp_noise.h, compiled here by g++ from the same header) against a C
+  restatement of the reference (nextafterf stepping + the f64 pair test):
+  dense over the zero / subnormal / first-normal range and the top binade of
+  both signs, strided over the rest, for every step count up to 8 (every rank
+  of tp <= 16). tools/noise_exhaustive.cpp run without a stride covers all
+  2^32 patterns (profiles/noise_exhaustive_r02.log: 68.7 G cases, 0
+  mismatches).
+* A numpy model of the previous fast path (UCP_NOISE_INT=0: `steps` nextafter
+  steps as +-steps on the bit pattern when they cross neither zero nor +-inf,
+  the nextafter loop otherwise) against the oracle restatement, on every
+  exponent's edge mantissas, the neighbourhoods of zero and of the largest
+  finite value, and random bit patterns, for every rank of tp up to 16.
+
+The GPU kernel itself is checked against the reference's own tables and the
+same edges in tests/test_gpu_parity.py."""
+
+import json
+import os
+import shutil
+import subprocess
 
 import numpy as np
 import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 from oracle import ucp_oracle as O
 
@@ -65,3 +82,28 @@ def test_noise_fast_path_model_matches_oracle(tp):
         with np.errstate(all="ignore"):
             want = O.partial_noise(x, t, tp).view(np.uint32)
         assert np.array_equal(_kernel_model(u, t, tp), want), (tp, t)
+
+
+@pytest.fixture(scope="module")
+def noise_ex(tmp_path_factory):
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    exe = str(tmp_path_factory.mktemp("noise") / "noise_ex")
+    subprocess.run(["g++", "-O2", "-fopenmp", "-std=c++17",
+                    os.path.join(ROOT, "tools", "noise_exhaustive.cpp"), "-o", exe], check=True)
+    return exe
+
+
+@pytest.mark.parametrize("rng", [
+    (1, 0, 1 << 25),                        # +0, subnormals, first two normal binades
+    (1, 0x7E800000, 0x80000000 + (1 << 25)),  # top binades, inf, NaN, -0, negative subnormals
+    (1, 0xFE800000, 1 << 32),               # negative top binades, -inf, negative NaN
+    (65521, 0, 1 << 32),                    # every region, strided
+])
+def test_integer_noise_matches_reference_restatement(noise_ex, rng):
+    stride, lo, hi = rng
+    out = subprocess.run([noise_ex, "8", str(stride), str(lo), str(hi)], capture_output=True,
+                         text=True, timeout=300)
+    res = json.loads(out.stdout)
+    assert out.returncode == 0 and res["mismatches"] == 0, res
+    assert res["checked"] > 0
