@@ -97,6 +97,51 @@ def test_mean_kernel_recovers_noised_partials(golden_arrays):
         assert np.array_equal(back.view(np.uint32), x.view(np.uint32)), tp
 
 
+def _adversarial_pairs(n: int, seed: int):
+    """f32 pairs at the edges of a two-group f64 MEAN: random patterns, partners at every exponent gap 0..40 (the f64 sum stops
+    being exact past 28), near-cancellation, sums that overflow f32 while
+    their half does not, and sums in the subnormal / 2^-124 range. Non-finite
+    inputs are left out (NaN payload rules are not part of the reference's
+    Partial data)."""
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    mode = rng.integers(0, 8, n)
+    gap = rng.integers(0, 41, n).astype(np.int64)
+    eb = np.maximum(((a >> 23) & 0xFF).astype(np.int64) - gap, 0).astype(np.uint32)
+    m = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    near = ((m & 1) << 31) | (eb << 23) | ((m >> 9) & 0x7FFFFF)
+    b = np.where(mode >= 3, near, b)
+    b = np.where(mode == 7, a ^ np.uint32(0x80000000) ^ ((m >> 3) & 7), b)
+    big = np.uint32(0x7F000000) | (m & 0x7FFFFF)           # overflow: both ~2^127, same sign
+    a = np.where(mode == 6, big, a)
+    b = np.where(mode == 6, big ^ (m & 0xFF), b)
+    tiny = (m & 0x00FFFFFF)                                 # subnormal / first normal binades
+    a = np.where(mode == 5, tiny | ((m & 2) << 30), a)
+    b = np.where(mode == 5, (tiny >> 3) | ((m & 4) << 29), b)
+    a, b = a.astype(np.uint32), b.astype(np.uint32)
+    fin = lambda u: (u & 0x7F800000) != 0x7F800000  # noqa: E731
+    keep = fin(a) & fin(b)
+    return a[keep].view(np.float32), b[keep].view(np.float32)
+
+
+@pytest.mark.parametrize("dp", [1, 2])
+def test_mean_two_groups_adversarial_matches_oracle(dp):
+    """Two-group MEAN (tp = 2 Partial sources) against the oracle's f64 mean
+    (ucp/convert.py:279-284) on adversarial pairs, bit for bit. (An f32 form
+    of the two-group mean, exact where RN32(a + b) is finite and >= 2^-124,
+    was measured slower than the f64 sum and not kept: ops_ab_r02.log r02zb.)"""
+    a, b = _adversarial_pairs(1 << 20, 11 + dp)
+    n = a.size
+    p = ParamSpec("pos.alibi", (n,), 0, ParamKind.ASYNC_PARTIAL)
+    c = cfg(tp=2, dp=dp)
+    msgs = [U.FragmentMsg(_m(p, kind="m", pattern="partial", placement=(0, t, d)), x)
+            for t, x in enumerate((a, b)) for d in range(dp)]
+    got = U.union(p, c, msgs)
+    want = O.union(p, c, [(m.meta, m.data) for m in msgs])
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
 def _m(p, kind="weight", pattern="replicate", placement=(0, 0, 0), shape=None, segments=None,
        flat_range=None, pad_elems=0):
     return RecordMeta(p.name, kind, pattern, placement, shape if shape is not None else p.shape,
