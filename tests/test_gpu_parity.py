@@ -66,16 +66,16 @@ def test_noise_kernel_matches_reference_tables(golden_arrays, tp):
 
 def test_noise_kernel_binade_edges_match_oracle():
     """Every exponent's first and last few mantissas (both signs), where the
-    nextafter steps cross a binade, the subnormal boundary, zero or inf:
-    the branch-free fast path and the step loop of noise1 must agree with
-    the reference formula (oracle restatement of ucp/parallel.py:340-370)."""
-    m = np.array([0, 1, 2, 3, 4, 5, 0x7FFFFA, 0x7FFFFB, 0x7FFFFC, 0x7FFFFD, 0x7FFFFE, 0x7FFFFF],
-                 dtype=np.uint32)
+    nextafter steps cross a binade, the subnormal boundary, zero or inf, for
+    up to 8 steps (tp 16): the kernel's integer noise (csrc/ucp_noise.h) must
+    agree with the reference formula (oracle restatement of
+    ucp/parallel.py:340-370)."""
+    m = np.concatenate([np.arange(0, 10), np.arange(0x7FFFF6, 0x800000)]).astype(np.uint32)
     bits = ((np.arange(256, dtype=np.uint32)[:, None] << 23) | m[None, :]).reshape(-1)
     bits = np.concatenate([bits, bits | np.uint32(0x80000000)])
     x = bits.view(np.float32)
     p = ParamSpec("pos.alibi", (x.size,), 0, ParamKind.ASYNC_PARTIAL)
-    for tp in (2, 7, 8):
+    for tp in (2, 7, 8, 16):
         c = cfg(tp=tp)
         for t in range(tp):
             meta = RecordMeta(p.name, "weight", "partial", (0, t, 0), p.shape)
