@@ -30,6 +30,28 @@
 #define UCP_NOISE_HD static inline
 #endif
 
+#ifndef UCP_NOISE_V2
+#define UCP_NOISE_V2 1  // 0: the first integer form (r02za), kept for A/B
+#endif
+
+#if UCP_NOISE_V2
+// Fewer operations, same function: a - 1 < 0x7f7fffff - s (unsigned) is
+// a != 0 && a + s < 0x7f800000 in one compare; a - s may wrap when the steps
+// cross zero (a < s), which the m2 < 2^24 clause covers; the kept pattern is
+// u -+ s, except towards zero across it: opposite sign, magnitude s - a.
+UCP_NOISE_HD uint32_t ucp_noise_bits(uint32_t u, uint32_t s, uint32_t odd) {
+  const uint32_t a = u & 0x7fffffffu;
+  const uint32_t am1 = a - 1u;
+  const uint32_t m2 = am1 + s;
+  const bool same = (((a - s) ^ m2) < 0x00800000u) || (m2 < 0x01000000u);
+  const bool ok = (am1 < 0x7f7fffffu - s) && same;
+  const bool tw = ((u >> 31) ^ odd) != 0u;  // towards zero
+  const uint32_t step = tw ? u - s : u + s;
+  const uint32_t cross = ((u & 0x80000000u) ^ 0x80000000u) + (s - a);
+  const uint32_t chosen = (tw && a < s) ? cross : step;
+  return ok ? chosen : u;
+}
+#else
 UCP_NOISE_HD uint32_t ucp_noise_bits(uint32_t u, uint32_t s, uint32_t odd) {
   const uint32_t a = u & 0x7fffffffu;
   const uint32_t sgn = u & 0x80000000u;
@@ -44,6 +66,7 @@ UCP_NOISE_HD uint32_t ucp_noise_bits(uint32_t u, uint32_t s, uint32_t odd) {
   const uint32_t chosen = tw ? toward : away;
   return ok ? chosen : u;
 }
+#endif
 
 // The per-run constants of ucp_noise_bits: s (steps) and odd, or s = 0 when
 // the run leaves every element unchanged.
