@@ -521,6 +521,9 @@ __device__ __forceinline__ void mean_vec_slot(const Ctx& c, uint64_t srow, uint6
 #ifndef UCP_NOISE_LEAN
 #define UCP_NOISE_LEAN 1  // 0: NOISE vector runs through the generic op_run
 #endif
+#ifndef UCP_NOISE_F32STORE
+#define UCP_NOISE_F32STORE 1  // 1: f32 NOISE destinations stored by a loop without the dtype switch
+#endif
 
 // NOISE of a vector run's segment (ucp/parallel.py:340-370 per element): each
 // lane's kVec slots of the primary are loaded together, replicas (if any)
@@ -564,6 +567,19 @@ __device__ __forceinline__ void noise_vec_segment(const Ctx& c, uint64_t srow, u
   for (int u = 0; u < kVec; ++u)
     v[u] = make_float4(noise1(v[u].x, t, tp), noise1(v[u].y, t, tp), noise1(v[u].z, t, tp),
                        noise1(v[u].w, t, tp));
+#endif
+#if UCP_NOISE_F32STORE
+  if (r.dtype == UCP_DT_F32) {  // uniform per run: f32 targets (Adam moments, f32 weights)
+    for (int d = 0; d < r.n_dst; ++d) {
+      char* dp = c.db + dst_off(c, d) + 4ull * (drow + head);
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        const uint32_t vi = lane + 32u * u;
+        if (vi < nvec) st4(dp + 16ull * vi, v[u]);
+      }
+    }
+    return;
+  }
 #endif
   const int esz = r.dtype == UCP_DT_F32 ? 4 : 2;
   for (int d = 0; d < r.n_dst; ++d) {
